@@ -1,0 +1,201 @@
+/*
+ * wpk.h -- C ABI of the B200-native Woodpecker-DL hot path (libwpk.so).
+ *
+ * The operation (§2.2 Halide listing; PAPER.md:15 and SPEC.md:136 for the fused
+ * epilogue): forward 2-D convolution for inference,
+ *
+ *   y[n,k,p,q] = act( b[k] + sum_{c<C/g, r<R, s<S}
+ *                     x[n, g(k)*C/g + c, p*stride_h - pad_h + r*dil_h, q*stride_w - pad_w + s*dil_w]
+ *                     * w[k, c, r, s] ),           act = ReLU | identity,  x = 0 outside the image,
+ *   P = floor((H + 2 pad_h - dil_h (R-1) - 1)/stride_h) + 1   (same for Q with W, S),
+ *
+ * together with the per-layer search that picks the kernel configuration ("identify most efficient
+ * codes per operator"; GA §2.3; RL-search §2.4).
+ *
+ * Conventions
+ *  - Every call returns wpk_status; no C++ exception crosses the ABI. On error a human-readable
+ *    message is available from wpk_last_error() (thread-local; valid until the next call on the
+ *    same thread).
+ *  - Device pointers are CUDA device pointers on the plan's device (allocated by the caller, e.g.
+ *    by PyTorch). Host pointers are plain process memory. Nothing here takes a torch type.
+ *  - Layouts (dense, row-major in the order given):
+ *      WPK_NCHW: x [N][C][H][W],  w [K][C/g][R][S] (KCRS),  y [N][K][P][Q]
+ *      WPK_NHWC: x [N][H][W][C],  w [K][R][S][C/g] (KRSC),  y [N][P][Q][K]
+ *      b [K] (or NULL iff epilogue == WPK_EPI_NONE).
+ *  - dtypes: x, w, b, y share one element type:
+ *      WPK_F32  float32, exact fp32 FMA on CUDA cores (strict-comparison path)
+ *      WPK_TF32 float32 in/out, tf32 tensor-core products, fp32 accumulate
+ *      WPK_BF16 bfloat16 in/out, fp32 accumulate;  WPK_F16 float16 in/out, fp32 accumulate.
+ *    The accumulator is fp32; bias is up-converted to fp32 and added before ReLU; the output is
+ *    rounded to nearest-even once.
+ */
+#ifndef WPK_H
+#define WPK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define WPK_API __attribute__((visibility("default")))
+#else
+#define WPK_API
+#endif
+
+#define WPK_ABI_VERSION 1
+#define WPK_NUM_GENES 7
+
+typedef enum {
+    WPK_OK = 0,
+    WPK_ERR_INVALID_ARGUMENT = 1, /* NULL / misaligned pointer, bad enum, bad option value     */
+    WPK_ERR_SHAPE = 2,            /* any dim < 1, P or Q < 1, C % g != 0, K % g != 0            */
+    WPK_ERR_UNSUPPORTED = 3,      /* groups not in {1, C==K}; device not sm_100                 */
+    WPK_ERR_INVALID_CONFIG = 4,   /* genes outside the family's space or violating a constraint */
+    WPK_ERR_EXHAUSTED = 5,        /* no valid config could be sampled / every candidate failed  */
+    WPK_ERR_CUDA = 6,             /* CUDA runtime/driver error (message in wpk_last_error)      */
+    WPK_ERR_OUT_OF_MEMORY = 7,    /* workspace too small / allocation failure                   */
+    WPK_ERR_INTERNAL = 8          /* broken invariant (e.g. ranks disagree on the chosen config) */
+} wpk_status;
+
+typedef enum { WPK_F32 = 0, WPK_TF32 = 1, WPK_BF16 = 2, WPK_F16 = 3 } wpk_dtype;
+typedef enum { WPK_NCHW = 0, WPK_NHWC = 1 } wpk_layout;
+typedef enum { WPK_EPI_NONE = 0, WPK_EPI_BIAS = 1, WPK_EPI_BIAS_RELU = 2 } wpk_epilogue;
+typedef enum { WPK_SEARCH_GA = 0, WPK_SEARCH_RL = 1, WPK_SEARCH_RANDOM = 2 } wpk_search;
+typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 2 } wpk_eval_mode;
+
+/* Kernel families ("schedule templates"). Each has 7 genes (PAPER.md:65 chromosome
+ * s = {c_0..c_6}); their meaning per family is listed by wpk_family_describe().
+ *   WPK_FAMILY_SIMT : direct conv on CUDA cores, genes = the paper's
+ *                     (T_x, T_y, T_z, Tile_x, Tile_y, Tile_z, Tile_rz), T_x*T_y*T_z<=1024
+ *   WPK_FAMILY_UMMA : tcgen05 implicit GEMM, genes = (BLOCK_N, STAGES, SPLIT_K, RASTER,
+ *                     CTAS_PER_SM, ACC_STAGES, BLOCK_M)
+ *   WPK_FAMILY_DW   : depthwise (groups == C == K), genes = (VEC_C, PIX_PER_THREAD, THREADS,
+ *                     ROWS_PER_CTA, -, -, -)                                                      */
+typedef enum { WPK_FAMILY_SIMT = 0, WPK_FAMILY_UMMA = 1, WPK_FAMILY_DW = 2, WPK_FAMILY_AUTO = -1 } wpk_family;
+
+/* Operator shape: the first 9 entries of the paper's O_conv generalised with
+ * explicit symmetric padding, dilation and groups (reading c2, c4). */
+typedef struct {
+    uint32_t struct_size; /* = sizeof(wpk_conv2d_shape) */
+    int32_t n, c, h, w, k, r, s;
+    int32_t stride_h, stride_w, pad_h, pad_w, dil_h, dil_w, groups;
+    int32_t layout;   /* wpk_layout   */
+    int32_t epilogue; /* wpk_epilogue */
+} wpk_conv2d_shape;
+
+/* All-gather of `bytes_per_rank` bytes from every rank: recv[r*bytes_per_rank ...] = send of rank
+ * r. Must be called collectively by every rank in the same order. Return 0 on success. Used by
+ * wpk_conv2d_tune to share fitness records when candidate evaluation is sharded over GPUs
+ * (BASELINE.json north_star: "an NCCL all-gather of fitness values"). */
+typedef int (*wpk_exchange_fn)(void *ctx, const void *send, size_t bytes_per_rank, void *recv);
+
+typedef struct {
+    uint32_t struct_size;     /* = sizeof(wpk_tune_options); fill with wpk_tune_options_init */
+    uint64_t seed;            /* counter-RNG seed (default 0)                                   */
+    int32_t rank, world;      /* this process's rank and the number of ranks (default 0, 1)    */
+    wpk_exchange_fn exchange; /* required when world > 1                                        */
+    void *exchange_ctx;
+    int32_t warmup, reps;     /* timing protocol: W untimed + R event-timed reps, median (3, 11) */
+    int32_t l2_flush;         /* 1: overwrite a >= 2x L2 buffer before every timed rep (default) */
+    int32_t eval_mode;        /* wpk_eval_mode (default MEASURED)                               */
+    int32_t family;           /* wpk_family to search; WPK_FAMILY_AUTO = the plan's default      */
+    const char *record_path;  /* if set: append every measured record as JSONL                  */
+    const char *replay_path;  /* if set with EVAL_REPLAY: read records instead of measuring     */
+    const char *log_path;     /* if set: per-generation (GA) / per-step (RL) history JSONL      */
+    double synthetic[1 + 2 * WPK_NUM_GENES]; /* EVAL_SYNTHETIC: base, w[7], c*[7] */
+    /* GA (defaults per DESIGN.md reading c15) */
+    int32_t ga_pop, ga_elites, ga_pool, ga_max_gen;
+    double ga_mutation, ga_eps;
+    /* PPO (defaults per DESIGN.md readings c21-c24) */
+    int32_t rl_envs, rl_horizon, rl_epochs, rl_minibatch;
+    double rl_gamma, rl_mu, rl_clip, rl_c1, rl_c2, rl_lr, rl_keep_prob;
+    int32_t rl_hidden[4];     /* 512, 1024, 1024, 512                                          */
+    int32_t rl_alpha_mode;    /* 0 = the paper's alpha_t = (0.8 alpha + beta)/t, 1 = EMA        */
+    int32_t max_seconds;      /* wall-clock cap for one tune (0 = none)                         */
+} wpk_tune_options;
+
+typedef struct wpk_plan_s *wpk_plan;
+
+/* Fill defaults (seed 0, rank 0, world 1, W=3, R=11, L2 flush, measured, GA 48/4/48/50/0.1/0.02,
+ * PPO E=1 T=64 epochs 4 minibatch 16 gamma .99 mu .95 clip .2 c1 .15 c2 20 lr 1e-4 keep .85). */
+WPK_API void wpk_tune_options_init(wpk_tune_options *opts);
+
+/* Output spatial size (host only; no device needed). WPK_ERR_SHAPE if P or Q < 1. */
+WPK_API wpk_status wpk_conv2d_output_dims(const wpk_conv2d_shape *shape, int32_t *p, int32_t *q);
+
+/* Validate the shape, form the implicit-GEMM view, choose the kernel family for (dtype, groups,
+ * alignment) and a deterministic valid default config. Host only: no CUDA call is made until the
+ * first run/tune. `device` is the CUDA ordinal the plan will run on. *out owns host state only. */
+WPK_API wpk_status wpk_conv2d_plan(const wpk_conv2d_shape *shape, wpk_dtype dtype, int device, wpk_plan *out);
+
+/* Search the plan's configuration space with GA / RL / random search, at most `budget` distinct
+ * measured configs; on success the best config found becomes the plan's config. A candidate that
+ * fails (launch error, invalid) scores beta = +inf and is recorded, not returned; returns
+ * WPK_ERR_EXHAUSTED only if every candidate failed. With EVAL_REPLAY / EVAL_SYNTHETIC no GPU is
+ * touched and the result is a pure function of (shape, dtype, search, budget, seed, records),
+ * identical for every world size. opts may be NULL (defaults). */
+WPK_API wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t budget, const wpk_tune_options *opts);
+
+/* Run the convolution on `stream` (a cudaStream_t; NULL = legacy default stream). Asynchronous:
+ * no host synchronisation, no allocation once a workspace is set. Pointers must be 16-byte
+ * aligned device pointers laid out as described above. Packed weights are cached per w pointer
+ * (weights are inference constants); after mutating w in place call
+ * wpk_conv2d_invalidate. One stream at a time per plan. */
+WPK_API wpk_status wpk_conv2d_run(wpk_plan plan, const void *x, const void *w, const void *b, void *y, void *stream);
+
+/* Same as run, but x and y are HOST pointers: copies x host->device, runs, copies y back, all on
+ * `stream`, then synchronises the stream. Device staging buffers live in the workspace. */
+WPK_API wpk_status wpk_conv2d_run_host(wpk_plan plan, const void *x_host, const void *w, const void *b,
+                               void *y_host, void *stream);
+
+WPK_API void wpk_conv2d_destroy(wpk_plan plan);
+WPK_API const char *wpk_last_error(void);
+
+/* Workspace: bytes the current config needs (layout transform, channel pad, packed weights,
+ * split-K partials, host-run staging). The caller may provide it (e.g. a torch tensor); if never
+ * set, the plan allocates and owns one on first run. set_workspace with a too-small buffer ->
+ * WPK_ERR_OUT_OF_MEMORY. */
+WPK_API wpk_status wpk_conv2d_workspace_size(wpk_plan plan, size_t *bytes);
+WPK_API wpk_status wpk_conv2d_set_workspace(wpk_plan plan, void *dev_ptr, size_t bytes);
+
+/* Current config: *family and genes[0..6]. set_config validates (WPK_ERR_INVALID_CONFIG). */
+WPK_API wpk_status wpk_conv2d_get_config(wpk_plan plan, int32_t *family, int32_t *genes);
+WPK_API wpk_status wpk_conv2d_set_config(wpk_plan plan, int32_t family, const int32_t *genes);
+/* 1 if (family, genes) is valid for this plan, else 0 (and the reason in wpk_last_error). */
+WPK_API int32_t wpk_conv2d_config_valid(wpk_plan plan, int32_t family, const int32_t *genes);
+
+/* Drop the packed-weight / tensor-map caches (call after mutating weights in place). */
+WPK_API wpk_status wpk_conv2d_invalidate(wpk_plan plan);
+
+/* Describe a family's gene domains: for gene g, domain values are written to
+ * values[g*32 .. g*32+counts[g]-1] (at most 32 per gene). names may be NULL. */
+WPK_API wpk_status wpk_family_describe(int32_t family, int32_t *counts, int32_t *values, const char **names);
+
+/* Number of kernel launches the last wpk_conv2d_run issued on its stream (for bench accounting). */
+WPK_API int32_t wpk_conv2d_last_launch_count(wpk_plan plan);
+
+/* Tuning history of the last tune: best beta (us), number of distinct measured configs,
+ * generations/steps, wall seconds. */
+WPK_API wpk_status wpk_conv2d_tune_stats(wpk_plan plan, double *best_us, int32_t *measured, int32_t *rounds,
+                                 double *seconds);
+
+/* RL-search learner primitives, exported so the C++ learner can be checked against the oracle
+ * (tests/test_tuner_parity.py). dims[0..5] = {obs, h1, h2, h3, h4, A+1}. params is the flat
+ * concatenation of (W1[h1][obs], b1, ..., W5[A+1][h4], b5) in float64. Computes the PPO loss
+ * -L and its gradient for one batch; mask (B x h4, or NULL) is the dropout mask. */
+WPK_API wpk_status wpk_ppo_loss_grad(const int32_t *dims, const double *params, int32_t batch, const double *obs,
+                             const int32_t *actions, const double *old_logp, const double *adv,
+                             const double *v_old, const double *consts /* c1, c2, clip */,
+                             const double *mask, double keep, double *loss, double *grad);
+/* GAE by backward recursion: adv[T] from r[T], v[T+1]. */
+WPK_API wpk_status wpk_gae(int32_t T, const double *r, const double *v, double gamma, double mu, double *adv);
+/* Observation O_conv with the feature scaling of DESIGN.md reading c24b. */
+WPK_API wpk_status wpk_observation(const wpk_conv2d_shape *shape, const int32_t *genes, double alpha_us, double *obs17);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WPK_H */

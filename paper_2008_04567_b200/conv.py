@@ -1,0 +1,174 @@
+"""Python face of the C ABI: a per-layer plan object that marshals torch tensors to
+wpk_conv2d_run / wpk_conv2d_tune. Every step of the convolution runs in libwpk.so kernels; torch
+only allocates device memory and provides streams (BASELINE.json north_star).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+
+_TORCH_DT = {"f32": torch.float32, "tf32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}
+
+
+def output_dims(n, c, h, w, k, r, s, stride=1, pad=0, dil=1, groups=1):
+    lib = L.load()
+    shp = L.make_shape(n, c, h, w, k, r, s, stride, pad, dil, groups)
+    p, q = ctypes.c_int32(), ctypes.c_int32()
+    L.check(lib.wpk_conv2d_output_dims(ctypes.byref(shp), ctypes.byref(p), ctypes.byref(q)))
+    return p.value, q.value
+
+
+@dataclass
+class TuneResult:
+    family: int
+    genes: list
+    best_us: float
+    measured: int
+    rounds: int
+    seconds: float
+
+
+class Conv2dPlan:
+    """wpk_conv2d_plan + run/tune for one convolution layer.
+
+    Layouts: "nchw" -> x [N,C,H,W], w [K,C/g,R,S], y [N,K,P,Q];  "nhwc" -> x [N,H,W,C],
+    w [K,R,S,C/g], y [N,P,Q,K] (dense tensors, i.e. a permuted channels_last tensor must be made
+    contiguous in that order)."""
+
+    def __init__(self, n, c, h, w, k, r, s, stride=1, pad=0, dil=1, groups=1, layout="nchw",
+                 epilogue="bias_relu", dtype="bf16", device: int | None = None):
+        self.lib = L.load()
+        self.dtype, self.layout, self.epilogue = dtype, layout, epilogue
+        self.device = torch.cuda.current_device() if device is None else device
+        self.shape = L.make_shape(n, c, h, w, k, r, s, stride, pad, dil, groups, layout, epilogue)
+        self.n, self.c, self.h, self.w, self.k, self.r, self.s = n, c, h, w, k, r, s
+        self.groups = groups
+        h_ = ctypes.c_void_p()
+        L.check(self.lib.wpk_conv2d_plan(ctypes.byref(self.shape), L.DTYPES[dtype], self.device, ctypes.byref(h_)))
+        self.handle = h_
+        self.p, self.q = output_dims(n, c, h, w, k, r, s, stride, pad, dil, groups)
+        self._ws = None
+        self._ws_bytes = -1
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            self.lib.wpk_conv2d_destroy(h)
+            self.handle = None
+
+    # -- config ----------------------------------------------------------------------------------
+    @property
+    def config(self):
+        fam = ctypes.c_int32()
+        genes = (ctypes.c_int32 * L.NUM_GENES)()
+        L.check(self.lib.wpk_conv2d_get_config(self.handle, ctypes.byref(fam), genes))
+        return fam.value, list(genes)
+
+    def set_config(self, family, genes):
+        fam = L.FAMILIES[family] if isinstance(family, str) else int(family)
+        arr = (ctypes.c_int32 * L.NUM_GENES)(*genes)
+        L.check(self.lib.wpk_conv2d_set_config(self.handle, fam, arr))
+        self._ws_bytes = -1
+
+    def config_valid(self, family, genes) -> bool:
+        fam = L.FAMILIES[family] if isinstance(family, str) else int(family)
+        arr = (ctypes.c_int32 * L.NUM_GENES)(*genes)
+        return bool(self.lib.wpk_conv2d_config_valid(self.handle, fam, arr))
+
+    def workspace_bytes(self) -> int:
+        b = ctypes.c_size_t()
+        L.check(self.lib.wpk_conv2d_workspace_size(self.handle, ctypes.byref(b)))
+        return b.value
+
+    def _ensure_workspace(self):
+        need = self.workspace_bytes()
+        if need != self._ws_bytes:
+            self._ws = torch.empty(max(need, 16), dtype=torch.uint8, device=f"cuda:{self.device}")
+            L.check(self.lib.wpk_conv2d_set_workspace(self.handle, ctypes.c_void_p(self._ws.data_ptr()), need))
+            self._ws_bytes = need
+
+    # -- shapes ----------------------------------------------------------------------------------
+    def x_shape(self):
+        return (self.n, self.c, self.h, self.w) if self.layout == "nchw" else (self.n, self.h, self.w, self.c)
+
+    def w_shape(self):
+        cpg = self.c // self.groups
+        return (self.k, cpg, self.r, self.s) if self.layout == "nchw" else (self.k, self.r, self.s, cpg)
+
+    def y_shape(self):
+        return (self.n, self.k, self.p, self.q) if self.layout == "nchw" else (self.n, self.p, self.q, self.k)
+
+    # -- run -------------------------------------------------------------------------------------
+    def run(self, x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, y: torch.Tensor | None = None,
+            stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        dt = _TORCH_DT[self.dtype]
+        for t, nm, shp in ((x, "x", self.x_shape()), (w, "w", self.w_shape())):
+            if t.dtype != dt or tuple(t.shape) != shp or not t.is_contiguous() or not t.is_cuda:
+                raise ValueError(f"{nm}: expected contiguous cuda {dt} of shape {shp}, got {t.dtype} {tuple(t.shape)}")
+        if y is None:
+            y = torch.empty(self.y_shape(), dtype=dt, device=x.device)
+        self._ensure_workspace()
+        s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
+        bp = ctypes.c_void_p(b.data_ptr()) if b is not None else None
+        L.check(self.lib.wpk_conv2d_run(self.handle, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                        bp, ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(s)))
+        return y
+
+    def run_host(self, x_host: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, y_host: torch.Tensor,
+                 stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """x_host/y_host are (pinned) CPU tensors; H2D + conv + D2H inside, then stream sync."""
+        self._ensure_workspace()
+        s = (stream or torch.cuda.current_stream(w.device)).cuda_stream
+        bp = ctypes.c_void_p(b.data_ptr()) if b is not None else None
+        L.check(self.lib.wpk_conv2d_run_host(self.handle, ctypes.c_void_p(x_host.data_ptr()),
+                                             ctypes.c_void_p(w.data_ptr()), bp,
+                                             ctypes.c_void_p(y_host.data_ptr()), ctypes.c_void_p(s)))
+        return y_host
+
+    def last_launch_count(self) -> int:
+        return int(self.lib.wpk_conv2d_last_launch_count(self.handle))
+
+    def invalidate(self):
+        L.check(self.lib.wpk_conv2d_invalidate(self.handle))
+
+    # -- tune ------------------------------------------------------------------------------------
+    def tune(self, search: str = "ga", budget: int = 64, opts: L.TuneOptions | None = None, **kw) -> TuneResult:
+        o = opts if opts is not None else make_options(**kw)
+        L.check(self.lib.wpk_conv2d_tune(self.handle, L.SEARCHES[search], int(budget), ctypes.byref(o)))
+        self._ws_bytes = -1
+        return self.tune_stats()
+
+    def tune_stats(self) -> TuneResult:
+        best, secs = ctypes.c_double(), ctypes.c_double()
+        meas, rounds = ctypes.c_int32(), ctypes.c_int32()
+        L.check(self.lib.wpk_conv2d_tune_stats(self.handle, ctypes.byref(best), ctypes.byref(meas),
+                                               ctypes.byref(rounds), ctypes.byref(secs)))
+        fam, genes = self.config
+        return TuneResult(fam, genes, best.value, meas.value, rounds.value, secs.value)
+
+
+def make_options(**kw) -> L.TuneOptions:
+    """wpk_tune_options with defaults, overridden by keyword arguments (field names of wpk.h)."""
+    o = L.TuneOptions()
+    L.load().wpk_tune_options_init(ctypes.byref(o))
+    keep = []
+    for k, v in kw.items():
+        if k in ("record_path", "replay_path", "log_path"):
+            v = v.encode() if v is not None else None
+            keep.append(v)
+        elif k == "eval_mode" and isinstance(v, str):
+            v = L.EVAL_MODES[v]
+        elif k == "family" and isinstance(v, str):
+            v = L.FAMILIES[v]
+        elif k == "synthetic":
+            arr = (ctypes.c_double * (1 + 2 * L.NUM_GENES))(*v)
+            v = arr
+        elif k == "rl_hidden":
+            v = (ctypes.c_int32 * 4)(*v)
+        setattr(o, k, v)
+    o._keep = keep
+    return o

@@ -1,0 +1,22 @@
+// Depthwise convolution (KB3) host interface.
+#pragma once
+#include <string>
+
+#include "wpk_internal.h"
+
+namespace wpk {
+
+struct DwArgs {
+    const void *x, *w, *b;   // w packed [R][S][C]
+    void *y;
+    int N, C, H, W, R, S, P, Q;
+    int sh, sw, ph, pw, dh, dw;
+    long long xs_n, xs_c, xs_h, xs_w;
+    long long ys_n, ys_c, ys_p, ys_q;
+    int epilogue;
+};
+
+int dw_launch(const DwArgs &a, int dtype, int vec, int pix, int threads, int sm_count, void *stream,
+              std::string *err);
+
+}  // namespace wpk

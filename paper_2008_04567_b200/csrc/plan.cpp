@@ -1,0 +1,359 @@
+// Plan creation, shape validation, schedule templates (gene spaces) and config validity.
+//
+// Shape rules: SURVEY.md §8(b) "Validation -> errors"; output size P/Q: floor formula (reading c3).
+// Schedule templates with tunable hyper-parameters: PAPER.md:59 (§2.2); chromosome encoding
+// s = {c_0..c_{n-1}}: PAPER.md:64-65; "verified first in order to meet certain constraints ...
+// the product of all dimension values is positive and <= 1024": PAPER.md:68.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "wpk_internal.h"
+
+namespace wpk {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+wpk_status fail(wpk_status st, const std::string &msg) {
+    g_last_error = msg;
+    return st;
+}
+
+static int out_size(int in, int pad, int dil, int f, int stride) {
+    long long num = (long long)in + 2LL * pad - (long long)dil * (f - 1) - 1;
+    if (num < 0) return 0;
+    return (int)(num / stride + 1);
+}
+
+static wpk_status to_desc(const wpk_conv2d_shape *s, int dtype, ConvDesc *d) {
+    if (!s) return fail(WPK_ERR_INVALID_ARGUMENT, "shape is NULL");
+    if (s->struct_size != sizeof(wpk_conv2d_shape))
+        return fail(WPK_ERR_INVALID_ARGUMENT, "wpk_conv2d_shape.struct_size mismatch (ABI version)");
+    if (dtype < WPK_F32 || dtype > WPK_F16) return fail(WPK_ERR_INVALID_ARGUMENT, "bad dtype");
+    if (s->layout != WPK_NCHW && s->layout != WPK_NHWC) return fail(WPK_ERR_INVALID_ARGUMENT, "bad layout");
+    if (s->epilogue < WPK_EPI_NONE || s->epilogue > WPK_EPI_BIAS_RELU)
+        return fail(WPK_ERR_INVALID_ARGUMENT, "bad epilogue");
+    const int dims[] = {s->n, s->c, s->h, s->w, s->k, s->r, s->s, s->stride_h, s->stride_w,
+                        s->dil_h, s->dil_w, s->groups};
+    for (int v : dims)
+        if (v < 1) return fail(WPK_ERR_SHAPE, "every dimension, stride, dilation and groups must be >= 1");
+    if (s->pad_h < 0 || s->pad_w < 0) return fail(WPK_ERR_SHAPE, "padding must be >= 0");
+    if (s->c % s->groups || s->k % s->groups) return fail(WPK_ERR_SHAPE, "C and K must be divisible by groups");
+    *d = ConvDesc{s->n, s->c, s->h, s->w, s->k, s->r, s->s, s->stride_h, s->stride_w, s->pad_h,
+                  s->pad_w, s->dil_h, s->dil_w, s->groups, s->layout, s->epilogue, 0, 0, dtype};
+    d->p = out_size(s->h, s->pad_h, s->dil_h, s->r, s->stride_h);
+    d->q = out_size(s->w, s->pad_w, s->dil_w, s->s, s->stride_w);
+    if (d->p < 1 || d->q < 1) return fail(WPK_ERR_SHAPE, "output is empty (P or Q < 1)");
+    const double elems[] = {(double)s->n * s->c * s->h * s->w, (double)s->k * (s->c / s->groups) * s->r * s->s,
+                            (double)s->n * s->k * d->p * d->q};
+    for (double e : elems)
+        if (e > 4.0e9) return fail(WPK_ERR_UNSUPPORTED, "tensor larger than 2^32 elements");
+    if (s->groups != 1 && !(s->groups == s->c && s->groups == s->k))
+        return fail(WPK_ERR_UNSUPPORTED, "groups must be 1 or C == K (depthwise) in v1");
+    return WPK_OK;
+}
+
+// ----------------------------------------------------------------------------------------------
+// Schedule templates
+// ----------------------------------------------------------------------------------------------
+static Space make_space(int family) {
+    Space sp;
+    sp.family = family;
+    if (family == WPK_FAMILY_SIMT) {
+        // the paper's own gene set: threads per block and outputs per thread
+        sp.dom = {{1, 2, 4, 8, 16, 32}, {1, 2, 4, 8, 16, 32}, {1, 2, 4, 8, 16, 32},
+                  {1, 2, 4}, {1, 2, 4}, {1, 2, 4}, {1, 2, 4, 8}};
+        sp.names = {"T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"};
+    } else if (family == WPK_FAMILY_UMMA) {
+        sp.dom = {{16, 32, 64, 96, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8}, {1, 2, 4, 8, 16},
+                  {0, 1}, {1, 2}, {1, 2}, {128}};
+        sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "RASTER", "CTAS_PER_SM", "ACC_STAGES", "BLOCK_M"};
+    } else {
+        sp.dom = {{1, 2, 4, 8}, {1, 2, 4}, {64, 128, 256, 512}, {1, 2, 4}, {0}, {0}, {0}};
+        sp.names = {"VEC_C", "PIX_PER_THREAD", "THREADS", "ROWS_PER_CTA", "-", "-", "-"};
+    }
+    return sp;
+}
+
+const Space &family_space(int family) {
+    static const Space spaces[3] = {make_space(0), make_space(1), make_space(2)};
+    return spaces[family < 0 || family > 2 ? 0 : family];
+}
+
+static bool in_domain(const Space &sp, const Config &cfg, std::string *why) {
+    for (int g = 0; g < WPK_NUM_GENES; ++g) {
+        const auto &d = sp.dom[g];
+        if (std::find(d.begin(), d.end(), cfg.genes[g]) == d.end()) {
+            if (why) *why = std::string("gene ") + sp.names[g] + " = " + std::to_string(cfg.genes[g]) + " not in its domain";
+            return false;
+        }
+    }
+    return true;
+}
+
+bool family_applicable(const ConvDesc &d, int family, std::string *why) {
+    auto no = [&](const char *m) { if (why) *why = m; return false; };
+    if (family == WPK_FAMILY_SIMT) {
+        if (d.g != 1 && family != WPK_FAMILY_SIMT) return no("groups");
+        return true;   // the SIMT kernel handles every valid shape, layout and dtype
+    }
+    if (family == WPK_FAMILY_DW) {
+        if (!(d.g == d.c && d.g == d.k && d.g > 1)) return no("DW family needs groups == C == K");
+        return true;
+    }
+    if (family == WPK_FAMILY_UMMA) {
+        if (d.dtype == WPK_F32) return no("UMMA family needs tf32/bf16/fp16 (F32 is the exact CUDA-core path)");
+        if (d.g != 1) return no("UMMA family needs groups == 1");
+        if (d.sh > 8 || d.sw > 8) return no("TMA im2col traversal stride must be <= 8");
+        // TMA im2col 4-D bounding-box corners must lie in [-128, 127] (cuda.h cuTensorMapEncodeIm2col)
+        int lo_h = -d.ph, lo_w = -d.pw, up_h = d.ph - (d.r - 1) * d.dh, up_w = d.pw - (d.s - 1) * d.dw;
+        for (int v : {lo_h, lo_w, up_h, up_w})
+            if (v < -128 || v > 127) return no("TMA im2col corner out of [-128,127]");
+        if ((d.r - 1) * d.dh > 65535 || (d.s - 1) * d.dw > 65535) return no("im2col offset too large");
+        return true;
+    }
+    return no("unknown family");
+}
+
+static int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::string *why) {
+    auto no = [&](const std::string &m) { if (why) *why = m; return false; };
+    const int e = d.elem();
+    g->bm = cfg.genes[6];
+    g->bn = cfg.genes[0];
+    g->bk = 128 / e;           // one 128-byte swizzle atom of K per stage
+    g->stages = cfg.genes[1];
+    g->splits = cfg.genes[2];
+    g->raster = cfg.genes[3];
+    g->ctas_per_sm = cfg.genes[4];
+    g->acc_stages = cfg.genes[5];
+    g->cpad = round_up(d.c, 16 / e);    // TMA global strides must be multiples of 16 B
+    g->c_blocks = (g->cpad + g->bk - 1) / g->bk;
+    g->num_kb = d.r * d.s * g->c_blocks;
+    if (g->splits > g->num_kb) return no("SPLIT_K larger than the number of K blocks");
+    g->kb_per_split = (g->num_kb + g->splits - 1) / g->splits;
+    if ((long long)(g->splits - 1) * g->kb_per_split >= g->num_kb) return no("SPLIT_K leaves an empty split");
+    g->m_tiles = (int)((d.M() + g->bm - 1) / g->bm);
+    g->n_tiles = (d.k + g->bn - 1) / g->bn;
+    g->work = (long long)g->m_tiles * g->n_tiles * g->splits;
+    size_t stage = (size_t)g->bm * 128 + (size_t)g->bn * 128;
+    g->smem_bytes = 1024 /*align slack*/ + (size_t)g->stages * stage + 256 /*barriers*/;
+    size_t smem_cap = (g->ctas_per_sm == 1) ? 227 * 1024 : 113 * 1024;
+    if (g->smem_bytes > smem_cap) return no("STAGES x tile exceeds shared memory");
+    int cols = g->acc_stages * g->bn;
+    int alloc = 32;
+    while (alloc < cols) alloc <<= 1;
+    g->tmem_cols = alloc;
+    if (alloc * g->ctas_per_sm > 512) return no("TMEM columns exceed 512 per SM");
+    if (g->bn > round_up(d.k, 16) * 2 && g->bn > 16) return no("BLOCK_N more than 2x the output channels");
+    return true;
+}
+
+bool config_valid(const ConvDesc &d, const Config &cfg, std::string *why) {
+    if (cfg.family < 0 || cfg.family > 2) { if (why) *why = "bad family"; return false; }
+    if (!family_applicable(d, cfg.family, why)) return false;
+    if (!in_domain(family_space(cfg.family), cfg, why)) return false;
+    const int *gn = cfg.genes;
+    if (cfg.family == WPK_FAMILY_SIMT) {
+        long long threads = (long long)gn[0] * gn[1] * gn[2];
+        if (threads < 1 || threads > 1024) {
+            if (why) *why = "T_x*T_y*T_z must be in [1, 1024]";
+            return false;
+        }
+        long long gy = (d.p + (long long)gn[1] * gn[4] - 1) / ((long long)gn[1] * gn[4]);
+        long long gz = (long long)d.n * ((d.k + (long long)gn[2] * gn[5] - 1) / ((long long)gn[2] * gn[5]));
+        if (gy > 65535 || gz > 65535) { if (why) *why = "grid y/z exceeds 65535"; return false; }
+        return true;
+    }
+    if (cfg.family == WPK_FAMILY_UMMA) {
+        UmmaGeom g;
+        return umma_geometry(d, cfg, &g, why);
+    }
+    // DW
+    int vec = gn[0];
+    if (d.c % vec) { if (why) *why = "VEC_C must divide C"; return false; }
+    if (d.elem() * vec > 16) { if (why) *why = "VEC_C*elem > 16 bytes"; return false; }
+    return true;
+}
+
+int default_family(const ConvDesc &d) {
+    if (d.g > 1 && d.g == d.c && d.g == d.k) return WPK_FAMILY_DW;
+    if (family_applicable(d, WPK_FAMILY_UMMA, nullptr)) return WPK_FAMILY_UMMA;
+    return WPK_FAMILY_SIMT;
+}
+
+Config default_config(const ConvDesc &d, int family) {
+    Config c;
+    c.family = family;
+    if (family == WPK_FAMILY_SIMT) {
+        int g[7] = {16, 4, 4, 1, 1, 1, 1};
+        std::memcpy(c.genes, g, sizeof g);
+        return c;
+    }
+    if (family == WPK_FAMILY_DW) {
+        int vec = 16 / d.elem();
+        while (vec > 1 && d.c % vec) vec >>= 1;
+        int g[7] = {vec, 1, 256, 1, 0, 0, 0};
+        std::memcpy(c.genes, g, sizeof g);
+        return c;
+    }
+    // UMMA: smallest BLOCK_N covering K (max 256), deepest pipeline that fits, split-K when the
+    // tile count cannot fill the machine, double-buffered accumulators.
+    int bn = 256;
+    for (int v : {32, 64, 128, 256})
+        if (v >= d.k) { bn = v; break; }
+    c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = 1;
+    c.genes[5] = 2; c.genes[6] = 128;
+    for (int st = 8; st >= 2; --st) {
+        c.genes[1] = st;
+        if (config_valid(d, c, nullptr)) break;
+    }
+    UmmaGeom g;
+    if (umma_geometry(d, c, &g, nullptr)) {
+        long long tiles = (long long)g.m_tiles * g.n_tiles;
+        for (int sp : {16, 8, 4, 2}) {
+            if (tiles * sp <= 2 * 148 && tiles * 4 < 148) {
+                Config t = c;
+                t.genes[2] = sp;
+                if (config_valid(d, t, nullptr)) { c = t; break; }
+            }
+        }
+    }
+    if (!config_valid(d, c, nullptr)) {   // shape too odd for the defaults: fall back to SIMT
+        return default_config(d, WPK_FAMILY_SIMT);
+    }
+    return c;
+}
+
+}  // namespace wpk
+
+using namespace wpk;
+
+extern "C" {
+
+const char *wpk_last_error(void) { return g_last_error.c_str(); }
+
+void wpk_tune_options_init(wpk_tune_options *o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof *o);
+    o->struct_size = sizeof *o;
+    o->world = 1;
+    o->warmup = 3;
+    o->reps = 11;
+    o->l2_flush = 1;
+    o->eval_mode = WPK_EVAL_MEASURED;
+    o->family = WPK_FAMILY_AUTO;
+    o->ga_pop = 48; o->ga_elites = 4; o->ga_pool = 48; o->ga_max_gen = 50;
+    o->ga_mutation = 0.1; o->ga_eps = 0.02;
+    o->rl_envs = 1; o->rl_horizon = 64; o->rl_epochs = 4; o->rl_minibatch = 16;
+    o->rl_gamma = 0.99; o->rl_mu = 0.95; o->rl_clip = 0.2; o->rl_c1 = 0.15; o->rl_c2 = 20.0;
+    o->rl_lr = 1e-4; o->rl_keep_prob = 0.85;
+    o->rl_hidden[0] = 512; o->rl_hidden[1] = 1024; o->rl_hidden[2] = 1024; o->rl_hidden[3] = 512;
+    o->rl_alpha_mode = 0;
+}
+
+wpk_status wpk_conv2d_output_dims(const wpk_conv2d_shape *shape, int32_t *p, int32_t *q) {
+    if (!p || !q) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL output pointer");
+    ConvDesc d;
+    wpk_status st = to_desc(shape, WPK_F32, &d);
+    if (st != WPK_OK && st != WPK_ERR_UNSUPPORTED) return st;
+    if (st == WPK_ERR_UNSUPPORTED) {   // dims are still well defined
+        set_error("");
+    }
+    *p = d.p;
+    *q = d.q;
+    if (d.p < 1 || d.q < 1) return fail(WPK_ERR_SHAPE, "output is empty");
+    return WPK_OK;
+}
+
+wpk_status wpk_conv2d_plan(const wpk_conv2d_shape *shape, wpk_dtype dtype, int device, wpk_plan *out) {
+    if (!out) return fail(WPK_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (device < 0) return fail(WPK_ERR_INVALID_ARGUMENT, "device must be >= 0");
+    ConvDesc d;
+    wpk_status st = to_desc(shape, (int)dtype, &d);
+    if (st != WPK_OK) return st;
+    Plan *p = new (std::nothrow) Plan();
+    if (!p) return fail(WPK_ERR_OUT_OF_MEMORY, "host allocation failed");
+    p->d = d;
+    p->device = device;
+    p->cfg = default_config(d, default_family(d));
+    std::string why;
+    if (!config_valid(d, p->cfg, &why)) {
+        delete p;
+        return fail(WPK_ERR_EXHAUSTED, "no valid default config: " + why);
+    }
+    *out = reinterpret_cast<wpk_plan>(p);
+    return WPK_OK;
+}
+
+wpk_status wpk_conv2d_get_config(wpk_plan plan, int32_t *family, int32_t *genes) {
+    if (!plan || !family || !genes) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    *family = p->cfg.family;
+    std::memcpy(genes, p->cfg.genes, sizeof p->cfg.genes);
+    return WPK_OK;
+}
+
+int32_t wpk_conv2d_config_valid(wpk_plan plan, int32_t family, const int32_t *genes) {
+    if (!plan || !genes) { set_error("NULL argument"); return 0; }
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    Config c;
+    c.family = family;
+    std::memcpy(c.genes, genes, sizeof c.genes);
+    std::string why;
+    if (!config_valid(p->d, c, &why)) { set_error(why); return 0; }
+    return 1;
+}
+
+wpk_status wpk_conv2d_set_config(wpk_plan plan, int32_t family, const int32_t *genes) {
+    if (!plan || !genes) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    Config c;
+    c.family = family;
+    std::memcpy(c.genes, genes, sizeof c.genes);
+    std::string why;
+    if (!config_valid(p->d, c, &why)) return fail(WPK_ERR_INVALID_CONFIG, why);
+    if (!(c.family == p->cfg.family)) p->packed_for = nullptr;
+    p->cfg = c;
+    return WPK_OK;
+}
+
+wpk_status wpk_conv2d_invalidate(wpk_plan plan) {
+    if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
+    reinterpret_cast<Plan *>(plan)->packed_for = nullptr;
+    return WPK_OK;
+}
+
+wpk_status wpk_family_describe(int32_t family, int32_t *counts, int32_t *values, const char **names) {
+    if (family < 0 || family > 2 || !counts || !values) return fail(WPK_ERR_INVALID_ARGUMENT, "bad argument");
+    const Space &sp = family_space(family);
+    for (int g = 0; g < WPK_NUM_GENES; ++g) {
+        counts[g] = (int)sp.dom[g].size();
+        for (size_t i = 0; i < sp.dom[g].size() && i < 32; ++i) values[g * 32 + i] = sp.dom[g][i];
+        if (names) names[g] = sp.names[g];
+    }
+    return WPK_OK;
+}
+
+int32_t wpk_conv2d_last_launch_count(wpk_plan plan) {
+    return plan ? reinterpret_cast<Plan *>(plan)->last_launches : 0;
+}
+
+wpk_status wpk_conv2d_tune_stats(wpk_plan plan, double *best_us, int32_t *measured, int32_t *rounds,
+                                 double *seconds) {
+    if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (best_us) *best_us = p->best_us;
+    if (measured) *measured = p->measured;
+    if (rounds) *rounds = p->rounds;
+    if (seconds) *seconds = p->tune_seconds;
+    return WPK_OK;
+}
+
+}  // extern "C"

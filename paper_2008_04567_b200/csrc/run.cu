@@ -1,0 +1,387 @@
+// wpk_conv2d_run: layout/alignment preparation (KB4 aux kernels) and dispatch to the kernel
+// family of the plan's config. Weight packing is cached per weight pointer because weights are
+// inference constants ("kept invariant during inference").
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "dwconv.h"
+#include "simt_conv.cuh"
+#include "umma_conv.h"
+#include "wpk_internal.h"
+
+namespace wpk {
+
+// ---- aux kernels (KB4) -----------------------------------------------------------------------------
+// NCHW -> NHWC with the channel dimension zero-padded to Cp (16-byte TMA stride alignment).
+template <typename T>
+__global__ void nchw_to_nhwc_pad_kernel(const T *__restrict__ x, T *__restrict__ out, int N, int C, int H, int W,
+                                        int Cp) {
+    const long long total = (long long)N * H * W * Cp;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(i % Cp);
+        long long t = i / Cp;
+        const int w = (int)(t % W);
+        t /= W;
+        const int h = (int)(t % H);
+        const int n = (int)(t / H);
+        out[i] = (c < C) ? x[(((long long)n * C + c) * H + h) * W + w] : T(0.f);
+    }
+}
+// NHWC [rows][C] -> [rows][Cp] zero padded.
+template <typename T>
+__global__ void nhwc_pad_kernel(const T *__restrict__ x, T *__restrict__ out, long long rows, int C, int Cp) {
+    const long long total = rows * Cp;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(i % Cp);
+        out[i] = (c < C) ? x[(i / Cp) * C + c] : T(0.f);
+    }
+}
+// Weights -> [K][R][S][Cp] from KCRS (src_nchw) or KRSC, zero-padding channels.
+template <typename T>
+__global__ void pack_krsc_kernel(const T *__restrict__ w, T *__restrict__ out, int K, int C, int R, int S, int Cp,
+                                 int src_kcrs) {
+    const long long total = (long long)K * R * S * Cp;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(i % Cp);
+        long long t = i / Cp;
+        const int s = (int)(t % S);
+        t /= S;
+        const int r = (int)(t % R);
+        const int k = (int)(t / R);
+        T v = T(0.f);
+        if (c < C) v = src_kcrs ? w[(((long long)k * C + c) * R + r) * S + s] : w[(((long long)k * R + r) * S + s) * C + c];
+        out[i] = v;
+    }
+}
+// Depthwise weights [C][R][S] (both layouts, C/g = 1) -> [R][S][C].
+template <typename T>
+__global__ void pack_rsc_kernel(const T *__restrict__ w, T *__restrict__ out, int C, int R, int S) {
+    const long long total = (long long)C * R * S;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(i % C);
+        const long long rs = i / C;
+        out[i] = w[(long long)c * R * S + rs];
+    }
+}
+
+static unsigned grid_for(long long total, int sm) {
+    long long b = (total + 255) / 256;
+    long long cap = (long long)sm * 32;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+template <typename T>
+static void launch_aux_t(int which, const void *src, void *dst, const ConvDesc &d, int cp, int sm, cudaStream_t st) {
+    if (which == 0)
+        nchw_to_nhwc_pad_kernel<T><<<grid_for((long long)d.n * d.h * d.w * cp, sm), 256, 0, st>>>(
+            (const T *)src, (T *)dst, d.n, d.c, d.h, d.w, cp);
+    else if (which == 1)
+        nhwc_pad_kernel<T><<<grid_for((long long)d.n * d.h * d.w * cp, sm), 256, 0, st>>>(
+            (const T *)src, (T *)dst, (long long)d.n * d.h * d.w, d.c, cp);
+    else if (which == 2)
+        pack_krsc_kernel<T><<<grid_for((long long)d.k * d.r * d.s * cp, sm), 256, 0, st>>>(
+            (const T *)src, (T *)dst, d.k, d.c, d.r, d.s, cp, d.layout == WPK_NCHW);
+    else
+        pack_rsc_kernel<T><<<grid_for((long long)d.c * d.r * d.s, sm), 256, 0, st>>>((const T *)src, (T *)dst, d.c,
+                                                                                     d.r, d.s);
+}
+
+static void launch_aux(int which, const void *src, void *dst, const ConvDesc &d, int cp, int sm, cudaStream_t st) {
+    if (d.dtype == WPK_BF16) launch_aux_t<__nv_bfloat16>(which, src, dst, d, cp, sm, st);
+    else if (d.dtype == WPK_F16) launch_aux_t<__half>(which, src, dst, d, cp, sm, st);
+    else launch_aux_t<float>(which, src, dst, d, cp, sm, st);
+}
+
+// ---- device properties ------------------------------------------------------------------------------
+int device_sm_count(int device) {
+    static std::mutex mu;
+    static int cache[64] = {0};
+    std::lock_guard<std::mutex> lk(mu);
+    if (device < 0 || device >= 64) return 148;
+    if (!cache[device]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) v = 148;
+        cache[device] = v;
+    }
+    return cache[device];
+}
+
+int device_l2_bytes(int device) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device) != cudaSuccess || v <= 0) v = 126 << 20;
+    return v;
+}
+
+// ---- workspace layout -----------------------------------------------------------------------------
+struct WsLayout {
+    size_t x_off = 0, x_bytes = 0;    // transformed / padded activations
+    size_t w_off = 0, w_bytes = 0;    // packed weights
+    size_t p_off = 0, p_bytes = 0;    // split-K partials
+    size_t hx_off = 0, hx_bytes = 0;  // run_host staging of x
+    size_t hy_off = 0, hy_bytes = 0;  // run_host staging of y
+    size_t total = 0;
+};
+
+static size_t al256(size_t v) { return (v + 255) / 256 * 256; }
+
+static WsLayout ws_layout(const ConvDesc &d, const Config &cfg, bool host_staging) {
+    WsLayout L;
+    const size_t e = d.elem();
+    size_t off = 0;
+    if (cfg.family == WPK_FAMILY_UMMA) {
+        UmmaGeom g;
+        umma_geometry(d, cfg, &g, nullptr);
+        if (d.layout == WPK_NCHW || g.cpad != d.c) {
+            L.x_off = off; L.x_bytes = al256((size_t)d.n * d.h * d.w * g.cpad * e); off += L.x_bytes;
+        }
+        if (d.layout == WPK_NCHW || g.cpad != d.c) {
+            L.w_off = off; L.w_bytes = al256((size_t)d.k * d.r * d.s * g.cpad * e); off += L.w_bytes;
+        }
+        if (g.splits > 1) {
+            L.p_off = off; L.p_bytes = al256((size_t)g.splits * d.M() * d.k * 4); off += L.p_bytes;
+        }
+    } else if (cfg.family == WPK_FAMILY_DW) {
+        L.w_off = off; L.w_bytes = al256((size_t)d.c * d.r * d.s * e); off += L.w_bytes;
+    }
+    if (host_staging) {
+        L.hx_off = off; L.hx_bytes = al256((size_t)d.n * d.c * d.h * d.w * e); off += L.hx_bytes;
+        L.hy_off = off; L.hy_bytes = al256((size_t)d.M() * d.k * e); off += L.hy_bytes;
+    }
+    L.total = off;
+    return L;
+}
+
+size_t workspace_bytes(const Plan &p, const Config &cfg, bool host_staging) {
+    return ws_layout(p.d, cfg, host_staging).total;
+}
+
+// ---- one run ------------------------------------------------------------------------------------------
+int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const void *b, void *y, void *stream,
+                char *ws, size_t ws_bytes) {
+    const ConvDesc &d = p.d;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int sm = device_sm_count(p.device);
+    WsLayout L = ws_layout(d, cfg, false);
+    if (L.total > ws_bytes) {
+        set_error("workspace too small: need " + std::to_string(L.total) + " bytes");
+        return -1;
+    }
+    int launches = 0;
+    std::string err;
+    if (cfg.family == WPK_FAMILY_SIMT) {
+        const int *g = cfg.genes;
+        SimtKernelFn fn = (d.dtype == WPK_BF16) ? simt_get_bf16(g[3], g[4], g[5], g[6])
+                          : (d.dtype == WPK_F16) ? simt_get_f16(g[3], g[4], g[5], g[6])
+                                                 : simt_get_f32(g[3], g[4], g[5], g[6]);
+        if (!fn) { set_error("no SIMT instantiation for these tiles"); return -1; }
+        SimtArgs a{};
+        a.x = x; a.w = w; a.b = b; a.y = y;
+        a.N = d.n; a.C = d.c; a.H = d.h; a.W = d.w; a.K = d.k; a.R = d.r; a.S = d.s; a.P = d.p; a.Q = d.q;
+        a.sh = d.sh; a.sw = d.sw; a.ph = d.ph; a.pw = d.pw; a.dh = d.dh; a.dw = d.dw;
+        a.Cpg = d.c / d.g; a.Kpg = d.k / d.g; a.groups = d.g;
+        const long long cpg = d.c / d.g;
+        if (d.layout == WPK_NCHW) {
+            a.xs_n = (long long)d.c * d.h * d.w; a.xs_c = (long long)d.h * d.w; a.xs_h = d.w; a.xs_w = 1;
+            a.ws_k = cpg * d.r * d.s; a.ws_c = (long long)d.r * d.s; a.ws_r = d.s; a.ws_s = 1;
+            a.ys_n = (long long)d.k * d.p * d.q; a.ys_k = (long long)d.p * d.q; a.ys_p = d.q; a.ys_q = 1;
+        } else {
+            a.xs_n = (long long)d.h * d.w * d.c; a.xs_c = 1; a.xs_h = (long long)d.w * d.c; a.xs_w = d.c;
+            a.ws_k = (long long)d.r * d.s * cpg; a.ws_c = 1; a.ws_r = (long long)d.s * cpg; a.ws_s = cpg;
+            a.ys_n = (long long)d.p * d.q * d.k; a.ys_k = 1; a.ys_p = (long long)d.q * d.k; a.ys_q = d.k;
+        }
+        a.epilogue = d.epilogue;
+        const int tz = g[2] * g[5];
+        a.kblocks = (d.k + tz - 1) / tz;
+        dim3 block(g[0], g[1], g[2]);
+        dim3 grid((d.q + g[0] * g[3] - 1) / (g[0] * g[3]), (d.p + g[1] * g[4] - 1) / (g[1] * g[4]),
+                  (unsigned)(d.n * a.kblocks));
+        fn<<<grid, block, 0, st>>>(a);
+        cudaError_t ce = cudaGetLastError();
+        if (ce != cudaSuccess) { set_error(std::string("simt_conv launch: ") + cudaGetErrorString(ce)); return -1; }
+        return 1;
+    }
+    if (cfg.family == WPK_FAMILY_DW) {
+        const void *wp = ws + L.w_off;
+        if (p.packed_for != w || p.packed_cfg_family != WPK_FAMILY_DW) {
+            launch_aux(3, w, ws + L.w_off, d, 0, sm, st);
+            ++launches;
+            p.packed_for = w;
+            p.packed_cfg_family = WPK_FAMILY_DW;
+        }
+        DwArgs a{};
+        a.x = x; a.w = wp; a.b = b; a.y = y;
+        a.N = d.n; a.C = d.c; a.H = d.h; a.W = d.w; a.R = d.r; a.S = d.s; a.P = d.p; a.Q = d.q;
+        a.sh = d.sh; a.sw = d.sw; a.ph = d.ph; a.pw = d.pw; a.dh = d.dh; a.dw = d.dw;
+        if (d.layout == WPK_NCHW) {
+            a.xs_n = (long long)d.c * d.h * d.w; a.xs_c = (long long)d.h * d.w; a.xs_h = d.w; a.xs_w = 1;
+            a.ys_n = (long long)d.c * d.p * d.q; a.ys_c = (long long)d.p * d.q; a.ys_p = d.q; a.ys_q = 1;
+        } else {
+            a.xs_n = (long long)d.h * d.w * d.c; a.xs_c = 1; a.xs_h = (long long)d.w * d.c; a.xs_w = d.c;
+            a.ys_n = (long long)d.p * d.q * d.c; a.ys_c = 1; a.ys_p = (long long)d.q * d.c; a.ys_q = d.c;
+        }
+        a.epilogue = d.epilogue;
+        int rc = dw_launch(a, d.dtype, cfg.genes[0], cfg.genes[1], cfg.genes[2], sm, stream, &err);
+        if (rc < 0) { set_error(err); return -1; }
+        return launches + rc;
+    }
+    // ---- UMMA family ----
+    UmmaGeom g;
+    std::string why;
+    if (!umma_geometry(d, cfg, &g, &why)) { set_error("invalid UMMA config: " + why); return -1; }
+    const void *xk = x, *wk = w;
+    if (d.layout == WPK_NCHW) {
+        launch_aux(0, x, ws + L.x_off, d, g.cpad, sm, st);
+        ++launches;
+        xk = ws + L.x_off;
+    } else if (g.cpad != d.c) {
+        launch_aux(1, x, ws + L.x_off, d, g.cpad, sm, st);
+        ++launches;
+        xk = ws + L.x_off;
+    }
+    if (d.layout == WPK_NCHW || g.cpad != d.c) {
+        if (p.packed_for != w || p.packed_cfg_family != WPK_FAMILY_UMMA) {
+            launch_aux(2, w, ws + L.w_off, d, g.cpad, sm, st);
+            ++launches;
+            p.packed_for = w;
+            p.packed_cfg_family = WPK_FAMILY_UMMA;
+        }
+        wk = ws + L.w_off;
+    }
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) { set_error(std::string("aux kernel launch: ") + cudaGetErrorString(ce)); return -1; }
+    UmmaLaunch U{};
+    U.dtype = d.dtype; U.x = xk; U.w = wk; U.b = b; U.y = y;
+    U.partial = (g.splits > 1) ? reinterpret_cast<float *>(ws + L.p_off) : nullptr;
+    U.N = d.n; U.H = d.h; U.W = d.w; U.K = d.k; U.R = d.r; U.S = d.s; U.P = d.p; U.Q = d.q;
+    U.stride_h = d.sh; U.stride_w = d.sw; U.pad_h = d.ph; U.pad_w = d.pw; U.dil_h = d.dh; U.dil_w = d.dw;
+    U.epilogue = d.epilogue; U.out_nchw = d.layout == WPK_NCHW; U.sm_count = sm; U.stream = stream; U.g = g;
+    int rc = umma_launch(U, &err);
+    if (rc < 0) { set_error(err); return -1; }
+    return launches + rc;
+}
+
+static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static wpk_status ensure_ws(Plan *p, size_t need, char **ws, size_t *bytes) {
+    if (p->ws_user) {
+        if (p->ws_user_bytes < need)
+            return fail(WPK_ERR_OUT_OF_MEMORY, "workspace too small: need " + std::to_string(need) + " bytes");
+        *ws = p->ws_user;
+        *bytes = p->ws_user_bytes;
+        return WPK_OK;
+    }
+    if (p->ws_own_bytes < need) {
+        if (p->ws_own) cudaFree(p->ws_own);
+        p->ws_own = nullptr;
+        p->ws_own_bytes = 0;
+        p->packed_for = nullptr;
+        if (need) {
+            if (cudaMalloc(&p->ws_own, need) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(WPK_ERR_OUT_OF_MEMORY, "cudaMalloc of the plan workspace failed");
+            }
+            p->ws_own_bytes = need;
+        }
+    }
+    *ws = p->ws_own;
+    *bytes = p->ws_own_bytes;
+    return WPK_OK;
+}
+
+}  // namespace wpk
+
+using namespace wpk;
+
+extern "C" {
+
+wpk_status wpk_conv2d_workspace_size(wpk_plan plan, size_t *bytes) {
+    if (!plan || !bytes) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    *bytes = workspace_bytes(*p, p->cfg, true);
+    return WPK_OK;
+}
+
+wpk_status wpk_conv2d_set_workspace(wpk_plan plan, void *dev_ptr, size_t bytes) {
+    if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (dev_ptr && !aligned16(dev_ptr)) return fail(WPK_ERR_INVALID_ARGUMENT, "workspace must be 16-byte aligned");
+    size_t need = workspace_bytes(*p, p->cfg, false);
+    if (dev_ptr && bytes < need)
+        return fail(WPK_ERR_OUT_OF_MEMORY, "workspace too small: need " + std::to_string(need) + " bytes");
+    if (dev_ptr != p->ws_user) p->packed_for = nullptr;
+    p->ws_user = static_cast<char *>(dev_ptr);
+    p->ws_user_bytes = dev_ptr ? bytes : 0;
+    return WPK_OK;
+}
+
+wpk_status wpk_conv2d_run(wpk_plan plan, const void *x, const void *w, const void *b, void *y, void *stream) {
+    if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (!x || !w || !y) return fail(WPK_ERR_INVALID_ARGUMENT, "x, w and y must be non-NULL");
+    if ((p->d.epilogue != WPK_EPI_NONE) != (b != nullptr))
+        return fail(WPK_ERR_INVALID_ARGUMENT, "b must be non-NULL iff the epilogue uses a bias");
+    if (!aligned16(x) || !aligned16(w) || !aligned16(y) || (b && !aligned16(b)))
+        return fail(WPK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) { cudaGetLastError(); return fail(WPK_ERR_CUDA, "no CUDA device"); }
+    if (cur != p->device && cudaSetDevice(p->device) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(WPK_ERR_CUDA, "cudaSetDevice failed");
+    }
+    char *ws;
+    size_t bytes;
+    wpk_status st = ensure_ws(p, workspace_bytes(*p, p->cfg, false), &ws, &bytes);
+    if (st != WPK_OK) return st;
+    int n = launch_conv(*p, p->cfg, x, w, b, y, stream, ws, bytes);
+    if (n < 0) return WPK_ERR_CUDA;
+    p->last_launches = n;
+    return WPK_OK;
+}
+
+wpk_status wpk_conv2d_run_host(wpk_plan plan, const void *x_host, const void *w, const void *b, void *y_host,
+                               void *stream) {
+    if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (!x_host || !y_host || !w) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL pointer");
+    const ConvDesc &d = p->d;
+    char *ws;
+    size_t bytes;
+    WsLayout L = ws_layout(d, p->cfg, true);
+    wpk_status st = ensure_ws(p, L.total, &ws, &bytes);
+    if (st != WPK_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t xb = (size_t)d.n * d.c * d.h * d.w * d.elem(), yb = (size_t)d.M() * d.k * d.elem();
+    if (cudaMemcpyAsync(ws + L.hx_off, x_host, xb, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(WPK_ERR_CUDA, "H2D copy failed");
+    }
+    int n = launch_conv(*p, p->cfg, ws + L.hx_off, w, b, ws + L.hy_off, stream, ws, bytes);
+    if (n < 0) return WPK_ERR_CUDA;
+    p->last_launches = n;
+    if (cudaMemcpyAsync(y_host, ws + L.hy_off, yb, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaError_t e = cudaGetLastError();
+        return fail(WPK_ERR_CUDA, std::string("D2H copy / sync failed: ") + cudaGetErrorString(e));
+    }
+    return WPK_OK;
+}
+
+void wpk_conv2d_destroy(wpk_plan plan) {
+    if (!plan) return;
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (p->ws_own) cudaFree(p->ws_own);
+    delete p;
+}
+
+}  // extern "C"

@@ -1,0 +1,441 @@
+// KB1: implicit-GEMM forward convolution on 5th-generation tensor cores (tcgen05 / TMEM / TMA).
+//
+// GEMM view:  D[m, k] = sum_kg A[m, kg] * B[k, kg]
+//   m  = (n, p, q) output pixel (M = N*P*Q),   k = output channel,
+//   kg = (r, s, c) reduction index, c innermost (NHWC activations, KRSC weights).
+//   A[m, (r,s,c)] = x[n, p*sh - ph + r*dh, q*sw - pw + s*dw, c]  (0 outside) -- never materialised:
+//   each K block (one filter tap (r,s) x BK channels) is fetched by ONE TMA im2col load of 128
+//   output pixels x BK channels (the hardware walks the pixels, applies stride, zero-fills padding).
+//   B[k, (r,s,c)] = w[k, r, s, c]: TMA tiled load of BLOCK_N x BK from the [K][R*S][C] weights.
+// Both operands land in shared memory in the canonical K-major 128-byte-swizzle layout (BK =
+// 128 bytes of K per stage), consumed by tcgen05.mma (kind::f16 for bf16/fp16, kind::tf32) issued
+// by one thread; the fp32 accumulator lives in TMEM (double-buffered: 2 x BLOCK_N columns), so the
+// epilogue of tile i overlaps the main loop of tile i+1.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
+// warps 2-5 = epilogue (tcgen05.ld -> +bias -> ReLU -> round -> 16-byte vector stores, or fp32
+// split-K partials). Persistent grid: CTAs loop over work items (tile, split) with a static
+// round-robin schedule; RASTER picks which GEMM dimension varies fastest.
+//
+// The fused epilogue realises the paper's operator fusion ("write one CUDA kernel
+// function for the fused operator"; SPEC.md:136 relu(bias_add(conv))).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <string>
+
+#include "ptx.cuh"
+#include "umma_conv.h"
+
+namespace wpk {
+
+enum { DT_F16 = 0, DT_BF16 = 1, DT_TF32 = 2 };
+
+template <int DT> struct OutT;
+template <> struct OutT<DT_F16> { using T = __half; };
+template <> struct OutT<DT_BF16> { using T = __nv_bfloat16; };
+template <> struct OutT<DT_TF32> { using T = float; };
+
+__device__ __forceinline__ float ld_bias(const __half *b, int k) { return __half2float(b[k]); }
+__device__ __forceinline__ float ld_bias(const __nv_bfloat16 *b, int k) { return __bfloat162float(b[k]); }
+__device__ __forceinline__ float ld_bias(const float *b, int k) { return b[k]; }
+
+__device__ __forceinline__ uint32_t pack2(float a, float b, __half *) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b, __nv_bfloat16 *) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ void st_out(__half *p, float v) { *p = __float2half_rn(v); }
+__device__ __forceinline__ void st_out(__nv_bfloat16 *p, float v) { *p = __float2bfloat16_rn(v); }
+__device__ __forceinline__ void st_out(float *p, float v) { *p = v; }
+
+struct WorkPos {
+    int mt, nt, split;
+};
+__device__ __forceinline__ WorkPos decode_work(long long w, const UmmaArgs &a) {
+    WorkPos r;
+    r.split = (int)(w % a.splits);
+    long long t = w / a.splits;
+    if (a.raster == 0) {
+        r.mt = (int)(t / a.n_tiles);
+        r.nt = (int)(t % a.n_tiles);
+    } else {
+        r.nt = (int)(t / a.m_tiles);
+        r.mt = (int)(t % a.m_tiles);
+    }
+    return r;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(192, 1)
+    umma_conv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ UmmaArgs a) {
+    using T = typename OutT<DT>::T;
+    constexpr bool kTF32 = (DT == DT_TF32);
+    constexpr uint32_t A_BYTES = 128 * 128;   // BLOCK_M rows x 128 B
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+    uint8_t *smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+    const uint32_t b_bytes = (uint32_t)a.bn * 128u;
+    uint8_t *smA = smem;
+    uint8_t *smB = smem + (size_t)a.stages * A_BYTES;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smB + (size_t)a.stages * b_bytes);
+    uint64_t *full = bars;            // [8]
+    uint64_t *empty = bars + 8;       // [8]
+    uint64_t *tfull = bars + 16;      // [2]
+    uint64_t *tempty = bars + 18;     // [2]
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 20);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int s = 0; s < a.stages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&tfull[s], 1);
+            ptx::mbar_init(&tempty[s], 4);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc(tmem_holder, a.tmem_cols);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            uint32_t stage = 0, phase = 0;
+            const uint32_t tx_bytes = A_BYTES + b_bytes;
+            for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
+                const WorkPos wp = decode_work(w, a);
+                const long long m0 = (long long)wp.mt * 128;
+                const int n0 = wp.nt * a.bn;
+                const int nimg = (int)(m0 / a.PQ);
+                const int rem = (int)(m0 % a.PQ);
+                const int p = rem / a.Q, q = rem % a.Q;
+                const int wc = q * a.stride_w - a.pad_w, hc = p * a.stride_h - a.pad_h;
+                const int kb0 = wp.split * a.kb_per_split;
+                const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    const int cb = kb % a.c_blocks;
+                    const int rs = kb / a.c_blocks;
+                    const int r = rs / a.S, s = rs % a.S;
+                    ptx::mbar_arrive_expect_tx(&full[stage], tx_bytes);
+                    ptx::tma_load_im2col_4d(smA + stage * A_BYTES, &tmA, &full[stage], cb * a.bk, wc, hc, nimg,
+                                            (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                    ptx::tma_load_3d(smB + stage * b_bytes, &tmB, &full[stage], cb * a.bk, rs, n0);
+                    if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (single thread) =====================
+        if (lane == 0) {
+            uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+            for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
+                const WorkPos wp = decode_work(w, a);
+                const int kb0 = wp.split * a.kb_per_split;
+                const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * (uint32_t)a.bn;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = ptx::smem_u32(smA + stage * A_BYTES);
+                    const uint32_t b_addr = ptx::smem_u32(smB + stage * b_bytes);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {   // 4 x 32 bytes of K per 128-byte stage
+                        const uint64_t ad = ptx::sw128_kmajor_desc(a_addr + kk * 32);
+                        const uint64_t bd = ptx::sw128_kmajor_desc(b_addr + kk * 32);
+                        ptx::umma<kTF32>(d_tmem, ad, bd, a.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                    }
+                    ptx::umma_commit(&empty[stage]);   // frees this smem stage when the MMAs finish
+                    if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
+                }
+                ptx::umma_commit(&tfull[acc]);         // accumulator ready for the epilogue
+                if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ===================== epilogue warps 2..5 =====================
+        const int quarter = warp & 3;   // TMEM lanes [32*quarter, 32*quarter+32) are visible to this warp
+        const int row = quarter * 32 + lane;
+        uint32_t acc = 0, acc_phase = 0;
+        const T *bias = static_cast<const T *>(a.bias);
+        T *y = static_cast<T *>(a.y);
+        for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
+            const WorkPos wp = decode_work(w, a);
+            const long long m = (long long)wp.mt * 128 + row;
+            const int n0 = wp.nt * a.bn;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * (uint32_t)a.bn;
+            const bool mval = m < a.M;
+            long long out_base = 0;   // NCHW: n*K*PQ + pq
+            if (a.out_nchw && mval) {
+                const long long nimg = m / a.PQ;
+                out_base = nimg * (long long)a.K * a.PQ + (m - nimg * a.PQ);
+            }
+            for (int c0 = 0; c0 < a.bn; c0 += 16) {
+                const int k0 = n0 + c0;
+                if (k0 >= a.K) break;   // warp-uniform
+                float v[16];
+                ptx::tmem_ld16(taddr + c0, v);
+                if (!mval) continue;
+                const bool full16 = (k0 + 16 <= a.K);
+                if (a.splits > 1) {
+                    float *dst = a.partial + ((long long)wp.split * a.M + m) * a.K + k0;
+                    if (full16 && a.vec_ok) {
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4)
+                            *reinterpret_cast<float4 *>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    } else {
+                        for (int j = 0; j < 16 && k0 + j < a.K; ++j) dst[j] = v[j];
+                    }
+                    continue;
+                }
+                if (a.epilogue >= 1) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] += (k0 + j < a.K) ? ld_bias(bias, k0 + j) : 0.f;
+                }
+                if (a.epilogue == 2) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
+                }
+                if (a.out_nchw) {
+                    for (int j = 0; j < 16 && k0 + j < a.K; ++j)
+                        st_out(y + out_base + (long long)(k0 + j) * a.PQ, v[j]);
+                } else {
+                    T *dst = y + m * a.K + k0;
+                    if (full16 && a.vec_ok) {
+                        if constexpr (sizeof(T) == 2) {
+                            uint32_t u[8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) u[j] = pack2(v[2 * j], v[2 * j + 1], (T *)nullptr);
+                            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(u[0], u[1], u[2], u[3]);
+                            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(u[4], u[5], u[6], u[7]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4)
+                                *reinterpret_cast<float4 *>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        }
+                    } else {
+                        for (int j = 0; j < 16 && k0 + j < a.K; ++j) st_out(dst + j, v[j]);
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, a.tmem_cols);
+    }
+}
+
+// Deterministic split-K fixup: y = act(b + sum_{split=0..S-1} partial[split]) in fixed split order.
+template <typename T>
+__global__ void splitk_reduce_kernel(const float *__restrict__ partial, int splits, long long M, int K,
+                                     const T *__restrict__ bias, T *__restrict__ y, int epilogue, int out_nchw,
+                                     long long PQ) {
+    const long long total = M * K;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        float s = 0.f;
+        for (int sp = 0; sp < splits; ++sp) s += partial[sp * total + i];
+        const int k = (int)(i % K);
+        const long long m = i / K;
+        if (epilogue >= 1) s += ld_bias(bias, k);
+        if (epilogue == 2) s = fmaxf(s, 0.f);
+        long long o = i;
+        if (out_nchw) {
+            const long long n = m / PQ;
+            o = (n * K + k) * PQ + (m - n * PQ);
+        }
+        st_out(y + o, s);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const int *, const int *, cuuint32_t, cuuint32_t,
+                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static void *driver_sym(const char *name) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        return nullptr;
+    return fn;
+}
+
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn f = (EncodeTiledFn)driver_sym("cuTensorMapEncodeTiled");
+    return f;
+}
+static EncodeIm2colFn encode_im2col() {
+    static EncodeIm2colFn f = (EncodeIm2colFn)driver_sym("cuTensorMapEncodeIm2col");
+    return f;
+}
+
+static uint32_t make_idesc(int dt, int bm, int bn) {
+    uint32_t fmt = (dt == DT_F16) ? 0u : (dt == DT_BF16) ? 1u : 2u;
+    uint32_t d = 0;
+    d |= 1u << 4;                          // c_format = F32
+    d |= fmt << 7;                         // a_format
+    d |= fmt << 10;                        // b_format
+    // a_major = b_major = 0 (K-major), no negate, dense
+    d |= (uint32_t)(bn >> 3) << 17;        // n_dim
+    d |= (uint32_t)(bm >> 4) << 24;        // m_dim
+    return d;
+}
+
+template <int DT>
+static bool set_smem_attr() {
+    static bool done = false;
+    if (!done) {
+        if (cudaFuncSetAttribute(umma_conv_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+            cudaSuccess)
+            return false;
+        done = true;
+    }
+    return true;
+}
+
+int umma_launch(const UmmaLaunch &L, std::string *err) {
+    const int dt = L.dtype == WPK_F16 ? DT_F16 : L.dtype == WPK_BF16 ? DT_BF16 : DT_TF32;
+    const int e = (dt == DT_TF32) ? 4 : 2;
+    const CUtensorMapDataType tdt = (dt == DT_F16)    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                    : (dt == DT_BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                      : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    if (!encode_tiled() || !encode_im2col()) {
+        *err = "cuTensorMapEncode* driver entry points unavailable";
+        return -1;
+    }
+    const UmmaGeom &g = L.g;
+    // ---- A: im2col view of x[N][H][W][Cp] -------------------------------------------------------
+    CUtensorMap tmA, tmB;
+    {
+        cuuint64_t dims[4] = {(cuuint64_t)g.cpad, (cuuint64_t)L.W, (cuuint64_t)L.H, (cuuint64_t)L.N};
+        cuuint64_t strides[3] = {(cuuint64_t)g.cpad * e, (cuuint64_t)g.cpad * e * L.W,
+                                 (cuuint64_t)g.cpad * e * L.W * L.H};
+        int lower[2] = {-L.pad_w, -L.pad_h};
+        int upper[2] = {L.pad_w - (L.S - 1) * L.dil_w, L.pad_h - (L.R - 1) * L.dil_h};
+        cuuint32_t estr[4] = {1, (cuuint32_t)L.stride_w, (cuuint32_t)L.stride_h, 1};
+        CUresult r = encode_im2col()(&tmA, tdt, 4, const_cast<void *>(L.x), dims, strides, lower, upper,
+                                     (cuuint32_t)g.bk, (cuuint32_t)g.bm, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            *err = "cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")";
+            return -1;
+        }
+    }
+    // ---- B: tiled view of w[K][R*S][Cp] ---------------------------------------------------------
+    {
+        cuuint64_t dims[3] = {(cuuint64_t)g.cpad, (cuuint64_t)(L.R * L.S), (cuuint64_t)L.K};
+        cuuint64_t strides[2] = {(cuuint64_t)g.cpad * e, (cuuint64_t)g.cpad * e * L.R * L.S};
+        cuuint32_t box[3] = {(cuuint32_t)g.bk, 1, (cuuint32_t)g.bn};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = encode_tiled()(&tmB, tdt, 3, const_cast<void *>(L.w), dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            *err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+            return -1;
+        }
+    }
+    UmmaArgs a{};
+    a.bias = L.b;
+    a.y = L.y;
+    a.partial = L.partial;
+    a.M = (long long)L.N * L.P * L.Q;
+    a.K = L.K;
+    a.P = L.P;
+    a.Q = L.Q;
+    a.PQ = (long long)L.P * L.Q;
+    a.stride_h = L.stride_h; a.stride_w = L.stride_w; a.pad_h = L.pad_h; a.pad_w = L.pad_w;
+    a.dil_h = L.dil_h; a.dil_w = L.dil_w; a.S = L.S;
+    a.c_blocks = g.c_blocks; a.num_kb = g.num_kb; a.kb_per_split = g.kb_per_split; a.splits = g.splits;
+    a.m_tiles = g.m_tiles; a.n_tiles = g.n_tiles; a.raster = g.raster; a.work = g.work;
+    a.bn = g.bn; a.bk = g.bk; a.stages = g.stages; a.acc_stages = g.acc_stages;
+    a.idesc = make_idesc(dt, g.bm, g.bn);
+    a.tmem_cols = (uint32_t)g.tmem_cols;
+    a.epilogue = L.epilogue;
+    a.out_nchw = L.out_nchw;
+    a.vec_ok = (L.K % 16 == 0) ? 1 : 0;   // 16-element chunks start 32/64-byte aligned
+    cudaStream_t st = (cudaStream_t)L.stream;
+    long long grid = (long long)L.sm_count * g.ctas_per_sm;
+    if (grid > g.work) grid = g.work;
+    int launches = 0;
+    cudaError_t ce;
+#define WPK_LAUNCH_UMMA(DTV)                                                                          \
+    do {                                                                                              \
+        if (!set_smem_attr<DTV>()) { *err = "cudaFuncSetAttribute failed"; return -1; }               \
+        umma_conv_kernel<DTV><<<(unsigned)grid, 192, g.smem_bytes, st>>>(tmA, tmB, a);                \
+    } while (0)
+    if (dt == DT_F16) WPK_LAUNCH_UMMA(DT_F16);
+    else if (dt == DT_BF16) WPK_LAUNCH_UMMA(DT_BF16);
+    else WPK_LAUNCH_UMMA(DT_TF32);
+#undef WPK_LAUNCH_UMMA
+    ce = cudaGetLastError();
+    if (ce != cudaSuccess) {
+        *err = std::string("umma_conv_kernel launch: ") + cudaGetErrorString(ce);
+        return -1;
+    }
+    ++launches;
+    if (g.splits > 1) {
+        long long total = a.M * a.K;
+        int threads = 256;
+        long long blocks = (total + threads - 1) / threads;
+        if (blocks > (long long)L.sm_count * 16) blocks = (long long)L.sm_count * 16;
+        if (dt == DT_F16)
+            splitk_reduce_kernel<__half><<<(unsigned)blocks, threads, 0, st>>>(
+                L.partial, g.splits, a.M, a.K, (const __half *)L.b, (__half *)L.y, L.epilogue, L.out_nchw, a.PQ);
+        else if (dt == DT_BF16)
+            splitk_reduce_kernel<__nv_bfloat16><<<(unsigned)blocks, threads, 0, st>>>(
+                L.partial, g.splits, a.M, a.K, (const __nv_bfloat16 *)L.b, (__nv_bfloat16 *)L.y, L.epilogue,
+                L.out_nchw, a.PQ);
+        else
+            splitk_reduce_kernel<float><<<(unsigned)blocks, threads, 0, st>>>(
+                L.partial, g.splits, a.M, a.K, (const float *)L.b, (float *)L.y, L.epilogue, L.out_nchw, a.PQ);
+        ce = cudaGetLastError();
+        if (ce != cudaSuccess) {
+            *err = std::string("splitk_reduce launch: ") + cudaGetErrorString(ce);
+            return -1;
+        }
+        ++launches;
+    }
+    return launches;
+}
+
+}  // namespace wpk

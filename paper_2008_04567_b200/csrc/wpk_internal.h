@@ -1,0 +1,103 @@
+// Internal declarations shared by the libwpk.so translation units (host C++ and CUDA).
+// Never included by oracle/ (task rule ③: the oracle shares no code with the product).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "wpk.h"
+
+namespace wpk {
+
+// --- error reporting -----------------------------------------------------------------------------
+void set_error(const std::string &msg);
+wpk_status fail(wpk_status st, const std::string &msg);
+
+// --- the GEMM view of one convolution (PAPER.md:86-93 O_conv shape, generalised) ----------------
+struct ConvDesc {
+    int n, c, h, w, k, r, s;
+    int sh, sw, ph, pw, dh, dw, g;
+    int layout, epilogue;
+    int p, q;          // output spatial size
+    int dtype;         // wpk_dtype
+    long long M() const { return (long long)n * p * q; }
+    long long flops() const { return 2LL * n * k * p * q * (c / g) * r * s; }
+    int elem() const { return (dtype == WPK_BF16 || dtype == WPK_F16) ? 2 : 4; }
+};
+
+struct Config {
+    int family = WPK_FAMILY_SIMT;
+    int genes[WPK_NUM_GENES] = {0, 0, 0, 0, 0, 0, 0};
+    bool operator==(const Config &o) const {
+        if (family != o.family) return false;
+        for (int i = 0; i < WPK_NUM_GENES; ++i)
+            if (genes[i] != o.genes[i]) return false;
+        return true;
+    }
+    bool operator<(const Config &o) const {
+        if (family != o.family) return family < o.family;
+        for (int i = 0; i < WPK_NUM_GENES; ++i)
+            if (genes[i] != o.genes[i]) return genes[i] < o.genes[i];
+        return false;
+    }
+};
+
+// Gene domains of one family ("schedule template", PAPER.md:59 / 65).
+struct Space {
+    int family;
+    std::vector<std::vector<int>> dom;   // 7 domains
+    std::vector<const char *> names;
+};
+const Space &family_space(int family);
+// Hardware/shape constraints; on false, *why says which ("verified first").
+bool config_valid(const ConvDesc &d, const Config &cfg, std::string *why);
+Config default_config(const ConvDesc &d, int family);
+int default_family(const ConvDesc &d);
+bool family_applicable(const ConvDesc &d, int family, std::string *why);
+
+// --- UMMA family: derived launch geometry --------------------------------------------------------
+struct UmmaGeom {
+    int bm, bn, bk, stages, splits, raster, ctas_per_sm, acc_stages;
+    int c_blocks, num_kb, kb_per_split, m_tiles, n_tiles;
+    long long work;
+    int cpad;           // channel count as stored for the kernel (C rounded up to the alignment)
+    size_t smem_bytes;
+    int tmem_cols;
+};
+bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::string *why);
+
+// --- device-side entry points (implemented in .cu files) -----------------------------------------
+struct Workspace {
+    char *base = nullptr;
+    size_t bytes = 0;
+};
+
+struct Plan;
+size_t workspace_bytes(const Plan &p, const Config &cfg, bool host_staging);
+// Launch everything for one run on `stream`; returns number of kernel launches or -1 (error set).
+int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const void *b, void *y,
+                void *stream, char *ws, size_t ws_bytes);
+int device_sm_count(int device);
+int device_l2_bytes(int device);
+
+struct Plan {
+    ConvDesc d;
+    int device = 0;
+    Config cfg;
+    // workspace
+    char *ws_user = nullptr;
+    size_t ws_user_bytes = 0;
+    char *ws_own = nullptr;
+    size_t ws_own_bytes = 0;
+    // packed weights cache
+    const void *packed_for = nullptr;
+    int packed_cfg_family = -1;
+    int last_launches = 0;
+    // tune stats
+    double best_us = 0, tune_seconds = 0;
+    int measured = 0, rounds = 0;
+};
+
+}  // namespace wpk

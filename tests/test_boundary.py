@@ -1,0 +1,131 @@
+"""C-ABI boundary tests that need no GPU: the library loads, exports every symbol include/wpk.h
+declares, struct sizes agree with the C compiler's, and host-side validation maps bad shapes and
+configs to the documented wpk_status codes."""
+import ctypes
+import os
+import subprocess
+
+import pytest
+
+import oracle
+import workloads
+from paper_2008_04567_b200 import _lib as L
+from paper_2008_04567_b200.conv import make_options
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = L.load()
+    names = L.header_symbols()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(lib, n), n
+    out = subprocess.check_output(["nm", "-D", "--defined-only", L.LIB_PATH]).decode()
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert set(names) <= exported
+
+
+def test_struct_sizes_match_c(tmp_path):
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "wpk.h"\nint main(){printf("%zu %zu\\n", '
+                   'sizeof(wpk_tune_options), sizeof(wpk_conv2d_shape));}\n')
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    a, b = map(int, subprocess.check_output([str(exe)]).split())
+    assert (a, b) == (ctypes.sizeof(L.TuneOptions), ctypes.sizeof(L.Shape))
+
+
+def _plan(shape, dtype="bf16"):
+    lib = L.load()
+    h = ctypes.c_void_p()
+    st = lib.wpk_conv2d_plan(ctypes.byref(shape), L.DTYPES[dtype], 0, ctypes.byref(h))
+    return st, h
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(n=0), L.ERR_SHAPE), (dict(c=0), L.ERR_SHAPE), (dict(stride=0), L.ERR_SHAPE),
+    (dict(h=1, pad=0), L.ERR_SHAPE),                                  # 3x3 on 1x1 -> empty output
+    (dict(groups=2, c=3), L.ERR_SHAPE), (dict(groups=2, c=4, k=6), L.ERR_UNSUPPORTED),
+    (dict(pad=-1), L.ERR_SHAPE),
+])
+def test_shape_validation(kw, status):
+    base = dict(n=1, c=4, h=8, w=8, k=8, r=3, s=3, stride=1, pad=1, dil=1, groups=1)
+    base.update(kw)
+    shp = L.make_shape(**base)
+    st, h = _plan(shp)
+    assert st == status, L.last_error()
+    assert L.last_error()
+
+
+def test_bad_struct_size_and_null():
+    lib = L.load()
+    shp = L.make_shape(1, 4, 8, 8, 8, 3, 3, 1, 1)
+    shp.struct_size = 4
+    st, _ = _plan(shp)
+    assert st == L.ERR_INVALID_ARGUMENT
+    assert lib.wpk_conv2d_plan(None, 0, 0, ctypes.byref(ctypes.c_void_p())) == L.ERR_INVALID_ARGUMENT
+    assert lib.wpk_conv2d_run(None, None, None, None, None, None) == L.ERR_INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("layer", workloads.resnet50(32) + workloads.vgg16(64) + workloads.mobilenet_v2(1)
+                         + workloads.table1() + [workloads.CONFIG1], ids=lambda l: l.name)
+def test_output_dims_and_default_plan(oracle_lib, layer):
+    from paper_2008_04567_b200 import output_dims
+    pq = output_dims(layer.n, layer.c, layer.h, layer.w, layer.k, layer.r, layer.s, layer.stride, layer.pad,
+                     layer.dil, layer.groups)
+    assert pq == oracle.out_dims(layer.n, layer.c, layer.h, layer.w, layer.k, layer.r, layer.s, layer.stride,
+                                 layer.pad, layer.dil, layer.groups)
+    for dtype in ("f32", "tf32", "bf16", "f16"):
+        shp = L.make_shape(layer.n, layer.c, layer.h, layer.w, layer.k, layer.r, layer.s, layer.stride, layer.pad,
+                           layer.dil, layer.groups, "nhwc")
+        st, h = _plan(shp, dtype)
+        assert st == L.OK, L.last_error()
+        lib = L.load()
+        fam, genes = ctypes.c_int32(), (ctypes.c_int32 * 7)()
+        L.check(lib.wpk_conv2d_get_config(h, ctypes.byref(fam), genes))
+        if layer.groups > 1:
+            assert fam.value == L.FAMILIES["dw"]
+        elif dtype == "f32":
+            assert fam.value == L.FAMILIES["simt"]
+        else:
+            assert fam.value == L.FAMILIES["umma"]
+        assert lib.wpk_conv2d_config_valid(h, fam, genes) == 1
+        lib.wpk_conv2d_destroy(h)
+
+
+def test_set_config_validation():
+    lib = L.load()
+    shp = L.make_shape(1, 64, 56, 56, 64, 3, 3, 1, 1, layout="nhwc")
+    st, h = _plan(shp, "f32")
+    assert st == 0
+    bad = (ctypes.c_int32 * 7)(32, 32, 2, 1, 1, 1, 1)         # 2048 threads > 1024
+    assert lib.wpk_conv2d_set_config(h, 0, bad) == L.ERR_INVALID_CONFIG
+    assert "1024" in L.last_error()
+    ok = (ctypes.c_int32 * 7)(16, 8, 4, 1, 1, 1, 1)
+    assert lib.wpk_conv2d_set_config(h, 0, ok) == L.OK
+    notin = (ctypes.c_int32 * 7)(7, 8, 4, 1, 1, 1, 1)
+    assert lib.wpk_conv2d_set_config(h, 0, notin) == L.ERR_INVALID_CONFIG
+    # f32 cannot use the tensor-core family
+    umma = (ctypes.c_int32 * 7)(64, 4, 1, 0, 1, 2, 128)
+    assert lib.wpk_conv2d_set_config(h, 1, umma) == L.ERR_INVALID_CONFIG
+    lib.wpk_conv2d_destroy(h)
+    st, h = _plan(shp, "bf16")
+    too_deep = (ctypes.c_int32 * 7)(256, 8, 1, 0, 1, 2, 128)   # 8 x 48 KB stages > 227 KB
+    assert lib.wpk_conv2d_set_config(h, 1, too_deep) == L.ERR_INVALID_CONFIG
+    assert lib.wpk_conv2d_set_config(h, 1, umma) == L.OK
+    lib.wpk_conv2d_destroy(h)
+
+
+def test_family_describe_matches_paper_genes():
+    names, doms = L.family_describe("simt")
+    assert names == ["T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"]
+    names, doms = L.family_describe("umma")
+    assert names[0] == "BLOCK_N" and 128 in doms[0]
+
+
+def test_options_defaults():
+    o = make_options()
+    assert (o.warmup, o.reps, o.world, o.ga_pop, o.ga_elites) == (3, 11, 1, 48, 4)
+    assert (o.rl_c1, o.rl_c2) == (0.15, 20.0)
+    assert list(o.rl_hidden) == [512, 1024, 1024, 512]

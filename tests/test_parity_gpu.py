@@ -1,0 +1,159 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle on the same seeded inputs.
+
+Exact-integer mode (x, w in {-1,0,1}, b in {-4..4}) must be bit-exact on every precision path
+(reading c11); uniform mode must meet BASELINE.json's tolerances: fp32 max-rel 1e-5, TF32
+normwise 5e-3, bf16/fp16 normwise 2e-2."""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from workloads import ConvLayer
+
+from _util import TOL, assert_bit_exact, oracle_full, rel_error, run_product
+
+pytestmark = pytest.mark.gpu
+
+SMALL = [
+    ConvLayer("cfg1", 1, 3, 8, 8, 8, 3, 3, 1, 1),
+    ConvLayer("3x3s1", 2, 64, 14, 14, 96, 3, 3, 1, 1),
+    ConvLayer("3x3s2", 2, 64, 15, 13, 64, 3, 3, 2, 1),
+    ConvLayer("1x1", 3, 128, 7, 9, 40, 1, 1, 1, 0),
+    ConvLayer("1x1s2", 2, 64, 14, 14, 128, 1, 1, 2, 0),
+    ConvLayer("dil2", 1, 32, 17, 17, 48, 3, 3, 1, 2, 2),
+    ConvLayer("7x7s2c3", 2, 3, 30, 30, 64, 7, 7, 2, 3),
+    ConvLayer("5x3_asym", 1, 16, 12, 20, 24, 5, 3, 1, 1),
+    ConvLayer("valid", 1, 64, 12, 10, 256, 3, 3, 1, 0),
+]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _setup():
+    oracle.build()
+    torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+@pytest.mark.parametrize("dtype", ["f32", "tf32", "bf16", "f16"])
+@pytest.mark.parametrize("layer", SMALL, ids=lambda l: l.name)
+def test_default_config_int_bit_exact(layer, dtype, layout):
+    x, w, b = workloads.generate(layer, dtype, "int", seed=11)
+    y, plan = run_product(layer, dtype, layout, x, w, b)
+    assert_bit_exact(y, oracle_full(layer, x, w, b))
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+@pytest.mark.parametrize("dtype", ["f32", "tf32", "bf16", "f16"])
+@pytest.mark.parametrize("layer", SMALL, ids=lambda l: l.name)
+def test_default_config_uniform_tolerance(layer, dtype, layout):
+    x, w, b = workloads.generate(layer, dtype, "uniform", seed=12)
+    y, plan = run_product(layer, dtype, layout, x, w, b)
+    err = rel_error(dtype, y, oracle_full(layer, x, w, b))
+    assert err <= TOL[dtype], err
+
+
+@pytest.mark.parametrize("epilogue", ["none", "bias", "bias_relu"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_epilogues(dtype, epilogue):
+    L = SMALL[1]
+    x, w, b = workloads.generate(L, dtype, "int", seed=13)
+    y, _ = run_product(L, dtype, "nhwc", x, w, b if epilogue != "none" else None, epilogue=epilogue)
+    assert_bit_exact(y, oracle_full(L, x, w, b, epilogue))
+
+
+def _umma_space():
+    bns = [16, 32, 64, 96, 128, 192, 256]
+    out = []
+    for bn, st, sp, ra, ctas, acc in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1], [1, 2], [1, 2]):
+        out.append((bn, st, sp, ra, ctas, acc, 128))
+    return out
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_umma_every_config_bit_exact(dtype):
+    """Every valid UMMA config in a sweep of the space on one shape with an M tail, K tail and
+    several K blocks: exact-integer outputs must be bit-identical (a tiling can change speed,
+    never values)."""
+    L = ConvLayer("sweep", 2, 64, 11, 13, 200, 3, 3, 1, 1)
+    x, w, b = workloads.generate(L, dtype, "int", seed=14)
+    ref = oracle_full(L, x, w, b)
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import to_layout, from_layout
+    plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype=dtype)
+    xl, wl = to_layout(x, w, "nhwc")
+    xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
+    n = 0
+    for genes in _umma_space():
+        if not plan.config_valid(1, genes):
+            continue
+        plan.set_config(1, genes)
+        y = plan.run(xl, wl, bc)
+        torch.cuda.synchronize()
+        assert_bit_exact(from_layout(y.cpu(), "nhwc"), ref)
+        n += 1
+    assert n > 100
+
+
+def test_simt_every_tile_template():
+    L = ConvLayer("simt", 2, 6, 9, 11, 10, 3, 3, 2, 1)
+    x, w, b = workloads.generate(L, "f32", "int", seed=15)
+    ref = oracle_full(L, x, w, b)
+    from paper_2008_04567_b200 import Conv2dPlan
+    plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nchw", dtype="f32")
+    xc, wc, bc = x.cuda(), w.cuda(), b.cuda()
+    for tx, ty, tz, trz in itertools.product([1, 2, 4], [1, 2, 4], [1, 2, 4], [1, 2, 4, 8]):
+        for T in [(8, 4, 2), (32, 1, 1), (1, 1, 32)]:
+            genes = list(T) + [tx, ty, tz, trz]
+            plan.set_config(0, genes)
+            y = plan.run(xc, wc, bc)
+            torch.cuda.synchronize()
+            assert_bit_exact(y.cpu(), ref)
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
+def test_depthwise(dtype, layout):
+    for L in [ConvLayer("dw", 2, 96, 15, 15, 96, 3, 3, 2, 1, 1, 96), ConvLayer("dw1", 1, 32, 12, 12, 32, 3, 3, 1, 1, 1, 32)]:
+        x, w, b = workloads.generate(L, dtype, "int", seed=16)
+        y, plan = run_product(L, dtype, layout, x, w, b)
+        assert plan.config[0] == 2
+        assert_bit_exact(y, oracle_full(L, x, w, b))
+        from paper_2008_04567_b200 import Conv2dPlan
+        for genes in itertools.product([1, 2, 4, 8], [1, 2, 4], [64, 256], [1]):
+            if plan.config_valid(2, list(genes) + [0, 0, 0]):
+                plan.set_config(2, list(genes) + [0, 0, 0])
+                from _util import to_layout, from_layout
+                xl, wl = to_layout(x, w, layout)
+                yy = plan.run(xl.cuda(), wl.cuda(), b.cuda())
+                torch.cuda.synchronize()
+                assert_bit_exact(from_layout(yy.cpu(), layout), oracle_full(L, x, w, b))
+
+
+def test_run_host_matches_device():
+    L = SMALL[1]
+    x, w, b = workloads.generate(L, "bf16", "int", seed=17)
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import to_layout
+    plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype="bf16")
+    xl, wl = to_layout(x, w, "nhwc")
+    yh = torch.empty(plan.y_shape(), dtype=torch.bfloat16).pin_memory()
+    plan.run_host(xl.pin_memory(), wl.cuda(), b.cuda(), yh)
+    yd = plan.run(xl.cuda(), wl.cuda(), b.cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(yh, yd.cpu())
+
+
+@pytest.mark.parametrize("layer", workloads.resnet50(32), ids=lambda l: l.name)
+def test_resnet50_n32_sampled_bf16(layer):
+    """Full-size bench layers (BASELINE.json configs[1], N=32 bf16 NHWC, default config): sampled
+    outputs (all borders of image 0 / first channels + 4096 random points) vs the oracle."""
+    x, w, b = workloads.generate(layer, "bf16", "int", seed=workloads.config_seed(1, 0))
+    y, plan = run_product(layer, "bf16", "nhwc", x, w, b)
+    pts = workloads.random_points(layer, plan.p, plan.q, 4096, seed=1).numpy()
+    ref = oracle.conv2d_points(x, w, b, pts, stride=layer.stride, pad=layer.pad, nthreads=8)
+    got = y[pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
+    want = torch.from_numpy(ref).to(torch.bfloat16)
+    assert torch.equal(got.float() + 0, want.float() + 0)
