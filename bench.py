@@ -1,0 +1,366 @@
+"""bench.py -- the driver's benchmark contract for the WPK hot path on B200.
+
+One step = one forward pass of every ResNet-50 v1.5 convolution (53 convs, 23 unique shapes) at
+N=32 per GPU, bf16 NHWC, fused bias+ReLU (BASELINE.json configs[1], N=32 bf16 -- the largest
+single-GPU case the metric is quoted on), each layer running the config chosen by the per-layer
+GA tuner (§2.3) before the timed region. value = whole-job conv TFLOP/s
+(2*N*K*P*Q*C*R*S summed over layers and ranks / max-over-ranks device time).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl wpk|reference] [--tune-budget B]
+
+N>1 runs under torchrun: every rank processes its own N=32 shard (the N=256 batch split along N,
+BASELINE.json configs[4]; weak scaling) and the GA population is sharded over the ranks with an
+NCCL all-gather of fitness records (paper_2008_04567_b200/dist.py).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "conv2d TFLOP/s per layer (% of B200 peak) vs same-box cuDNN; tuning time 1/2/4/8 GPU"
+PEAK_FALLBACK = {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}   # B200_PROFILING.md fallback
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return dict(PEAK_FALLBACK), "fallback (B200_PROFILING.md)"
+
+
+def layer_flops(L, p, q):
+    return 2 * L.n * L.k * p * q * (L.c // L.groups) * L.r * L.s
+
+
+def layer_bytes(L, p, q, elem):
+    return elem * (L.n * L.c * L.h * L.w + L.k * (L.c // L.groups) * L.r * L.s + L.k + L.n * L.k * p * q)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
+                          and "Not" not in r[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# -------------------------------------------------------------------------------------------------
+# reference arm: the oracle (test infrastructure) timed on the host cores
+# -------------------------------------------------------------------------------------------------
+def oracle_sample_step(layers, per_layer_points, nthreads, seed=0):
+    """One bounded sample of the workload through the oracle: `per_layer_points` outputs of every
+    unique layer (x 'count'), computed one by one. Returns (flops, seconds)."""
+    import oracle
+    import workloads
+    flops, secs = 0.0, 0.0
+    for i, L in enumerate(layers):
+        x, w, b = workloads.generate(L, "bf16", "uniform", seed=workloads.config_seed(1, i))
+        p, q = oracle.out_dims(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups)
+        pts = workloads.random_points(L, p, q, per_layer_points, seed=seed + i).numpy()[-per_layer_points:]
+        t0 = time.perf_counter()
+        for _ in range(L.count):
+            oracle.conv2d_points(x, w, b, pts, stride=L.stride, pad=L.pad, nthreads=nthreads)
+        secs += time.perf_counter() - t0
+        flops += L.count * len(pts) * 2.0 * (L.c // L.groups) * L.r * L.s
+    return flops, secs
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    import workloads
+    oracle.build()
+    layers = workloads.resnet50(32)
+    cores = os.cpu_count() or 1
+    pts = args.ref_points
+    for _ in range(args.warmup):
+        oracle_sample_step(layers, max(pts // 8, 16), cores)
+    tot_f, tot_s = 0.0, 0.0
+    for k in range(args.steps):
+        f, s = oracle_sample_step(layers, pts, cores, seed=100 + k)
+        tot_f += f
+        tot_s += s
+    tflops = tot_f / tot_s / 1e12
+    sample = (f"{pts} sampled outputs x 53 ResNet-50 convs (N=32 bf16-rounded inputs, float64 oracle) "
+              f"per step, computed one by one")
+    line = {"impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "resnet50_convs_n32_bf16_nhwc_bias_relu (sampled)",
+                                            "global_batch": 32, "parallelism": "host cores"},
+            "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------------------------------------------
+# WPK arm
+# -------------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="wpk", choices=["wpk", "reference"])
+    ap.add_argument("--batch", type=int, default=32, help="images per GPU")
+    ap.add_argument("--tune-budget", type=int, default=24, help="distinct configs measured per unique layer")
+    ap.add_argument("--search", default="ga", choices=["ga", "rl", "random", "none"])
+    ap.add_argument("--no-cudnn", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-points", type=int, default=256)
+    ap.add_argument("--cpu-sample-points", type=int, default=128)
+    ap.add_argument("--layers-json", default=None, help="also write the per-layer table here")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import workloads
+    from paper_2008_04567_b200 import Conv2dPlan, make_options
+    from paper_2008_04567_b200 import selector
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    from paper_2008_04567_b200 import dist as wdist
+
+    peaks, peak_src = load_peaks()
+    layers = workloads.resnet50(args.batch)
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- plans, inputs (resident in HBM), tuning -------------------------------------------------
+    t_tune0 = time.perf_counter()
+    units = []           # one entry per conv of the network (53), sharing the layer's plan
+    plans = []
+    tune_info = []
+    for i, L in enumerate(layers):
+        plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups, layout="nhwc",
+                          dtype="bf16", device=local)
+        if args.search != "none" and args.tune_budget > 0:
+            ex = wdist.make_exchange(pg) if world > 1 else {}
+            res = plan.tune(args.search, args.tune_budget, seed=i, rank=rank, world=world, **ex)
+            tune_info.append({"layer": L.name, "best_us": res.best_us, "measured": res.measured,
+                              "family": res.family, "genes": res.genes})
+        plans.append(plan)
+        for c in range(L.count):
+            x, w, b = workloads.generate(L, "bf16", "uniform", seed=workloads.config_seed(1, i) + 7919 * c + rank)
+            xd = x.permute(0, 2, 3, 1).contiguous().to(dev)
+            wd = w.permute(0, 2, 3, 1).contiguous().to(dev)
+            bd = b.to(dev)
+            yd = torch.empty(plan.y_shape(), dtype=torch.bfloat16, device=dev)
+            units.append((i, plan, xd, wd, bd, yd))
+    torch.cuda.synchronize()
+    tune_seconds = time.perf_counter() - t_tune0
+
+    total_flops = sum(layer_flops(L, plans[i].p, plans[i].q) * L.count for i, L in enumerate(layers))
+
+    def step(events=None):
+        launches = 0
+        for j, (i, plan, xd, wd, bd, yd) in enumerate(units):
+            if events is not None:
+                events[j][0].record(stream)
+            plan.run(xd, wd, bd, yd, stream=stream)
+            if events is not None:
+                events[j][1].record(stream)
+            launches += plan.last_launch_count()
+        return launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region ------------------------------------------------------------------------------
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in units]
+          for _ in range(args.steps)]
+    if pg is not None:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        launches = 0
+        for k in range(args.steps):
+            launches += step(ev[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if pg is not None:
+        tt = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+        torch.distributed.barrier()
+    ms_per_step = ms / args.steps
+    value = total_flops * world * args.steps / (ms * 1e-3) / 1e12
+
+    # per-layer device times from the live events (average over steps)
+    per_unit_ms = [statistics.mean(ev[k][j][0].elapsed_time(ev[k][j][1]) for k in range(args.steps))
+                   for j in range(len(units))]
+    per_layer_ms = [0.0] * len(layers)
+    for j, (i, *_rest) in enumerate(units):
+        per_layer_ms[i] += per_unit_ms[j]
+    kern_ms = sum(per_unit_ms)
+    achieved = total_flops / (kern_ms * 1e-3) / 1e12
+    peak = float(peaks.get("bf16_tflops", PEAK_FALLBACK["bf16_tflops"]))
+
+    # ---- e2e through the public API with host buffers ----------------------------------------------
+    host = []
+    h2d = d2h = 0
+    for (i, plan, xd, wd, bd, yd) in units:
+        xh = xd.cpu().pin_memory()
+        yh = torch.empty(yd.shape, dtype=yd.dtype).pin_memory()
+        host.append((plan, xh, wd, bd, yh))
+        h2d += xh.numel() * xh.element_size()
+        d2h += yh.numel() * yh.element_size()
+    for (plan, xh, wd, bd, yh) in host:     # warm-up of the host path
+        plan.run_host(xh, wd, bd, yh, stream=stream)
+    e2e_steps = max(1, min(args.steps, 5))
+    if pg is not None:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        for (plan, xh, wd, bd, yh) in host:
+            plan.run_host(xh, wd, bd, yh, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if pg is not None:
+        tt = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = total_flops * world * e2e_steps / (e2e_ms * 1e-3) / 1e12
+
+    # ---- per-layer table vs same-box cuDNN (outside the timed region) -------------------------------
+    table = []
+    if rank == 0:
+        for i, L in enumerate(layers):
+            plan = plans[i]
+            unit = next(u for u in units if u[0] == i)
+            _, _, xd, wd, bd, yd = unit
+            fl = layer_flops(L, plan.p, plan.q)
+            row = {"layer": L.name, "count": L.count, "gflop": fl / 1e9,
+                   "wpk_us_live": per_layer_ms[i] / L.count * 1e3,
+                   "config": plan.config[1], "family": plan.config[0]}
+            row["wpk_tflops_live"] = fl / (row["wpk_us_live"] * 1e-6) / 1e12
+            if not args.no_cudnn:
+                sel = selector.select(plan, xd, wd, bd, yd, L.stride, L.pad, L.dil, L.groups)
+                row.update({"wpk_us": sel.own_us, "cudnn_us": sel.cudnn_us, "cudnn_variant": sel.cudnn_variant,
+                            "speedup_vs_cudnn": sel.cudnn_us / sel.own_us, "selector": sel.choice,
+                            "wpk_tflops": fl / (sel.own_us * 1e-6) / 1e12,
+                            "pct_peak": fl / (sel.own_us * 1e-6) / 1e12 / peak})
+            table.append(row)
+
+    # ---- CPU oracle baseline (rank 0, N=1 only) -----------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        cores = os.cpu_count() or 1
+        f, s = oracle_sample_step(workloads.resnet50(32), args.cpu_sample_points, cores)
+        cpu = {"value": f / s / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+               "sample": f"{args.cpu_sample_points} sampled outputs of each of the 53 ResNet-50 convs (N=32), "
+                         f"float64 7-loop oracle, OpenMP over points; {s:.1f} s"}
+
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("umma_dram_bytes_per_step")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"resnet50_v1.5_all_53_convs_n{args.batch}_bf16_nhwc_bias_relu",
+                       "global_batch": args.batch * world, "per_gpu_batch": args.batch,
+                       "parallelism": f"dp{world} (batch split along N)", "tune": args.search,
+                       "tune_budget_per_layer": args.tune_budget,
+                       "l2": "inputs larger than L2 (1.44 GB per step; every conv has its own buffers)"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "umma_conv_kernel (+ split-K fixup where chosen), all 53 launches",
+                         "peak_source": peak_src + " bf16 burst"},
+            "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "tuning_seconds": tune_seconds,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "layers": table,
+            "tune": tune_info,
+        }
+        if args.layers_json:
+            json.dump(line, open(args.layers_json, "w"), indent=1)
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

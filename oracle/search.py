@@ -216,20 +216,30 @@ def ga_run(domains, valid, evaluate, seed: int, budget: int, params: GAParams | 
     return res
 
 
-def random_run(domains, valid, evaluate, seed: int, budget: int, max_draw_factor: int = 100):
-    """Random search baseline: uniform valid samples, best-ever."""
+def random_run(domains, valid, evaluate, seed: int, budget: int, batch: int = 48,
+               max_draw_factor: int = 100):
+    """Random search baseline: uniform valid samples, best-ever. Samples are drawn
+    in batches of `batch` new distinct configs (so that a batch can be measured in parallel,
+    SURVEY.md §8(e)); duplicates cost no budget (reading c16)."""
     memo = _Memo(evaluate, budget)
     res = SearchResult(None, math.inf)
     rng = Rng(seed, 0)
-    draws = 0
-    while not memo.exhausted and draws < max_draw_factor * max(budget, 1):
-        c = _sample_valid(domains, valid, rng, 10000)
-        draws += 1
-        if memo.measure_batch([c]):
+    draws, limit = 0, max_draw_factor * max(budget, 1)
+    rounds = 0
+    while not memo.exhausted and draws < limit:
+        room = budget - len(memo.order)
+        b = []
+        while len(b) < min(batch, room) and draws < limit:
+            c = _sample_valid(domains, valid, rng, 10000)
+            draws += 1
+            if c not in memo.table and c not in b:
+                b.append(c)
+        for c in memo.measure_batch(b):
             res.measured.append(c)
             if memo.table[c] < res.best_beta:
                 res.best, res.best_beta = c, memo.table[c]
-    res.history.append({"measured": len(memo.order), "best_beta": res.best_beta})
+        rounds += 1
+        res.history.append({"round": rounds, "measured": len(memo.order), "best_beta": res.best_beta})
     return res
 
 

@@ -5,6 +5,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -101,6 +102,27 @@ static void launch_aux(int which, const void *src, void *dst, const ConvDesc &d,
     if (d.dtype == WPK_BF16) launch_aux_t<__nv_bfloat16>(which, src, dst, d, cp, sm, st);
     else if (d.dtype == WPK_F16) launch_aux_t<__half>(which, src, dst, d, cp, sm, st);
     else launch_aux_t<float>(which, src, dst, d, cp, sm, st);
+}
+
+// Deterministic pseudo-random fill in [-1, 1) (tuning buffers; values do not affect timing much).
+template <typename T>
+__global__ void fill_random_kernel(T *p, size_t n, unsigned long long seed) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        unsigned long long z = seed * 0x9E3779B97F4A7C15ull + i;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        p[i] = T((float)(z >> 40) * (1.0f / 8388608.0f) - 1.0f);
+    }
+}
+
+void fill_random_device(void *p, size_t n, int dtype, uint64_t seed, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 4096);
+    if (blocks == 0) return;
+    if (dtype == WPK_BF16) fill_random_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((__nv_bfloat16 *)p, n, seed);
+    else if (dtype == WPK_F16) fill_random_kernel<__half><<<blocks, 256, 0, st>>>((__half *)p, n, seed);
+    else fill_random_kernel<float><<<blocks, 256, 0, st>>>((float *)p, n, seed);
 }
 
 // ---- device properties ------------------------------------------------------------------------------

@@ -1,9 +1,467 @@
-// placeholder; replaced by the real tuner
-#include "wpk_internal.h"
+// wpk_conv2d_tune: the per-operator automated search (§2.3 genetic search, §2.4
+// RL-search, plus the random-search baseline of PAPER.md:161) over the plan's kernel-family gene
+// space, with fitness from CUDA-event kernel time.
+//
+// Candidate evaluation ("compile ... then execute them to get the runtime") is pure
+// measurement here: tiles are runtime parameters, so nothing is compiled per candidate. The new
+// distinct candidates of a generation are sharded over ranks (index j -> rank j mod world) and
+// their fitness records are all-gathered through the wpk_exchange_fn callback (NCCL via torch in
+// practice); every rank then runs the identical deterministic searcher update.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "tune.h"
+
+namespace wpk {
+
+void fill_random_device(void *p, size_t n, int dtype, uint64_t seed, void *stream);   // run.cu
+
+double wall_seconds() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+bool TuneCtx::time_up() const { return o.max_seconds > 0 && wall_seconds() - t_start > o.max_seconds; }
+
+std::string genes_json(const Config &c) {
+    std::string s = "[";
+    for (int g = 0; g < WPK_NUM_GENES; ++g) s += (g ? "," : "") + std::to_string(c.genes[g]);
+    return s + "]";
+}
+
+static std::string dbl(double v) {
+    if (!std::isfinite(v)) return "Infinity";
+    char b[64];
+    snprintf(b, sizeof b, "%.17g", v);
+    return b;
+}
+
+void log_line(TuneCtx &t, const std::string &s) {
+    if (t.log && t.o.rank == 0) {
+        fputs(s.c_str(), t.log);
+        fputc('\n', t.log);
+        fflush(t.log);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------------
+// measured evaluator (W warm-ups + R event-timed reps, median; L2 flushed before each rep)
+// ---------------------------------------------------------------------------------------------------
+struct GpuBench {
+    cudaStream_t st = nullptr;
+    void *x = nullptr, *w = nullptr, *b = nullptr, *y = nullptr, *ws = nullptr, *flush = nullptr;
+    size_t ws_bytes = 0, flush_bytes = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    bool ok = false;
+    std::string err;
+
+    bool init(Plan &p) {
+        const ConvDesc &d = p.d;
+        if (cudaSetDevice(p.device) != cudaSuccess) return fail_("cudaSetDevice");
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail_("stream");
+        const size_t e = d.elem();
+        size_t xb = (size_t)d.n * d.c * d.h * d.w * e, wb = (size_t)d.k * (d.c / d.g) * d.r * d.s * e;
+        size_t yb = (size_t)d.M() * d.k * e;
+        if (cudaMalloc(&x, xb) || cudaMalloc(&w, wb) || cudaMalloc(&b, d.k * e + 16) || cudaMalloc(&y, yb))
+            return fail_("cudaMalloc of tuning buffers");
+        fill_random_device(x, xb / e, d.dtype, 1, st);
+        fill_random_device(w, wb / e, d.dtype, 2, st);
+        fill_random_device(b, d.k, d.dtype, 3, st);
+        flush_bytes = (size_t)2 * device_l2_bytes(p.device);
+        if (cudaMalloc(&flush, flush_bytes)) return fail_("cudaMalloc of the L2 flush buffer");
+        if (cudaEventCreate(&e0) || cudaEventCreate(&e1)) return fail_("events");
+        if (cudaStreamSynchronize(st)) return fail_("init sync");
+        ok = true;
+        return true;
+    }
+    bool fail_(const char *m) {
+        cudaError_t e = cudaGetLastError();
+        err = std::string(m) + ": " + cudaGetErrorString(e);
+        return false;
+    }
+    ~GpuBench() {
+        for (void *ptr : {x, w, b, y, ws, flush})
+            if (ptr) cudaFree(ptr);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (st) cudaStreamDestroy(st);
+    }
+    // Wait for the stream with a host watchdog (a hung kernel aborts the tune, not the box).
+    bool sync_with_deadline(double seconds) {
+        double t0 = wall_seconds();
+        while (true) {
+            cudaError_t q = cudaStreamQuery(st);
+            if (q == cudaSuccess) return true;
+            if (q != cudaErrorNotReady) { err = cudaGetErrorString(q); return false; }
+            if (wall_seconds() - t0 > seconds) { err = "candidate exceeded the watchdog deadline"; return false; }
+        }
+    }
+    // Returns the median microseconds, +inf on a recoverable failure; sets *fatal on a sticky error.
+    double measure(Plan &p, const Config &cfg, int warmup, int reps, bool l2flush, bool *fatal) {
+        size_t need = workspace_bytes(p, cfg, false);
+        if (need > ws_bytes) {
+            if (ws) cudaFree(ws);
+            ws = nullptr;
+            ws_bytes = 0;
+            if (cudaMalloc(&ws, need) != cudaSuccess) { cudaGetLastError(); return INFINITY; }
+            ws_bytes = need;
+        }
+        p.packed_for = nullptr;
+        for (int i = 0; i < warmup; ++i)
+            if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes) < 0) return INFINITY;
+        if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
+        std::vector<float> t;
+        for (int i = 0; i < reps; ++i) {
+            if (l2flush) cudaMemsetAsync(flush, i & 0xff, flush_bytes, st);
+            cudaEventRecord(e0, st);
+            if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes) < 0) return INFINITY;
+            cudaEventRecord(e1, st);
+            if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            t.push_back(ms * 1000.f);
+        }
+        std::sort(t.begin(), t.end());
+        return t[t.size() / 2];
+    }
+};
+
+// ---------------------------------------------------------------------------------------------------
+// replay records: one JSON object per line {"family": f, "genes": [...], "beta_us": v}
+// ---------------------------------------------------------------------------------------------------
+static bool parse_record(const char *line, Config *c, double *beta) {
+    const char *g = strstr(line, "\"genes\"");
+    const char *b = strstr(line, "\"beta_us\"");
+    const char *f = strstr(line, "\"family\"");
+    if (!g || !b) return false;
+    g = strchr(g, '[');
+    if (!g) return false;
+    ++g;
+    for (int i = 0; i < WPK_NUM_GENES; ++i) {
+        char *end;
+        c->genes[i] = (int)strtol(g, &end, 10);
+        if (end == g) return false;
+        g = end;
+        while (*g == ',' || *g == ' ') ++g;
+    }
+    b = strchr(b, ':');
+    if (!b) return false;
+    ++b;
+    while (*b == ' ') ++b;
+    if (!strncmp(b, "Infinity", 8) || !strncmp(b, "null", 4)) *beta = INFINITY;
+    else *beta = strtod(b, nullptr);
+    c->family = 0;
+    if (f && (f = strchr(f, ':'))) c->family = (int)strtol(f + 1, nullptr, 10);
+    return true;
+}
+
+static bool load_replay(TuneCtx &t, const char *path) {
+    FILE *fp = fopen(path, "r");
+    if (!fp) return false;
+    char buf[4096];
+    while (fgets(buf, sizeof buf, fp)) {
+        Config c;
+        double beta;
+        if (parse_record(buf, &c, &beta)) t.replay[c] = beta;
+    }
+    fclose(fp);
+    return true;
+}
+
+// ---------------------------------------------------------------------------------------------------
+// sharded batch evaluation
+// ---------------------------------------------------------------------------------------------------
+struct Rec {
+    int32_t idx;
+    int32_t status;
+    double beta;
+};
+static_assert(sizeof(Rec) == 16, "record layout");
+
+static double evaluate_one(TuneCtx &t, const Config &c, int32_t *status) {
+    *status = 0;
+    if (!t.valid(c)) { *status = 1; return INFINITY; }
+    switch (t.o.eval_mode) {
+    case WPK_EVAL_REPLAY: {
+        auto it = t.replay.find(c);
+        if (it == t.replay.end()) { *status = 2; return INFINITY; }
+        return it->second;
+    }
+    case WPK_EVAL_SYNTHETIC: {   // SPEC.md:235-249 surface, log2(1+gene) so that 0-valued genes are defined
+        const double *s = t.o.synthetic;
+        double v = s[0];
+        for (int g = 0; g < WPK_NUM_GENES; ++g) {
+            double dlt = std::log2(1.0 + c.genes[g]) - std::log2(1.0 + s[1 + WPK_NUM_GENES + g]);
+            v += s[1 + g] * dlt * dlt;
+        }
+        return v;
+    }
+    default: {
+        bool fatal = false;
+        double b = t.gb->measure(*t.plan, c, t.o.warmup, t.o.reps, t.o.l2_flush != 0, &fatal);
+        if (fatal) { t.err = WPK_ERR_CUDA; set_error("tune: " + t.gb->err); *status = 3; }
+        else if (!std::isfinite(b)) *status = 4;
+        return b;
+    }
+    }
+}
+
+std::vector<Config> TuneCtx::measure_batch(const std::vector<Config> &cfgs) {
+    std::vector<Config> fresh;
+    for (const Config &c : cfgs) {
+        if (memo.count(c)) continue;
+        if (std::find(fresh.begin(), fresh.end(), c) != fresh.end()) continue;
+        fresh.push_back(c);
+    }
+    int room = budget - (int)order.size();
+    if ((int)fresh.size() > room) fresh.resize(std::max(room, 0));
+    if (fresh.empty() || err != WPK_OK) return {};
+    const int n = (int)fresh.size(), world = std::max(1, o.world), rank = o.rank;
+    const int per = (n + world - 1) / world;
+    std::vector<Rec> send(per), recv((size_t)per * world);
+    for (int i = 0; i < per; ++i) {
+        int j = rank + i * world;
+        if (j < n) {
+            int32_t st;
+            double b = evaluate_one(*this, fresh[j], &st);
+            send[i] = Rec{j, st, b};
+        } else {
+            send[i] = Rec{-1, 0, 0.0};
+        }
+    }
+    std::vector<double> beta(n, INFINITY);
+    if (world > 1) {
+        if (!o.exchange || o.exchange(o.exchange_ctx, send.data(), per * sizeof(Rec), recv.data()) != 0) {
+            err = WPK_ERR_INTERNAL;
+            set_error("tune: exchange (all-gather of fitness records) failed");
+            return {};
+        }
+    } else {
+        recv = send;
+    }
+    for (const Rec &r : recv)
+        if (r.idx >= 0 && r.idx < n) beta[r.idx] = r.beta;
+    for (int j = 0; j < n; ++j) {
+        memo[fresh[j]] = beta[j];
+        order.push_back(fresh[j]);
+        if (rec && rank == 0 && o.eval_mode == WPK_EVAL_MEASURED) {
+            fprintf(rec, "{\"family\": %d, \"genes\": %s, \"beta_us\": %s}\n", fresh[j].family,
+                    genes_json(fresh[j]).c_str(), dbl(beta[j]).c_str());
+        }
+        if (beta[j] < best_beta) {   // best-ever; ties keep the first measured
+            best_beta = beta[j];
+            best = fresh[j];
+            have_best = true;
+        }
+    }
+    if (rec) fflush(rec);
+    return fresh;
+}
+
+// Step1 sampler: each gene uniform over its domain, rejection until valid.
+bool sample_valid(TuneCtx &t, Rng &rng, Config *out, int max_reject) {
+    for (int i = 0; i < max_reject; ++i) {
+        Config c;
+        c.family = t.family;
+        for (int g = 0; g < WPK_NUM_GENES; ++g) {
+            const auto &d = t.sp->dom[g];
+            c.genes[g] = d[randint(rng.next(), d.size())];
+        }
+        if (t.valid(c)) { *out = c; return true; }
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------------------------------
+// GA, step by step as oracle/search.py ga_run
+// ---------------------------------------------------------------------------------------------------
+static int roulette(const std::vector<double> &P, double v) {
+    double prev = 0.0;
+    for (size_t i = 0; i < P.size(); ++i) {
+        if (prev < v && v <= P[i]) return (int)i;
+        prev = P[i];
+    }
+    return (int)P.size() - 1;
+}
+
+static wpk_status ga_search(TuneCtx &t) {
+    const wpk_tune_options &o = t.o;
+    const int popsize = std::max(1, o.ga_pop);
+    const int m_pool = o.ga_pool > 0 ? o.ga_pool : popsize;
+    std::vector<Config> pop;
+    Rng rng(o.seed, 0);
+    for (int i = 0; i < popsize; ++i) {                      // Step1
+        Config c;
+        if (!sample_valid(t, rng, &c)) return fail(WPK_ERR_EXHAUSTED, "GA Step1: no valid config sampled");
+        pop.push_back(c);
+    }
+    for (int gen = 0;; ++gen) {
+        t.measure_batch(pop);                                 // Step2 (memoised, sharded)
+        if (t.err != WPK_OK) return t.err;
+        std::vector<Config> kept;
+        std::vector<double> betas;
+        for (const Config &c : pop) {
+            auto it = t.memo.find(c);
+            if (it != t.memo.end()) { kept.push_back(c); betas.push_back(it->second); }
+        }
+        pop.swap(kept);
+        double mn = INFINITY, mx = -INFINITY, sum = 0;
+        int nf = 0;
+        for (double b : betas)
+            if (std::isfinite(b)) { mn = std::min(mn, b); mx = std::max(mx, b); sum += b; ++nf; }
+        const double spread = nf ? (mx - mn) / mn : INFINITY;
+        t.rounds = gen + 1;
+        {
+            std::string s = "{\"gen\": " + std::to_string(gen) + ", \"pop\": [";
+            for (size_t i = 0; i < pop.size(); ++i) s += (i ? "," : "") + genes_json(pop[i]);
+            s += "], \"beta\": [";
+            for (size_t i = 0; i < betas.size(); ++i) s += (i ? "," : "") + dbl(betas[i]);
+            s += "], \"best_beta\": " + dbl(t.best_beta) + ", \"mean_beta\": " + dbl(nf ? sum / nf : INFINITY) +
+                 ", \"spread\": " + dbl(spread) + ", \"measured\": " + std::to_string(t.order.size()) + "}";
+            log_line(t, s);
+        }
+        // Step4: runtimes close enough, budget, generation cap
+        if (spread < o.ga_eps || t.exhausted() || gen + 1 >= o.ga_max_gen || pop.empty() || nf == 0 || t.time_up())
+            break;
+        // Step3
+        Rng r(o.seed, (uint64_t)gen + 1);
+        const int n = (int)pop.size();
+        std::vector<double> f(n), p(n);
+        double tot = 0;
+        for (int i = 0; i < n; ++i) f[i] = std::isfinite(betas[i]) ? 1.0 / betas[i] : 0.0;
+        for (int i = 0; i < n; ++i) tot += f[i];
+        for (int i = 0; i < n; ++i) p[i] = f[i] / tot;          // Eq. (1)
+        std::vector<int> idx(n);
+        std::iota(idx.begin(), idx.end(), 0);
+        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return p[a] > p[b]; });
+        const int k = std::min(o.ga_elites, n);
+        std::vector<Config> nxt;
+        for (int i = 0; i < k; ++i) nxt.push_back(pop[idx[i]]);  // elites
+        const int m = std::min(m_pool, n);
+        double psum = 0;
+        for (int i = 0; i < m; ++i) psum += p[idx[i]];
+        std::vector<double> P(m);
+        double acc = 0;
+        for (int i = 0; i < m; ++i) { acc += p[idx[i]] / psum; P[i] = acc; }   // Eq. (2), renormalised
+        while ((int)nxt.size() < popsize) {
+            bool got = false;
+            Config child;
+            for (int tr = 0; tr < 100 && !got; ++tr) {
+                const Config &a = pop[idx[roulette(P, uniform_oc(r.next()))]];
+                const Config &b = pop[idx[roulette(P, uniform_oc(r.next()))]];
+                Config c;
+                c.family = t.family;
+                for (int g = 0; g < WPK_NUM_GENES; ++g) c.genes[g] = ((r.next() >> 63) == 0) ? a.genes[g] : b.genes[g];
+                for (int g = 0; g < WPK_NUM_GENES; ++g)
+                    if (uniform_co(r.next()) < o.ga_mutation) {
+                        const auto &d = t.sp->dom[g];
+                        c.genes[g] = d[randint(r.next(), d.size())];
+                    }
+                if (t.valid(c)) { child = c; got = true; }
+            }
+            if (!got && !sample_valid(t, r, &child)) return fail(WPK_ERR_EXHAUSTED, "GA: no valid child");
+            nxt.push_back(child);
+        }
+        pop.swap(nxt);
+    }
+    return WPK_OK;
+}
+
+// Random search (PAPER.md:161 baseline): batches of uniform valid samples, best-ever.
+static wpk_status random_search(TuneCtx &t) {
+    Rng rng(t.o.seed, 0);
+    long long draws = 0;
+    const long long limit = 100LL * std::max(t.budget, 1);
+    const int batch = std::max(1, t.o.ga_pop);
+    while (!t.exhausted() && draws < limit && !t.time_up()) {
+        std::vector<Config> b;
+        const int room = t.budget - (int)t.order.size();
+        while ((int)b.size() < std::min(batch, room) && draws < limit) {
+            Config c;
+            if (!sample_valid(t, rng, &c)) return fail(WPK_ERR_EXHAUSTED, "random search: no valid config");
+            ++draws;
+            if (!t.memo.count(c) && std::find(b.begin(), b.end(), c) == b.end()) b.push_back(c);
+        }
+        t.measure_batch(b);
+        if (t.err != WPK_OK) return t.err;
+        ++t.rounds;
+        log_line(t, "{\"round\": " + std::to_string(t.rounds) + ", \"measured\": " + std::to_string(t.order.size()) +
+                        ", \"best_beta\": " + dbl(t.best_beta) + "}");
+    }
+    return WPK_OK;
+}
+
+}  // namespace wpk
+
 using namespace wpk;
-extern "C" {
-wpk_status wpk_conv2d_tune(wpk_plan, wpk_search, int32_t, const wpk_tune_options *) { return fail(WPK_ERR_UNSUPPORTED, "tune not built yet"); }
-wpk_status wpk_ppo_loss_grad(const int32_t *, const double *, int32_t, const double *, const int32_t *, const double *, const double *, const double *, const double *, const double *, double, double *, double *) { return WPK_ERR_UNSUPPORTED; }
-wpk_status wpk_gae(int32_t, const double *, const double *, double, double, double *) { return WPK_ERR_UNSUPPORTED; }
-wpk_status wpk_observation(const wpk_conv2d_shape *, const int32_t *, double, double *) { return WPK_ERR_UNSUPPORTED; }
+
+extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t budget, const wpk_tune_options *opts) {
+    if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
+    if (budget < 1) return fail(WPK_ERR_INVALID_ARGUMENT, "budget must be >= 1");
+    if (search < WPK_SEARCH_GA || search > WPK_SEARCH_RANDOM) return fail(WPK_ERR_INVALID_ARGUMENT, "bad search");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    TuneCtx t;
+    t.plan = p;
+    if (opts) {
+        if (opts->struct_size != sizeof(wpk_tune_options))
+            return fail(WPK_ERR_INVALID_ARGUMENT, "wpk_tune_options.struct_size mismatch");
+        t.o = *opts;
+    } else {
+        wpk_tune_options_init(&t.o);
+    }
+    if (t.o.world < 1 || t.o.rank < 0 || t.o.rank >= t.o.world) return fail(WPK_ERR_INVALID_ARGUMENT, "bad rank/world");
+    if (t.o.world > 1 && !t.o.exchange) return fail(WPK_ERR_INVALID_ARGUMENT, "world > 1 needs an exchange callback");
+    if (t.o.reps < 1 || t.o.warmup < 0) return fail(WPK_ERR_INVALID_ARGUMENT, "bad timing protocol");
+    t.family = (t.o.family == WPK_FAMILY_AUTO) ? default_family(p->d) : t.o.family;
+    std::string why;
+    if (!family_applicable(p->d, t.family, &why)) return fail(WPK_ERR_INVALID_ARGUMENT, "family not applicable: " + why);
+    t.sp = &family_space(t.family);
+    t.budget = budget;
+    t.t_start = wall_seconds();
+    if (t.o.eval_mode == WPK_EVAL_REPLAY) {
+        if (!t.o.replay_path || !load_replay(t, t.o.replay_path))
+            return fail(WPK_ERR_INVALID_ARGUMENT, "replay mode needs a readable replay_path");
+    }
+    GpuBench gb;
+    if (t.o.eval_mode == WPK_EVAL_MEASURED) {
+        if (!gb.init(*p)) return fail(WPK_ERR_CUDA, "tune: " + gb.err);
+        t.gb = &gb;
+    }
+    if (t.o.record_path && t.o.rank == 0) t.rec = fopen(t.o.record_path, "a");
+    if (t.o.log_path && t.o.rank == 0) t.log = fopen(t.o.log_path, "w");
+    wpk_status st;
+    if (search == WPK_SEARCH_GA) st = ga_search(t);
+    else if (search == WPK_SEARCH_RANDOM) st = random_search(t);
+    else st = rl_search(t);
+    if (t.rec) fclose(t.rec);
+    if (t.log) fclose(t.log);
+    if (st != WPK_OK) return st;
+    if (!t.have_best || !std::isfinite(t.best_beta)) return fail(WPK_ERR_EXHAUSTED, "every candidate failed");
+    // every rank must have chosen the same config (replicated deterministic searcher state)
+    if (t.o.world > 1) {
+        Rec mine{t.best.family, 0, t.best_beta};
+        int32_t h = 0;
+        for (int g = 0; g < WPK_NUM_GENES; ++g) h = h * 1000003 + t.best.genes[g];
+        mine.status = h;
+        std::vector<Rec> all(t.o.world);
+        if (t.o.exchange(t.o.exchange_ctx, &mine, sizeof(Rec), all.data()) != 0)
+            return fail(WPK_ERR_INTERNAL, "tune: final exchange failed");
+        for (const Rec &r : all)
+            if (r.idx != mine.idx || r.status != mine.status || r.beta != mine.beta)
+                return fail(WPK_ERR_INTERNAL, "tune: ranks disagree on the chosen config");
+    }
+    p->cfg = t.best;
+    p->packed_for = nullptr;
+    p->best_us = t.best_beta;
+    p->measured = (int)t.order.size();
+    p->rounds = t.rounds;
+    p->tune_seconds = wall_seconds() - t.t_start;
+    return WPK_OK;
 }

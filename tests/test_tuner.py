@@ -1,0 +1,243 @@
+"""Tuner parity and behaviour (CPU only: replay / synthetic evaluators, no GPU).
+
+* GA and random search in C++ (wpk_conv2d_tune) reproduce oracle/search.py generation by
+  generation on the same replayed timing set and seed (both sides implement the same
+  counter-based RNG independently).
+* Sharding the evaluation over 2 gloo ranks yields the identical search and chosen config.
+* The RL learner's loss/gradient, GAE and observation match the oracle.
+* Searches beat random search on synthetic surfaces (SPEC.md:601-602 analogue)."""
+import ctypes
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import search as S
+from paper_2008_04567_b200 import Conv2dPlan, _lib as L, make_options
+
+SHAPE = dict(n=1, c=4, h=9, w=9, k=6, r=3, s=3, stride=1, pad=1)
+
+
+def simt_space():
+    names, doms = L.family_describe("simt")
+    return doms
+
+
+def valid(c):
+    return c[0] * c[1] * c[2] <= 1024
+
+
+def surface_beta(c, seed):
+    """A deterministic synthetic runtime table (the test's own evaluator)."""
+    rng = np.random.default_rng(seed)
+    doms = simt_space()
+    star = [d[int(rng.integers(len(d)))] for d in doms]
+    wts = rng.uniform(0.05, 1.0, 7)
+    v = 10.0 + sum(wi * (math.log2(ci) - math.log2(si)) ** 2 for wi, ci, si in zip(wts, c, star))
+    return float(v)
+
+
+@pytest.fixture(scope="module")
+def replay_file(tmp_path_factory):
+    doms = simt_space()
+    path = tmp_path_factory.mktemp("replay") / "simt.jsonl"
+    table = {}
+    with open(path, "w") as f:
+        for c in itertools.product(*doms):
+            if valid(c):
+                b = surface_beta(c, 3)
+                table[c] = b
+                f.write(json.dumps({"family": 0, "genes": list(c), "beta_us": b}) + "\n")
+    return str(path), table
+
+
+def _plan():
+    return Conv2dPlan(**SHAPE, layout="nchw", dtype="f32", device=0)
+
+
+def _run_cpp(search, budget, seed, replay, log, **kw):
+    plan = _plan()
+    res = plan.tune(search, budget, seed=seed, eval_mode="replay", replay_path=replay, log_path=log,
+                    family="simt", **kw)
+    return plan, res
+
+
+@pytest.mark.parametrize("seed,budget", [(0, 300), (5, 64), (9, 1000)])
+def test_ga_matches_oracle_generation_by_generation(replay_file, tmp_path, seed, budget):
+    path, table = replay_file
+    log = str(tmp_path / "ga.jsonl")
+    plan, res = _run_cpp("ga", budget, seed, path, log)
+    ora = S.ga_run(simt_space(), valid, lambda c: table[c], seed=seed, budget=budget)
+    gens = [json.loads(l) for l in open(log)]
+    assert len(gens) == len(ora.history)
+    for g, h in zip(gens, ora.history):
+        assert g["pop"] == h["pop"]
+        assert g["beta"] == h["beta"]
+        assert g["best_beta"] == h["best_beta"] and g["measured"] == h["measured"]
+    assert tuple(res.genes) == ora.best and res.best_us == ora.best_beta
+    assert res.measured == len(ora.measured) <= budget
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_random_matches_oracle(replay_file, tmp_path, seed):
+    path, table = replay_file
+    plan, res = _run_cpp("random", 200, seed, path, str(tmp_path / "r.jsonl"))
+    ora = S.random_run(simt_space(), valid, lambda c: table[c], seed=seed, budget=200)
+    assert tuple(res.genes) == ora.best and res.best_us == ora.best_beta and res.measured == 200
+
+
+def test_ga_near_enumerated_optimum(replay_file):
+    path, table = replay_file
+    opt = min(table.values())
+    plan, res = _run_cpp("ga", 2000, 0, path, None)
+    assert res.best_us <= 1.05 * opt
+
+
+def _worker(rank, world, port, path, budget, search, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2008_04567_b200 import dist as wdist
+    plan = Conv2dPlan(**SHAPE, layout="nchw", dtype="f32", device=0)
+    log = out + f".log{rank}"
+    res = plan.tune(search, budget, seed=4, eval_mode="replay", replay_path=path, log_path=log, family="simt",
+                    rank=rank, world=world, **wdist.make_exchange())
+    with open(out + f".{rank}", "w") as f:
+        json.dump({"genes": res.genes, "best": res.best_us, "measured": res.measured}, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("search", ["ga", "random"])
+def test_world_size_invariance_gloo(replay_file, tmp_path, search):
+    path, table = replay_file
+    budget = 150
+    plan, res1 = _run_cpp(search, budget, 4, path, str(tmp_path / "w1.jsonl"))
+    out = str(tmp_path / "w2")
+    mp.start_processes(_worker, args=(2, 29517 + hash(search) % 100, path, budget, search, out), nprocs=2,
+                       start_method="spawn")
+    r0, r1 = (json.load(open(out + f".{r}")) for r in (0, 1))
+    assert r0 == r1
+    assert r0["genes"] == res1.genes and r0["best"] == res1.best_us and r0["measured"] == res1.measured
+    assert open(out + ".log0").read() == open(str(tmp_path / "w1.jsonl")).read()
+
+
+def _worker_rl(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2008_04567_b200 import dist as wdist
+    plan = Conv2dPlan(**SHAPE, layout="nchw", dtype="f32", device=0)
+    syn = [10.0] + [0.5] * 7 + [8, 4, 2, 2, 1, 2, 4]
+    res = plan.tune("rl", 120, seed=2, eval_mode="synthetic", synthetic=syn, family="simt", rank=rank, world=world,
+                    rl_hidden=[32, 32, 32, 32], rl_horizon=8, rl_envs=4, **wdist.make_exchange())
+    with open(out + f".{rank}", "w") as f:
+        json.dump({"genes": res.genes, "best": res.best_us, "measured": res.measured}, f)
+    dist.destroy_process_group()
+
+
+def test_rl_world_size_invariance_gloo(tmp_path):
+    syn = [10.0] + [0.5] * 7 + [8, 4, 2, 2, 1, 2, 4]
+    plan = _plan()
+    res1 = plan.tune("rl", 120, seed=2, eval_mode="synthetic", synthetic=syn, family="simt",
+                     rl_hidden=[32, 32, 32, 32], rl_horizon=8, rl_envs=4)
+    out = str(tmp_path / "rl")
+    mp.start_processes(_worker_rl, args=(2, 29611, out), nprocs=2, start_method="spawn")
+    r0, r1 = (json.load(open(out + f".{r}")) for r in (0, 1))
+    assert r0 == r1 and r0["genes"] == res1.genes and r0["best"] == res1.best_us
+
+
+def test_rl_deterministic_and_budget():
+    syn = [10.0] + [0.5] * 7 + [8, 4, 2, 2, 1, 2, 4]
+    outs = []
+    for _ in range(2):
+        plan = _plan()
+        r = plan.tune("rl", 100, seed=3, eval_mode="synthetic", synthetic=syn, family="simt",
+                      rl_hidden=[32, 64, 64, 32], rl_horizon=16, rl_envs=2)
+        outs.append((r.genes, r.best_us, r.measured))
+        assert r.measured <= 100
+    assert outs[0] == outs[1]
+
+
+# --- learner primitives vs the oracle -----------------------------------------------------------
+def _flat(params):
+    return np.concatenate([np.concatenate([W.ravel(), b]) for W, b in params])
+
+
+@pytest.mark.parametrize("use_mask", [False, True])
+def test_ppo_loss_grad_matches_oracle(use_mask):
+    rng = np.random.default_rng(7)
+    A = 5
+    dims = [17, 12, 10, 9, 8, A + 1]
+    params = [(rng.standard_normal((dims[i + 1], dims[i])) * 0.4, rng.standard_normal(dims[i + 1]) * 0.1)
+              for i in range(5)]
+    B = 9
+    obs = rng.standard_normal((B, 17))
+    act = rng.integers(0, A, B).astype(np.int32)
+    old_logp = np.log(rng.uniform(0.1, 0.4, B))
+    adv = rng.standard_normal(B)
+    v_old = rng.standard_normal(B)
+    keep = 0.85
+    mask = (rng.uniform(size=(B, dims[4])) < keep).astype(np.float64) if use_mask else None
+    consts = S.PPOConsts(c1=0.15, c2=20.0, clip=0.2)
+    loss_o, grads_o = S.ppo_grad(params, obs, act, old_logp, adv, v_old, consts, mask, keep if use_mask else 1.0)
+    lib = L.load()
+    P = _flat(params)
+    g = np.zeros_like(P)
+    loss = ctypes.c_double()
+    dp = lambda a: np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    dims_c = (ctypes.c_int32 * 6)(*dims)
+    cs = np.array([0.15, 20.0, 0.2])
+    mk = np.ascontiguousarray(mask) if use_mask else None
+    L.check(lib.wpk_ppo_loss_grad(dims_c, dp(P), B, dp(obs), act.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                  dp(old_logp), dp(adv), dp(v_old), dp(cs), dp(mk) if use_mask else None,
+                                  keep if use_mask else 1.0, ctypes.byref(loss),
+                                  g.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    assert loss.value == pytest.approx(loss_o, rel=1e-12, abs=1e-12)
+    np.testing.assert_allclose(g, _flat(grads_o), rtol=1e-9, atol=1e-12)
+
+
+def test_gae_and_observation_match_oracle():
+    lib = L.load()
+    rng = np.random.default_rng(8)
+    for T in (1, 2, 7, 16):
+        r = rng.standard_normal(T)
+        v = rng.standard_normal(T + 1)
+        out = np.zeros(T)
+        dp = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        L.check(lib.wpk_gae(T, dp(r), dp(v), 0.99, 0.95, dp(out)))
+        np.testing.assert_allclose(out, S.gae(r.tolist(), v.tolist(), 0.99, 0.95)[0], rtol=0, atol=1e-12)
+    shp = L.make_shape(32, 64, 56, 56, 128, 3, 3, 2, 1)
+    genes = [128, 4, 1, 0, 1, 2, 128]
+    o = np.zeros(17)
+    L.check(lib.wpk_observation(ctypes.byref(shp), (ctypes.c_int32 * 7)(*genes), 12.5,
+                                o.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    want = S.observation((32, 64, 128, 3, 3, 56, 56, 2, 1), genes, 12.5)
+    np.testing.assert_allclose(o, want, rtol=0, atol=1e-15)
+
+
+# --- search behaviour on synthetic surfaces (SPEC.md:601-602 analogue) ---------------------------
+def test_searches_beat_random_on_synthetic_surfaces():
+    doms = simt_space()
+    wins_ga = wins_rl = 0
+    for seed in range(10):
+        rng = np.random.default_rng(seed)
+        star = [d[int(rng.integers(len(d)))] for d in doms]
+        while not valid(star):
+            star = [d[int(rng.integers(len(d)))] for d in doms]
+        syn = [10.0] + list(rng.uniform(0.05, 1.0, 7)) + star
+        kw = dict(eval_mode="synthetic", synthetic=syn, family="simt", seed=seed)
+        rnd = _plan().tune("random", 256, **kw).best_us
+        ga = _plan().tune("ga", 256, **kw).best_us
+        rl = _plan().tune("rl", 256, rl_hidden=[64, 64, 64, 64], rl_horizon=16, rl_envs=4, rl_lr=1e-3,
+                          rl_alpha_mode=1, **kw).best_us
+        wins_ga += ga <= rnd
+        wins_rl += rl <= rnd
+    assert wins_ga >= 9
+    print("rl wins", wins_rl)
