@@ -166,6 +166,9 @@ def main():
     ap.add_argument("--ref-points", type=int, default=256)
     ap.add_argument("--cpu-sample-points", type=int, default=128)
     ap.add_argument("--layers-json", default=None, help="also write the per-layer table here")
+    ap.add_argument("--layer-events", action="store_true",
+                    help="record events between layers inside the timed region (defeats PDL overlap); by "
+                         "default per-layer times come from an instrumented pass right after the timed steps")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -187,7 +190,7 @@ def main():
 
     peaks, peak_src = load_peaks()
     layers = workloads.resnet50(args.batch)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)
 
     # ---- plans, inputs (resident in HBM), tuning -------------------------------------------------
     t_tune0 = time.perf_counter()
@@ -215,19 +218,32 @@ def main():
 
     total_flops = sum(layer_flops(L, plans[i].p, plans[i].q) * L.count for i, L in enumerate(layers))
 
+    # Each conv is captured once into a CUDA graph (launch overhead out of the timed region; "CUDA
+    # streams and graphs instead of a tracing compiler"). A warm-up eager run first packs any weights.
+    for (i, plan, xd, wd, bd, yd) in units:
+        plan.run(xd, wd, bd, yd, stream=stream)
+    torch.cuda.synchronize()
+    graphs, graph_launches = [], []
+    for (i, plan, xd, wd, bd, yd) in units:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            plan.run(xd, wd, bd, yd, stream=stream)
+        graphs.append(g)
+        graph_launches.append(plan.last_launch_count())
+    torch.cuda.synchronize()
+
     def step(events=None):
-        launches = 0
-        for j, (i, plan, xd, wd, bd, yd) in enumerate(units):
+        for j, g in enumerate(graphs):
             if events is not None:
                 events[j][0].record(stream)
-            plan.run(xd, wd, bd, yd, stream=stream)
+            g.replay()
             if events is not None:
                 events[j][1].record(stream)
-            launches += plan.last_launch_count()
-        return launches
+        return sum(graph_launches)
 
-    for _ in range(args.warmup):
-        step()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
     torch.cuda.synchronize()
 
     # ---- timed region ------------------------------------------------------------------------------
@@ -241,8 +257,9 @@ def main():
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         launches = 0
-        for k in range(args.steps):
-            launches += step(ev[k])
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                launches += step(ev[k] if args.layer_events else None)
         t1.record(stream)
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
@@ -255,8 +272,16 @@ def main():
     value = total_flops * world * args.steps / (ms * 1e-3) / 1e12
 
     # per-layer device times from the live events (average over steps)
-    per_unit_ms = [statistics.mean(ev[k][j][0].elapsed_time(ev[k][j][1]) for k in range(args.steps))
-                   for j in range(len(units))]
+    if not args.layer_events:   # per-layer split from instrumented passes right after the timed steps
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                step(ev[k])
+        torch.cuda.synchronize()
+        per_unit_ms = [statistics.mean(ev[k][j][0].elapsed_time(ev[k][j][1]) for k in range(args.steps))
+                       for j in range(len(units))]
+    else:
+        per_unit_ms = [statistics.mean(ev[k][j][0].elapsed_time(ev[k][j][1]) for k in range(args.steps))
+                       for j in range(len(units))]
     per_layer_ms = [0.0] * len(layers)
     for j, (i, *_rest) in enumerate(units):
         per_layer_ms[i] += per_unit_ms[j]
@@ -275,6 +300,7 @@ def main():
         d2h += yh.numel() * yh.element_size()
     for (plan, xh, wd, bd, yh) in host:     # warm-up of the host path
         plan.run_host(xh, wd, bd, yh, stream=stream)
+    torch.cuda.synchronize()
     e2e_steps = max(1, min(args.steps, 5))
     if pg is not None:
         torch.distributed.barrier()
@@ -306,7 +332,8 @@ def main():
                    "config": plan.config[1], "family": plan.config[0]}
             row["wpk_tflops_live"] = fl / (row["wpk_us_live"] * 1e-6) / 1e12
             if not args.no_cudnn:
-                sel = selector.select(plan, xd, wd, bd, yd, L.stride, L.pad, L.dil, L.groups)
+                with torch.cuda.stream(stream):
+                    sel = selector.select(plan, xd, wd, bd, yd, L.stride, L.pad, L.dil, L.groups)
                 row.update({"wpk_us": sel.own_us, "cudnn_us": sel.cudnn_us, "cudnn_variant": sel.cudnn_variant,
                             "speedup_vs_cudnn": sel.cudnn_us / sel.own_us, "selector": sel.choice,
                             "wpk_tflops": fl / (sel.own_us * 1e-6) / 1e12,

@@ -71,9 +71,10 @@ typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 
  *   WPK_FAMILY_SIMT : direct conv on CUDA cores, genes = the paper's
  *                     (T_x, T_y, T_z, Tile_x, Tile_y, Tile_z, Tile_rz), T_x*T_y*T_z<=1024
  *   WPK_FAMILY_UMMA : tcgen05 implicit GEMM, genes = (BLOCK_N, STAGES, SPLIT_K, RASTER,
- *                     CTAS_PER_SM, ACC_STAGES, BLOCK_M)
+ *                     A_MODE, ACC_STAGES, BLOCK_M); A_MODE 0 = TMA im2col producer (plain TMA
+ *                     tiles for 1x1/s1/p0), 1 = explicit im2col matrix (small-C layers)
  *   WPK_FAMILY_DW   : depthwise (groups == C == K), genes = (VEC_C, PIX_PER_THREAD, THREADS,
- *                     ROWS_PER_CTA, -, -, -)                                                      */
+ *                     -, -, -, -)                                                      */
 typedef enum { WPK_FAMILY_SIMT = 0, WPK_FAMILY_UMMA = 1, WPK_FAMILY_DW = 2, WPK_FAMILY_AUTO = -1 } wpk_family;
 
 /* Operator shape: the first 9 entries of the paper's O_conv generalised with

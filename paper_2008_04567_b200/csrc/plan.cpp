@@ -5,6 +5,7 @@
 // s = {c_0..c_{n-1}}: PAPER.md:64-65; "verified first in order to meet certain constraints ...
 // the product of all dimension values is positive and <= 1024": PAPER.md:68.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -70,11 +71,11 @@ static Space make_space(int family) {
         sp.names = {"T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"};
     } else if (family == WPK_FAMILY_UMMA) {
         sp.dom = {{16, 32, 64, 96, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8}, {1, 2, 4, 8, 16},
-                  {0, 1}, {1, 2}, {1, 2}, {128}};
-        sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "RASTER", "CTAS_PER_SM", "ACC_STAGES", "BLOCK_M"};
+                  {0, 1}, {0, 1}, {1, 2}, {128, 256}};
+        sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "RASTER", "A_MODE", "ACC_STAGES", "BLOCK_M"};
     } else {
-        sp.dom = {{1, 2, 4, 8}, {1, 2, 4}, {64, 128, 256, 512}, {1, 2, 4}, {0}, {0}, {0}};
-        sp.names = {"VEC_C", "PIX_PER_THREAD", "THREADS", "ROWS_PER_CTA", "-", "-", "-"};
+        sp.dom = {{1, 2, 4, 8}, {1, 2, 4}, {64, 128, 256, 512}, {1}, {0}, {0}, {0}};
+        sp.names = {"VEC_C", "PIX_PER_THREAD", "THREADS", "-", "-", "-", "-"};
     }
     return sp;
 }
@@ -97,10 +98,7 @@ static bool in_domain(const Space &sp, const Config &cfg, std::string *why) {
 
 bool family_applicable(const ConvDesc &d, int family, std::string *why) {
     auto no = [&](const char *m) { if (why) *why = m; return false; };
-    if (family == WPK_FAMILY_SIMT) {
-        if (d.g != 1 && family != WPK_FAMILY_SIMT) return no("groups");
-        return true;   // the SIMT kernel handles every valid shape, layout and dtype
-    }
+    if (family == WPK_FAMILY_SIMT) return true;   // the SIMT kernel handles every valid shape, layout and dtype
     if (family == WPK_FAMILY_DW) {
         if (!(d.g == d.c && d.g == d.k && d.g > 1)) return no("DW family needs groups == C == K");
         return true;
@@ -130,11 +128,20 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->stages = cfg.genes[1];
     g->splits = cfg.genes[2];
     g->raster = cfg.genes[3];
-    g->ctas_per_sm = cfg.genes[4];
+    g->ctas_per_sm = 1;
+    g->a_mode = cfg.genes[4];
     g->acc_stages = cfg.genes[5];
-    g->cpad = round_up(d.c, 16 / e);    // TMA global strides must be multiples of 16 B
-    g->c_blocks = (g->cpad + g->bk - 1) / g->bk;
-    g->num_kb = d.r * d.s * g->c_blocks;
+    if (g->a_mode == 1) {
+        // explicit im2col: A = [M][R*S*C] materialised in the workspace, then a plain GEMM
+        g->cpad = round_up(d.r * d.s * d.c, 8);   // 8-element vectors in the im2col kernel
+        g->c_blocks = (g->cpad + g->bk - 1) / g->bk;
+        g->num_kb = g->c_blocks;
+        if ((double)d.M() * g->cpad * e > 4.0e9) return no("explicit im2col matrix larger than 4 GB");
+    } else {
+        g->cpad = round_up(d.c, 16 / e);    // TMA global strides must be multiples of 16 B
+        g->c_blocks = (g->cpad + g->bk - 1) / g->bk;
+        g->num_kb = d.r * d.s * g->c_blocks;
+    }
     if (g->splits > g->num_kb) return no("SPLIT_K larger than the number of K blocks");
     g->kb_per_split = (g->num_kb + g->splits - 1) / g->splits;
     if ((long long)(g->splits - 1) * g->kb_per_split >= g->num_kb) return no("SPLIT_K leaves an empty split");
@@ -142,10 +149,27 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->n_tiles = (d.k + g->bn - 1) / g->bn;
     g->work = (long long)g->m_tiles * g->n_tiles * g->splits;
     size_t stage = (size_t)g->bm * 128 + (size_t)g->bn * 128;
-    g->smem_bytes = 1024 /*align slack*/ + (size_t)g->stages * stage + 256 /*barriers*/;
+    if (g->bm == 256 && g->a_mode == 0 && !(d.r == 1 && d.s == 1 && d.sh == 1 && d.sw == 1 && d.ph == 0 && d.pw == 0))
+        ;   // a 256-pixel im2col box is one TMA (pixelsPerColumn <= 1024)
+    // A operand: a 1x1 / stride-1 / unpadded conv is a plain GEMM on x viewed as [N*H*W][C]
+    g->a_tiled = (g->a_mode == 1 || (d.r == 1 && d.s == 1 && d.sh == 1 && d.sw == 1 && d.ph == 0 && d.pw == 0 &&
+                                      g->cpad == d.c && !getenv("WPK_A_IM2COL"))) ? 1 : 0;
+    // epilogue through shared memory + TMA store: NHWC output, whole 128-byte column chunks
+    const int out_elem = (g->splits > 1) ? 4 : e;
+    const int cw = 128 / out_elem;
+    g->epi_tma = (d.layout == WPK_NHWC && g->bn % cw == 0 && ((long long)d.k * out_elem) % 16 == 0 &&
+                  !getenv("WPK_EPI_DIRECT")) ? 1 : 0;
+    size_t off = (size_t)g->stages * stage;
+    g->epi_off = off;
+    if (g->epi_tma) off += 8 * 2 * 32 * 128;   // 8 epilogue warps x 2 buffers x 32 rows x 128 B
+    g->bias_off = off;
+    off += ((size_t)d.k * 4 + 15) / 16 * 16;
+    g->bar_off = off;
+    off += 256;
+    g->smem_bytes = 1024 /*align slack*/ + off;
     size_t smem_cap = (g->ctas_per_sm == 1) ? 227 * 1024 : 113 * 1024;
     if (g->smem_bytes > smem_cap) return no("STAGES x tile exceeds shared memory");
-    int cols = g->acc_stages * g->bn;
+    int cols = g->acc_stages * (g->bm / 128) * g->bn;
     int alloc = 32;
     while (alloc < cols) alloc <<= 1;
     g->tmem_cols = alloc;
@@ -165,6 +189,10 @@ bool config_valid(const ConvDesc &d, const Config &cfg, std::string *why) {
             if (why) *why = "T_x*T_y*T_z must be in [1, 1024]";
             return false;
         }
+        if (d.elem() == 2 && gn[6] != 1) {   // 16-bit SIMT variants are instantiated with Tile_rz = 1 only
+            if (why) *why = "Tile_rz must be 1 for 16-bit dtypes on the SIMT family";
+            return false;
+        }
         long long gy = (d.p + (long long)gn[1] * gn[4] - 1) / ((long long)gn[1] * gn[4]);
         long long gz = (long long)d.n * ((d.k + (long long)gn[2] * gn[5] - 1) / ((long long)gn[2] * gn[5]));
         if (gy > 65535 || gz > 65535) { if (why) *why = "grid y/z exceeds 65535"; return false; }
@@ -178,6 +206,7 @@ bool config_valid(const ConvDesc &d, const Config &cfg, std::string *why) {
     int vec = gn[0];
     if (d.c % vec) { if (why) *why = "VEC_C must divide C"; return false; }
     if (d.elem() * vec > 16) { if (why) *why = "VEC_C*elem > 16 bytes"; return false; }
+    if (d.layout == WPK_NCHW && vec != 1) { if (why) *why = "NCHW depthwise needs VEC_C = 1"; return false; }
     return true;
 }
 
@@ -196,18 +225,22 @@ Config default_config(const ConvDesc &d, int family) {
         return c;
     }
     if (family == WPK_FAMILY_DW) {
-        int vec = 16 / d.elem();
+        int vec = (d.layout == WPK_NCHW) ? 1 : 16 / d.elem();
         while (vec > 1 && d.c % vec) vec >>= 1;
         int g[7] = {vec, 1, 256, 1, 0, 0, 0};
         std::memcpy(c.genes, g, sizeof g);
         return c;
     }
-    // UMMA: smallest BLOCK_N covering K (max 256), deepest pipeline that fits, split-K when the
-    // tile count cannot fill the machine, double-buffered accumulators.
-    int bn = 256;
-    for (int v : {32, 64, 128, 256})
-        if (v >= d.k) { bn = v; break; }
-    c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = 1;
+    // UMMA: the widest BLOCK_N (<= 256, covering K) that still gives about one wave of tiles; split-K
+    // when even that cannot fill the machine; deepest pipeline that fits; double-buffered TMEM.
+    const long long m_tiles = (d.M() + 127) / 128;
+    int bn = 16;
+    for (int v : {256, 128, 64, 32, 16}) {
+        if (v > 16 && v / 2 >= d.k) continue;              // do not pad K by more than 2x
+        bn = v;
+        if (m_tiles * ((d.k + v - 1) / v) >= 120) break;
+    }
+    c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c < 16) ? 1 : 0;
     c.genes[5] = 2; c.genes[6] = 128;
     for (int st = 8; st >= 2; --st) {
         c.genes[1] = st;
@@ -216,11 +249,13 @@ Config default_config(const ConvDesc &d, int family) {
     UmmaGeom g;
     if (umma_geometry(d, c, &g, nullptr)) {
         long long tiles = (long long)g.m_tiles * g.n_tiles;
-        for (int sp : {16, 8, 4, 2}) {
-            if (tiles * sp <= 2 * 148 && tiles * 4 < 148) {
+        if (tiles < 100) {
+            for (int sp : {2, 4, 8, 16}) {
                 Config t = c;
                 t.genes[2] = sp;
-                if (config_valid(d, t, nullptr)) { c = t; break; }
+                if (!config_valid(d, t, nullptr)) break;
+                c = t;
+                if (tiles * sp >= 120) break;
             }
         }
     }

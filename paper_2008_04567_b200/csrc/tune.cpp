@@ -23,6 +23,7 @@
 namespace wpk {
 
 void fill_random_device(void *p, size_t n, int dtype, uint64_t seed, void *stream);   // run.cu
+void l2_flush_device(const void *buf, size_t bytes, void *sink, void *stream);          // run.cu
 
 double wall_seconds() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -75,7 +76,8 @@ struct GpuBench {
         fill_random_device(w, wb / e, d.dtype, 2, st);
         fill_random_device(b, d.k, d.dtype, 3, st);
         flush_bytes = (size_t)2 * device_l2_bytes(p.device);
-        if (cudaMalloc(&flush, flush_bytes)) return fail_("cudaMalloc of the L2 flush buffer");
+        if (cudaMalloc(&flush, flush_bytes + 256)) return fail_("cudaMalloc of the L2 flush buffer");
+        cudaMemsetAsync(flush, 1, flush_bytes + 256, st);
         if (cudaEventCreate(&e0) || cudaEventCreate(&e1)) return fail_("events");
         if (cudaStreamSynchronize(st)) return fail_("init sync");
         ok = true;
@@ -119,7 +121,7 @@ struct GpuBench {
         if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
         std::vector<float> t;
         for (int i = 0; i < reps; ++i) {
-            if (l2flush) cudaMemsetAsync(flush, i & 0xff, flush_bytes, st);
+            if (l2flush) l2_flush_device(flush, flush_bytes, (char *)flush + flush_bytes, st);
             cudaEventRecord(e0, st);
             if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes) < 0) return INFINITY;
             cudaEventRecord(e1, st);

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstring>
 #include <string>
 
 #include "ptx.cuh"
@@ -51,6 +52,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, __nv_bfloat16 *) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t *>(&h);
 }
+__device__ __forceinline__ uint32_t pack2(float, float, float *) { return 0u; }   // unused (fp32 out)
 __device__ __forceinline__ void st_out(__half *p, float v) { *p = __float2half_rn(v); }
 __device__ __forceinline__ void st_out(__nv_bfloat16 *p, float v) { *p = __float2bfloat16_rn(v); }
 __device__ __forceinline__ void st_out(float *p, float v) { *p = v; }
@@ -72,21 +74,143 @@ __device__ __forceinline__ WorkPos decode_work(long long w, const UmmaArgs &a) {
     return r;
 }
 
+// Epilogue for one 32-row x (column chunk) slab: TMEM -> registers -> (+bias, ReLU, round) ->
+// swizzled smem staging -> TMA store (epi_tma), or direct global stores.
+template <typename T>
+struct EpiCtx {
+    const UmmaArgs *a;
+    const float *sBias;
+    uint8_t *sEpi;        // this warp's 2 x 4 KB staging buffers
+    uint32_t ebuf;
+    int lane;
+};
+
+template <typename T>
+__device__ __forceinline__ void epi_chunk_tma(EpiCtx<T> &E, const CUtensorMap *tmY, uint32_t taddr, int k0, int mrow,
+                                              int split, bool final_out) {
+    const UmmaArgs &a = *E.a;
+    uint32_t pk[32];
+    if (final_out && sizeof(T) == 2) {
+#pragma unroll
+        for (int sub = 0; sub < 4; ++sub) {
+            float v[16];
+            ptx::tmem_ld16(taddr + sub * 16, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                v[j] += E.sBias[min(k0 + sub * 16 + j, a.K - 1)];
+                if (a.epilogue == 2) v[j] = fmaxf(v[j], 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pk[sub * 8 + j] = pack2(v[2 * j], v[2 * j + 1], (T *)nullptr);
+        }
+    } else {
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub) {
+            float v[16];
+            ptx::tmem_ld16(taddr + sub * 16, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                if (final_out) {
+                    v[j] += E.sBias[min(k0 + sub * 16 + j, a.K - 1)];
+                    if (a.epilogue == 2) v[j] = fmaxf(v[j], 0.f);
+                }
+                pk[sub * 16 + j] = __float_as_uint(v[j]);
+            }
+        }
+    }
+    // staging buffer reuse: the TMA store issued two chunks ago must have finished reading it
+    if (E.lane == 0) ptx::bulk_wait_read<1>();
+    __syncwarp();
+    uint8_t *bufp = E.sEpi + E.ebuf * 4096;
+    const uint32_t buf = ptx::smem_u32(bufp) + (uint32_t)E.lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        ptx::st_shared_v4(buf + ((uint32_t)(j ^ (E.lane & 7)) << 4), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (E.lane == 0) {
+        if (final_out) ptx::tma_store_2d(tmY, bufp, k0, mrow);
+        else ptx::tma_store_3d(tmY, bufp, k0, mrow, split);
+        ptx::bulk_commit();
+    }
+    E.ebuf ^= 1;
+}
+
+template <typename T>
+__device__ __forceinline__ void epi_chunk_direct(EpiCtx<T> &E, uint32_t taddr, int k0, long long m, int split,
+                                                 bool final_out) {
+    const UmmaArgs &a = *E.a;
+    float v[16];
+    ptx::tmem_ld16(taddr, v);
+    if (m >= a.M) return;
+    const bool full16 = (k0 + 16 <= a.K);
+    if (!final_out) {
+        float *dst = a.partial + ((long long)split * a.M + m) * a.K + k0;
+        if (full16 && a.vec_ok) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+                *reinterpret_cast<float4 *>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (k0 + j < a.K) dst[j] = v[j];
+        }
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        v[j] += E.sBias[min(k0 + j, a.K - 1)];
+        if (a.epilogue == 2) v[j] = fmaxf(v[j], 0.f);
+    }
+    T *y = static_cast<T *>(a.y);
+    if (a.out_nchw) {
+        const long long nimg = m / a.PQ;
+        const long long base = nimg * (long long)a.K * a.PQ + (m - nimg * a.PQ);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (k0 + j < a.K) st_out(y + base + (long long)(k0 + j) * a.PQ, v[j]);
+        return;
+    }
+    T *dst = y + m * a.K + k0;
+    if (full16 && a.vec_ok) {
+        if constexpr (sizeof(T) == 2) {
+            uint32_t u[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) u[j] = pack2(v[2 * j], v[2 * j + 1], (T *)nullptr);
+            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(u[0], u[1], u[2], u[3]);
+            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(u[4], u[5], u[6], u[7]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+                *reinterpret_cast<float4 *>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (k0 + j < a.K) st_out(dst + j, v[j]);
+    }
+}
+
+// 12 warps: 0 = A producer, 1 = TMEM allocator + MMA issuer, 2 = B producer, 3 = spare,
+// 4..11 = epilogue (two groups of four; warp w reads TMEM lanes [32*(w%4), +32)).
 template <int DT>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(384, 1)
     umma_conv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ UmmaArgs a) {
+                     const __grid_constant__ CUtensorMap tmY, const __grid_constant__ UmmaArgs a) {
     using T = typename OutT<DT>::T;
     constexpr bool kTF32 = (DT == DT_TF32);
-    constexpr uint32_t A_BYTES = 128 * 128;   // BLOCK_M rows x 128 B
 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
     uint8_t *smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+    const uint32_t a_bytes = (uint32_t)a.bm * 128u;
     const uint32_t b_bytes = (uint32_t)a.bn * 128u;
+    const int nsub = a.bm / 128;                                       // 128-row MMAs per tile
     uint8_t *smA = smem;
-    uint8_t *smB = smem + (size_t)a.stages * A_BYTES;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smB + (size_t)a.stages * b_bytes);
+    uint8_t *smB = smem + (size_t)a.stages * a_bytes;
+    uint8_t *sEpi = smem + a.epi_off;                                  // [8 warps][2][32 rows][128 B]
+    float *sBias = reinterpret_cast<float *>(smem + a.bias_off);      // [K]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.bar_off);
     uint64_t *full = bars;            // [8]
     uint64_t *empty = bars + 8;       // [8]
     uint64_t *tfull = bars + 16;      // [2]
@@ -94,17 +218,20 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 20);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long *dbg = a.dbg ? a.dbg + blockIdx.x * 8 : nullptr;
+    if (dbg && threadIdx.x == 0) dbg[0] = ptx::globaltimer();
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
+        if (a.epi_tma) ptx::prefetch_tmap(&tmY);
         for (int s = 0; s < a.stages; ++s) {
-            ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], 1);
+            ptx::mbar_init(&full[s], 2);       // A producer + B producer
+            ptx::mbar_init(&empty[s], 1);      // MMA commit
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&tfull[s], 1);
-            ptx::mbar_init(&tempty[s], 4);
+            ptx::mbar_init(&tempty[s], 8);     // 8 epilogue warps
         }
         ptx::fence_mbar_init();
     }
@@ -112,35 +239,62 @@ __global__ void __launch_bounds__(192, 1)
         ptx::tmem_alloc(tmem_holder, a.tmem_cols);
         ptx::tmem_relinquish();
     }
+    // Programmatic dependent launch: everything above overlapped the previous kernel's tail; inputs
+    // (x, w, b) may be produced by it, so wait for its completion before the first global read.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (warp >= 4) {   // bias -> smem once (fp32); zero when there is no bias or for split-K partials
+        const T *bias = static_cast<const T *>(a.bias);
+        for (int k = threadIdx.x - 128; k < a.K; k += 256)
+            sBias[k] = (a.epilogue >= 1 && a.splits == 1) ? ld_bias(bias, k) : 0.f;
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    if (dbg && threadIdx.x == 0) dbg[1] = ptx::globaltimer();
 
-    if (warp == 0) {
-        // ===================== TMA producer =====================
+    if (warp == 0 || warp == 2) {
+        // ===================== TMA producers: warp 0 -> A (activations), warp 2 -> B (weights) ====
         if (lane == 0) {
+            const bool isA = (warp == 0);
             uint32_t stage = 0, phase = 0;
-            const uint32_t tx_bytes = A_BYTES + b_bytes;
+            const uint32_t tx = isA ? a_bytes : b_bytes;
+            uint8_t *dst0 = isA ? smA : smB;
             for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
                 const WorkPos wp = decode_work(w, a);
-                const long long m0 = (long long)wp.mt * 128;
+                const long long m0 = (long long)wp.mt * a.bm;
                 const int n0 = wp.nt * a.bn;
-                const int nimg = (int)(m0 / a.PQ);
-                const int rem = (int)(m0 % a.PQ);
-                const int p = rem / a.Q, q = rem % a.Q;
-                const int wc = q * a.stride_w - a.pad_w, hc = p * a.stride_h - a.pad_h;
+                int wc = 0, hc = 0, nimg = 0;
+                if (isA && !a.a_tiled) {
+                    nimg = (int)(m0 / a.PQ);
+                    const int rem = (int)(m0 - (long long)nimg * a.PQ);
+                    const int p = rem / a.Q, q = rem - (rem / a.Q) * a.Q;
+                    wc = q * a.stride_w - a.pad_w;
+                    hc = p * a.stride_h - a.pad_h;
+                }
                 const int kb0 = wp.split * a.kb_per_split;
                 const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+                // (r, s, c-block) of kb0, then advanced incrementally (no divisions in the k loop)
+                int cb = kb0 % a.c_blocks;
+                int rs = kb0 / a.c_blocks;
+                int r = rs / a.S, s = rs % a.S;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    const int cb = kb % a.c_blocks;
-                    const int rs = kb / a.c_blocks;
-                    const int r = rs / a.S, s = rs % a.S;
-                    ptx::mbar_arrive_expect_tx(&full[stage], tx_bytes);
-                    ptx::tma_load_im2col_4d(smA + stage * A_BYTES, &tmA, &full[stage], cb * a.bk, wc, hc, nimg,
-                                            (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
-                    ptx::tma_load_3d(smB + stage * b_bytes, &tmB, &full[stage], cb * a.bk, rs, n0);
+                    ptx::mbar_arrive_expect_tx(&full[stage], tx);
+                    uint8_t *dst = dst0 + stage * tx;
+                    if (!isA)
+                        ptx::tma_load_3d(dst, &tmB, &full[stage], cb * a.bk, rs, n0);
+                    else if (a.a_tiled)
+                        ptx::tma_load_2d(dst, &tmA, &full[stage], cb * a.bk, (int)m0);
+                    else
+                        ptx::tma_load_im2col_4d(dst, &tmA, &full[stage], cb * a.bk, wc, hc, nimg,
+                                                (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                    if (++cb == a.c_blocks) {
+                        cb = 0;
+                        ++rs;
+                        if (++s == a.S) { s = 0; ++r; }
+                    }
                     if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -149,107 +303,79 @@ __global__ void __launch_bounds__(192, 1)
         // ===================== MMA issuer (single thread) =====================
         if (lane == 0) {
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+            const uint64_t a_desc0 = ptx::sw128_kmajor_desc(ptx::smem_u32(smA));
+            const uint64_t b_desc0 = ptx::sw128_kmajor_desc(ptx::smem_u32(smB));
+            const uint32_t acc_cols = (uint32_t)(nsub * a.bn);
             for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
                 const WorkPos wp = decode_work(w, a);
                 const int kb0 = wp.split * a.kb_per_split;
                 const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * (uint32_t)a.bn;
+                const uint32_t d_tmem = tmem_base + acc * acc_cols;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
-                    const uint32_t a_addr = ptx::smem_u32(smA + stage * A_BYTES);
-                    const uint32_t b_addr = ptx::smem_u32(smB + stage * b_bytes);
+                    if (dbg && w == blockIdx.x && kb == kb0) dbg[2] = ptx::globaltimer();
+                    const uint64_t ad = a_desc0 + (uint64_t)((stage * a_bytes) >> 4);
+                    const uint64_t bd = b_desc0 + (uint64_t)((stage * b_bytes) >> 4);
+                    for (int h = 0; h < nsub; ++h) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {   // 4 x 32 bytes of K per 128-byte stage
-                        const uint64_t ad = ptx::sw128_kmajor_desc(a_addr + kk * 32);
-                        const uint64_t bd = ptx::sw128_kmajor_desc(b_addr + kk * 32);
-                        ptx::umma<kTF32>(d_tmem, ad, bd, a.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < 4; ++kk)   // 4 x 32 bytes of K per 128-byte stage (+2 desc units)
+                            ptx::umma<kTF32>(d_tmem + h * a.bn, ad + h * (16384 >> 4) + 2 * kk, bd + 2 * kk, a.idesc,
+                                             (kb > kb0 || kk > 0) ? 1u : 0u);
                     }
                     ptx::umma_commit(&empty[stage]);   // frees this smem stage when the MMAs finish
                     if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
                 }
                 ptx::umma_commit(&tfull[acc]);         // accumulator ready for the epilogue
+                if (dbg && w == blockIdx.x) dbg[3] = ptx::globaltimer();
                 if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
             }
         }
-    } else {
-        // ===================== epilogue warps 2..5 =====================
-        const int quarter = warp & 3;   // TMEM lanes [32*quarter, 32*quarter+32) are visible to this warp
-        const int row = quarter * 32 + lane;
+    } else if (warp >= 4) {
+        // ===================== epilogue warps 4..11 =====================
+        const int quarter = warp & 3;          // TMEM lane quarter this warp may access
+        const int grp = (warp - 4) >> 2;       // 0 or 1
         uint32_t acc = 0, acc_phase = 0;
-        const T *bias = static_cast<const T *>(a.bias);
-        T *y = static_cast<T *>(a.y);
+        const bool final_out = (a.splits == 1);
+        EpiCtx<T> E{&a, sBias, sEpi + (size_t)(warp - 4) * 8192, 0u, lane};
+        const uint32_t acc_cols = (uint32_t)(nsub * a.bn);
+        const int cw = a.epi_tma ? (final_out ? (int)(128 / sizeof(T)) : 32) : 16;
+        const int nchunks = (a.bn + cw - 1) / cw;
         for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
             const WorkPos wp = decode_work(w, a);
-            const long long m = (long long)wp.mt * 128 + row;
             const int n0 = wp.nt * a.bn;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
-            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * (uint32_t)a.bn;
-            const bool mval = m < a.M;
-            long long out_base = 0;   // NCHW: n*K*PQ + pq
-            if (a.out_nchw && mval) {
-                const long long nimg = m / a.PQ;
-                out_base = nimg * (long long)a.K * a.PQ + (m - nimg * a.PQ);
-            }
-            for (int c0 = 0; c0 < a.bn; c0 += 16) {
-                const int k0 = n0 + c0;
-                if (k0 >= a.K) break;   // warp-uniform
-                float v[16];
-                ptx::tmem_ld16(taddr + c0, v);
-                if (!mval) continue;
-                const bool full16 = (k0 + 16 <= a.K);
-                if (a.splits > 1) {
-                    float *dst = a.partial + ((long long)wp.split * a.M + m) * a.K + k0;
-                    if (full16 && a.vec_ok) {
-#pragma unroll
-                        for (int j = 0; j < 16; j += 4)
-                            *reinterpret_cast<float4 *>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            // slabs = (h, chunk) pairs; group g takes h == g when nsub == 2, else every other chunk
+            for (int h = 0; h < nsub; ++h) {
+                if (nsub == 2 && h != grp) continue;
+                const int mrow = wp.mt * a.bm + h * 128 + quarter * 32;
+                const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * acc_cols + h * a.bn;
+                for (int ci = (nsub == 2 ? 0 : grp); ci < nchunks; ci += (nsub == 2 ? 1 : 2)) {
+                    const int c0 = ci * cw;
+                    const int k0 = n0 + c0;
+                    if (k0 >= a.K) break;   // warp-uniform
+                    if (a.epi_tma) {
+                        epi_chunk_tma<T>(E, &tmY, tbase + c0, k0, mrow, wp.split, final_out);
                     } else {
-                        for (int j = 0; j < 16 && k0 + j < a.K; ++j) dst[j] = v[j];
-                    }
-                    continue;
-                }
-                if (a.epilogue >= 1) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] += (k0 + j < a.K) ? ld_bias(bias, k0 + j) : 0.f;
-                }
-                if (a.epilogue == 2) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
-                }
-                if (a.out_nchw) {
-                    for (int j = 0; j < 16 && k0 + j < a.K; ++j)
-                        st_out(y + out_base + (long long)(k0 + j) * a.PQ, v[j]);
-                } else {
-                    T *dst = y + m * a.K + k0;
-                    if (full16 && a.vec_ok) {
-                        if constexpr (sizeof(T) == 2) {
-                            uint32_t u[8];
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) u[j] = pack2(v[2 * j], v[2 * j + 1], (T *)nullptr);
-                            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(u[0], u[1], u[2], u[3]);
-                            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(u[4], u[5], u[6], u[7]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 16; j += 4)
-                                *reinterpret_cast<float4 *>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                        }
-                    } else {
-                        for (int j = 0; j < 16 && k0 + j < a.K; ++j) st_out(dst + j, v[j]);
+                        epi_chunk_direct<T>(E, tbase + c0, k0, (long long)mrow + lane, wp.split, final_out);
                     }
                 }
             }
             ptx::tc_fence_before();
             __syncwarp();
+            if (dbg && warp == 4 && lane == 0 && w == blockIdx.x) dbg[4] = ptx::globaltimer();
             if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
             if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
         }
+        if (a.epi_tma && lane == 0) ptx::bulk_wait_all();
+        if (dbg && warp == 4 && lane == 0) dbg[5] = ptx::globaltimer();
     }
 
     __syncthreads();
+    if (dbg && threadIdx.x == 0) dbg[6] = ptx::globaltimer();
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, a.tmem_cols);
@@ -342,9 +468,31 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
         return -1;
     }
     const UmmaGeom &g = L.g;
-    // ---- A: im2col view of x[N][H][W][Cp] -------------------------------------------------------
-    CUtensorMap tmA, tmB;
-    {
+    CUtensorMap tmA, tmB, tmY;
+    UmmaMapCache *mc = L.cache;
+    const bool hit = mc && mc->valid && mc->x == L.x && mc->w == L.w && mc->y == L.y && mc->partial == L.partial &&
+                     mc->cfg == L.cfg;
+    if (hit) {
+        tmA = mc->a;
+        tmB = mc->b;
+        tmY = mc->yy;
+        goto launch;
+    }
+    // ---- A: im2col view of x[N][H][W][Cp] (or a plain [N*H*W][Cp] matrix for 1x1/s1/p0) --------
+    std::memset(&tmY, 0, sizeof tmY);
+    if (g.a_tiled) {
+        cuuint64_t dims[2] = {(cuuint64_t)g.cpad, (cuuint64_t)L.a_rows};
+        cuuint64_t strides[1] = {(cuuint64_t)g.cpad * e};
+        cuuint32_t box[2] = {(cuuint32_t)g.bk, (cuuint32_t)g.bm};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = encode_tiled()(&tmA, tdt, 2, const_cast<void *>(L.x), dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            *err = "cuTensorMapEncodeTiled(A) failed (" + std::to_string((int)r) + ")";
+            return -1;
+        }
+    } else {
         cuuint64_t dims[4] = {(cuuint64_t)g.cpad, (cuuint64_t)L.W, (cuuint64_t)L.H, (cuuint64_t)L.N};
         cuuint64_t strides[3] = {(cuuint64_t)g.cpad * e, (cuuint64_t)g.cpad * e * L.W,
                                  (cuuint64_t)g.cpad * e * L.W * L.H};
@@ -360,10 +508,36 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
             return -1;
         }
     }
+    // ---- Y: TMA-store view of the NHWC output [M][K] (or the fp32 split-K partials [S][M][K]) ---
+    if (g.epi_tma) {
+        const long long M = (long long)L.N * L.P * L.Q;
+        CUresult r;
+        if (g.splits == 1) {
+            cuuint64_t dims[2] = {(cuuint64_t)L.K, (cuuint64_t)M};
+            cuuint64_t strides[1] = {(cuuint64_t)L.K * e};
+            cuuint32_t box[2] = {(cuuint32_t)(128 / e), 32};
+            cuuint32_t estr[2] = {1, 1};
+            r = encode_tiled()(&tmY, tdt, 2, L.y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        } else {
+            cuuint64_t dims[3] = {(cuuint64_t)L.K, (cuuint64_t)M, (cuuint64_t)g.splits};
+            cuuint64_t strides[2] = {(cuuint64_t)L.K * 4, (cuuint64_t)L.K * 4 * M};
+            cuuint32_t box[3] = {32, 32, 1};
+            cuuint32_t estr[3] = {1, 1, 1};
+            r = encode_tiled()(&tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, L.partial, dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        }
+        if (r != CUDA_SUCCESS) {
+            *err = "cuTensorMapEncodeTiled(Y) failed (" + std::to_string((int)r) + ")";
+            return -1;
+        }
+    }
     // ---- B: tiled view of w[K][R*S][Cp] ---------------------------------------------------------
     {
-        cuuint64_t dims[3] = {(cuuint64_t)g.cpad, (cuuint64_t)(L.R * L.S), (cuuint64_t)L.K};
-        cuuint64_t strides[2] = {(cuuint64_t)g.cpad * e, (cuuint64_t)g.cpad * e * L.R * L.S};
+        cuuint64_t dims[3] = {(cuuint64_t)g.cpad, (cuuint64_t)L.b_rs, (cuuint64_t)L.K};
+        cuuint64_t strides[2] = {(cuuint64_t)g.cpad * e, (cuuint64_t)g.cpad * e * L.b_rs};
         cuuint32_t box[3] = {(cuuint32_t)g.bk, 1, (cuuint32_t)g.bn};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = encode_tiled()(&tmB, tdt, 3, const_cast<void *>(L.w), dims, strides, box, estr,
@@ -374,6 +548,11 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
             return -1;
         }
     }
+    if (mc) {
+        mc->x = L.x; mc->w = L.w; mc->y = L.y; mc->partial = L.partial; mc->cfg = L.cfg;
+        mc->a = tmA; mc->b = tmB; mc->yy = tmY; mc->valid = true;
+    }
+launch:
     UmmaArgs a{};
     a.bias = L.b;
     a.y = L.y;
@@ -387,27 +566,43 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
     a.dil_h = L.dil_h; a.dil_w = L.dil_w; a.S = L.S;
     a.c_blocks = g.c_blocks; a.num_kb = g.num_kb; a.kb_per_split = g.kb_per_split; a.splits = g.splits;
     a.m_tiles = g.m_tiles; a.n_tiles = g.n_tiles; a.raster = g.raster; a.work = g.work;
-    a.bn = g.bn; a.bk = g.bk; a.stages = g.stages; a.acc_stages = g.acc_stages;
-    a.idesc = make_idesc(dt, g.bm, g.bn);
+    a.bm = g.bm; a.bn = g.bn; a.bk = g.bk; a.stages = g.stages; a.acc_stages = g.acc_stages;
+    a.idesc = make_idesc(dt, 128, g.bn);   // every MMA is 128 x BN (BLOCK_M 256 = two of them)
     a.tmem_cols = (uint32_t)g.tmem_cols;
     a.epilogue = L.epilogue;
     a.out_nchw = L.out_nchw;
     a.vec_ok = (L.K % 16 == 0) ? 1 : 0;   // 16-element chunks start 32/64-byte aligned
+    a.a_tiled = g.a_tiled;
+    a.epi_tma = g.epi_tma;
+    a.epi_off = (uint32_t)g.epi_off;
+    a.bias_off = (uint32_t)g.bias_off;
+    a.bar_off = (uint32_t)g.bar_off;
+    a.dbg = L.dbg;
     cudaStream_t st = (cudaStream_t)L.stream;
     long long grid = (long long)L.sm_count * g.ctas_per_sm;
     if (grid > g.work) grid = g.work;
     int launches = 0;
-    cudaError_t ce;
+    cudaError_t ce = cudaSuccess;
 #define WPK_LAUNCH_UMMA(DTV)                                                                          \
     do {                                                                                              \
         if (!set_smem_attr<DTV>()) { *err = "cudaFuncSetAttribute failed"; return -1; }               \
-        umma_conv_kernel<DTV><<<(unsigned)grid, 192, g.smem_bytes, st>>>(tmA, tmB, a);                \
+        ce = cudaLaunchKernelEx(&lc, umma_conv_kernel<DTV>, tmA, tmB, tmY, a);                       \
     } while (0)
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)grid);
+    lc.blockDim = dim3(384);
+    lc.dynamicSmemBytes = g.smem_bytes;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
     if (dt == DT_F16) WPK_LAUNCH_UMMA(DT_F16);
     else if (dt == DT_BF16) WPK_LAUNCH_UMMA(DT_BF16);
     else WPK_LAUNCH_UMMA(DT_TF32);
 #undef WPK_LAUNCH_UMMA
-    ce = cudaGetLastError();
+    if (ce == cudaSuccess) ce = cudaGetLastError();
     if (ce != cudaSuccess) {
         *err = std::string("umma_conv_kernel launch: ") + cudaGetErrorString(ce);
         return -1;

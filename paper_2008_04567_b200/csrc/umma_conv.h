@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <string>
 
+#include <cuda.h>
+
 #include "wpk_internal.h"
 
 namespace wpk {
@@ -16,9 +18,22 @@ struct UmmaArgs {
     int stride_h, stride_w, pad_h, pad_w, dil_h, dil_w, S;
     int c_blocks, num_kb, kb_per_split, splits;
     int m_tiles, n_tiles, raster;
-    int bn, bk, stages, acc_stages;
+    int bm, bn, bk, stages, acc_stages;
     uint32_t idesc, tmem_cols;
     int epilogue, out_nchw, vec_ok;
+    int a_tiled, epi_tma;
+    uint32_t epi_off, bias_off, bar_off;
+    unsigned long long *dbg;        // optional per-CTA timeline (globaltimer ns), debug only
+};
+
+// Tensor maps of the last launch, reused while pointers and config are unchanged (host-side
+// encode is a few microseconds per map).
+struct UmmaMapCache {
+    bool valid = false;
+    const void *x = nullptr, *w = nullptr;
+    void *y = nullptr, *partial = nullptr;
+    Config cfg;
+    CUtensorMap a, b, yy;
 };
 
 struct UmmaLaunch {
@@ -31,8 +46,13 @@ struct UmmaLaunch {
     int N, H, W, K, R, S, P, Q;
     int stride_h, stride_w, pad_h, pad_w, dil_h, dil_w;
     int epilogue, out_nchw;
+    long long a_rows;                // rows of the 2-D A view when g.a_tiled (N*H*W, or M for explicit im2col)
+    int b_rs;                        // taps folded in B's middle dim (R*S, or 1 for explicit im2col)
     int sm_count;
     void *stream;
+    unsigned long long *dbg = nullptr;
+    UmmaMapCache *cache = nullptr;
+    Config cfg;
     UmmaGeom g;
 };
 

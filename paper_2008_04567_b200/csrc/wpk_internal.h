@@ -63,7 +63,11 @@ struct UmmaGeom {
     int c_blocks, num_kb, kb_per_split, m_tiles, n_tiles;
     long long work;
     int cpad;           // channel count as stored for the kernel (C rounded up to the alignment)
+    int a_mode;         // 0: TMA im2col (or tiled for 1x1), 1: explicit im2col matrix in the workspace
+    int a_tiled;        // 1: A fetched by a plain 2-D TMA tile load (1x1, stride 1, pad 0), else im2col
+    int epi_tma;        // 1: epilogue stages 32x128-byte tiles in smem and TMA-stores them
     size_t smem_bytes;
+    size_t epi_off, bias_off, bar_off;   // byte offsets of the epilogue staging, bias, barriers
     int tmem_cols;
 };
 bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::string *why);
@@ -95,6 +99,7 @@ struct Plan {
     const void *packed_for = nullptr;
     int packed_cfg_family = -1;
     int last_launches = 0;
+    void *map_cache = nullptr;   // UmmaMapCache (umma_conv.h)
     // tune stats
     double best_us = 0, tune_seconds = 0;
     int measured = 0, rounds = 0;

@@ -21,8 +21,14 @@ def l2_flush_buffer(device) -> torch.Tensor:
     dev = torch.device(device)
     if dev not in _FLUSH:
         l2 = getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 << 20)
-        _FLUSH[dev] = torch.empty(2 * max(l2, 64 << 20), dtype=torch.uint8, device=dev)
+        _FLUSH[dev] = torch.ones(2 * max(l2, 64 << 20), dtype=torch.uint8, device=dev)
     return _FLUSH[dev]
+
+
+def l2_flush(buf: torch.Tensor):
+    """Evict L2 by READING a 2x-L2 buffer (a write-based flush would leave ~L2-size dirty lines whose
+    write-back would then be charged to the timed kernel)."""
+    torch.sum(buf.view(torch.int32), dtype=torch.int64)
 
 
 def time_fn(fn, warmup: int = 3, reps: int = 11, flush: bool = True, stream=None) -> float:
@@ -35,7 +41,7 @@ def time_fn(fn, warmup: int = 3, reps: int = 11, flush: bool = True, stream=None
         ts = []
         for _ in range(reps):
             if buf is not None:
-                buf.zero_()
+                l2_flush(buf)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             fn()

@@ -107,11 +107,11 @@ def test_set_config_validation():
     notin = (ctypes.c_int32 * 7)(7, 8, 4, 1, 1, 1, 1)
     assert lib.wpk_conv2d_set_config(h, 0, notin) == L.ERR_INVALID_CONFIG
     # f32 cannot use the tensor-core family
-    umma = (ctypes.c_int32 * 7)(64, 4, 1, 0, 1, 2, 128)
+    umma = (ctypes.c_int32 * 7)(64, 4, 1, 0, 0, 2, 128)
     assert lib.wpk_conv2d_set_config(h, 1, umma) == L.ERR_INVALID_CONFIG
     lib.wpk_conv2d_destroy(h)
     st, h = _plan(shp, "bf16")
-    too_deep = (ctypes.c_int32 * 7)(256, 8, 1, 0, 1, 2, 128)   # 8 x 48 KB stages > 227 KB
+    too_deep = (ctypes.c_int32 * 7)(256, 8, 1, 0, 0, 2, 128)   # 8 x 48 KB stages > 227 KB
     assert lib.wpk_conv2d_set_config(h, 1, too_deep) == L.ERR_INVALID_CONFIG
     assert lib.wpk_conv2d_set_config(h, 1, umma) == L.OK
     lib.wpk_conv2d_destroy(h)

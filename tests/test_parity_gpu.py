@@ -67,8 +67,9 @@ def test_epilogues(dtype, epilogue):
 def _umma_space():
     bns = [16, 32, 64, 96, 128, 192, 256]
     out = []
-    for bn, st, sp, ra, ctas, acc in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1], [1, 2], [1, 2]):
-        out.append((bn, st, sp, ra, ctas, acc, 128))
+    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1], [0, 1], [1, 2],
+                                                          [128, 256]):
+        out.append((bn, st, sp, ra, amode, acc, bm))
     return out
 
 
@@ -95,6 +96,32 @@ def test_umma_every_config_bit_exact(dtype):
         assert_bit_exact(from_layout(y.cpu(), "nhwc"), ref)
         n += 1
     assert n > 100
+
+
+@pytest.mark.parametrize("env", [{}, {"WPK_EPI_DIRECT": "1"}, {"WPK_A_IM2COL": "1"}])
+@pytest.mark.parametrize("dtype", ["bf16", "f16", "tf32"])
+def test_umma_1x1_and_epilogue_paths(dtype, env, monkeypatch):
+    """1x1 layers (tiled A path), split-K partials through the TMA store, the direct epilogue."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import to_layout, from_layout
+    for L in [ConvLayer("1x1a", 2, 128, 9, 11, 192, 1, 1, 1, 0), ConvLayer("1x1b", 1, 256, 7, 7, 72, 1, 1, 1, 0)]:
+        x, w, b = workloads.generate(L, dtype, "int", seed=21)
+        ref = oracle_full(L, x, w, b)
+        plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype=dtype)
+        xl, wl = to_layout(x, w, "nhwc")
+        xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
+        for genes in [(64, 4, 1, 0, 0, 2, 128), (128, 3, 2, 1, 0, 2, 128), (256, 2, 4, 0, 0, 1, 128),
+                      (32, 4, 1, 0, 0, 2, 128), (96, 5, 2, 0, 0, 2, 128), (192, 3, 1, 1, 0, 2, 128),
+                      (64, 4, 1, 0, 1, 2, 128), (128, 4, 2, 0, 1, 2, 128), (64, 4, 1, 0, 0, 2, 256),
+                      (128, 3, 2, 0, 0, 1, 256), (96, 4, 1, 1, 0, 2, 256), (32, 4, 2, 0, 1, 2, 256)]:
+            if not plan.config_valid(1, list(genes)):
+                continue
+            plan.set_config(1, list(genes))
+            y = plan.run(xl, wl, bc)
+            torch.cuda.synchronize()
+            assert_bit_exact(from_layout(y.cpu(), "nhwc"), ref)
 
 
 def test_simt_every_tile_template():

@@ -1,0 +1,71 @@
+"""Per-CTA timeline of one tcgen05 conv launch (globaltimer ns, relative to the earliest CTA start):
+start, setup done, first full stage, first tile MMAs issued, first tile epilogue done, all epilogues
+done, CTA end.  usage: python tools/timeline.py LAYER [genes]"""
+import ctypes, sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, numpy as np
+import workloads
+from paper_2008_04567_b200 import Conv2dPlan, _lib
+
+name = sys.argv[1]
+L = next(l for l in workloads.resnet50(32) if l.name == name)
+plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype="bf16")
+if len(sys.argv) > 2:
+    plan.set_config(1, [int(v) for v in sys.argv[2:9]])
+x, w, b = workloads.generate(L, "bf16", "uniform", seed=1)
+xd = x.permute(0, 2, 3, 1).contiguous().cuda(); wd = w.permute(0, 2, 3, 1).contiguous().cuda(); bd = b.cuda()
+y = torch.empty(plan.y_shape(), dtype=xd.dtype, device="cuda")
+dbg = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+lib = _lib.load()
+lib.wpk_debug_set_timeline.argtypes = [ctypes.c_void_p]
+for i in range(3):
+    plan.run(xd, wd, bd, y)
+torch.cuda.synchronize()
+lib.wpk_debug_set_timeline(ctypes.c_void_p(dbg.data_ptr()))
+flush = torch.ones(300 << 20, dtype=torch.uint8, device="cuda")
+torch.sum(flush.view(torch.int32), dtype=torch.int64)
+plan.run(xd, wd, bd, y)
+torch.cuda.synchronize()
+lib.wpk_debug_set_timeline(None)
+t = dbg.view(148, 8).cpu().numpy().astype(np.float64)
+t = t[t[:, 0] > 0]
+t0 = t[:, 0].min()
+rel = (t[:, :7] - t0) / 1000.0
+names = ["start", "setup", "1st_full", "1st_mma_done", "1st_epi_done", "epi_all_done", "end"]
+print(name, plan.config, "CTAs", len(t))
+for i, n in enumerate(names):
+    col = rel[:, i]
+    col = col[col > -1e6]
+    print(f"  {n:14s} min {col.min():8.2f}  median {np.median(col):8.2f}  max {col.max():8.2f} us")
+
+# event-timed duration of the same launch vs the in-kernel span, and host cost of one run() call
+import time
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.sum(flush.view(torch.int32), dtype=torch.int64)
+e0.record(); plan.run(xd, wd, bd, y); e1.record(); torch.cuda.synchronize()
+print(f"  event-timed run: {e0.elapsed_time(e1) * 1e3:.2f} us; kernel span {rel.max():.2f} us")
+# back-to-back
+e0.record()
+for i in range(50):
+    plan.run(xd, wd, bd, y)
+e1.record(); torch.cuda.synchronize()
+print(f"  50 back-to-back runs: {e0.elapsed_time(e1) * 1e3 / 50:.2f} us each")
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for i in range(200):
+    plan.run(xd, wd, bd, y)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+print(f"  host time per run() call: {(t1 - t0) / 200 * 1e6:.1f} us")
+g = torch.cuda.CUDAGraph()
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(s):
+    plan.run(xd, wd, bd, y)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(50):
+            plan.run(xd, wd, bd, y, stream=s)
+torch.cuda.synchronize()
+e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+print(f"  graph of 50 runs: {e0.elapsed_time(e1) * 1e3 / 50:.2f} us each")
