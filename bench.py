@@ -163,9 +163,11 @@ def main():
     ap.add_argument("--search", default="ga", choices=["ga", "rl", "random", "none"])
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-points", type=int, default=256)
-    ap.add_argument("--cpu-sample-points", type=int, default=128)
+    ap.add_argument("--ref-points", type=int, default=1024)
+    ap.add_argument("--cpu-sample-points", type=int, default=12288)
     ap.add_argument("--layers-json", default=None, help="also write the per-layer table here")
+    ap.add_argument("--configs-out", default=None, help="write the per-layer chosen configs (JSON)")
+    ap.add_argument("--configs-in", default=None, help="use these per-layer configs instead of tuning")
     ap.add_argument("--layer-events", action="store_true",
                     help="record events between layers inside the timed region (defeats PDL overlap); by "
                          "default per-layer times come from an instrumented pass right after the timed steps")
@@ -200,7 +202,10 @@ def main():
     for i, L in enumerate(layers):
         plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups, layout="nhwc",
                           dtype="bf16", device=local)
-        if args.search != "none" and args.tune_budget > 0:
+        if args.configs_in:
+            fam, genes = json.load(open(args.configs_in))[L.name]
+            plan.set_config(fam, genes)
+        elif args.search != "none" and args.tune_budget > 0:
             ex = wdist.make_exchange(pg) if world > 1 else {}
             res = plan.tune(args.search, args.tune_budget, seed=i, rank=rank, world=world, **ex)
             tune_info.append({"layer": L.name, "best_us": res.best_us, "measured": res.measured,
@@ -215,6 +220,8 @@ def main():
             units.append((i, plan, xd, wd, bd, yd))
     torch.cuda.synchronize()
     tune_seconds = time.perf_counter() - t_tune0
+    if args.configs_out and rank == 0:
+        json.dump({L.name: list(plans[i].config) for i, L in enumerate(layers)}, open(args.configs_out, "w"))
 
     total_flops = sum(layer_flops(L, plans[i].p, plans[i].q) * L.count for i, L in enumerate(layers))
 
