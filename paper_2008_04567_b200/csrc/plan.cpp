@@ -159,15 +159,18 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     const int cw = 128 / out_elem;
     g->epi_tma = (d.layout == WPK_NHWC && g->bn % cw == 0 && ((long long)d.k * out_elem) % 16 == 0 &&
                   !getenv("WPK_EPI_DIRECT")) ? 1 : 0;
+    const size_t smem_cap = 227 * 1024;
+    const size_t fixed = 1024 /*align slack*/ + ((size_t)d.k * 4 + 15) / 16 * 16 /*bias*/ + 256 /*barriers*/;
+    // 8 epilogue warps x {2, else 1} staging buffers x 32 rows x 128 B
+    g->epi_bufs = (g->epi_tma && (size_t)g->stages * stage + 8 * 2 * 4096 + fixed <= smem_cap) ? 2 : 1;
     size_t off = (size_t)g->stages * stage;
     g->epi_off = off;
-    if (g->epi_tma) off += 8 * 2 * 32 * 128;   // 8 epilogue warps x 2 buffers x 32 rows x 128 B
+    if (g->epi_tma) off += (size_t)8 * g->epi_bufs * 4096;
     g->bias_off = off;
     off += ((size_t)d.k * 4 + 15) / 16 * 16;
     g->bar_off = off;
     off += 256;
     g->smem_bytes = 1024 /*align slack*/ + off;
-    size_t smem_cap = (g->ctas_per_sm == 1) ? 227 * 1024 : 113 * 1024;
     if (g->smem_bytes > smem_cap) return no("STAGES x tile exceeds shared memory");
     int cols = g->acc_stages * (g->bm / 128) * g->bn;
     int alloc = 32;
@@ -231,14 +234,15 @@ Config default_config(const ConvDesc &d, int family) {
         std::memcpy(c.genes, g, sizeof g);
         return c;
     }
-    // UMMA: the widest BLOCK_N (<= 256, covering K) that still gives about one wave of tiles; split-K
-    // when even that cannot fill the machine; deepest pipeline that fits; double-buffered TMEM.
-    const long long m_tiles = (d.M() + 127) / 128;
+    // UMMA default: BLOCK_M 128 and the widest BLOCK_N (<= 256) that does not pad K by more than 2x
+    // -- per-SM L2->SMEM feed (~70 B/clk, tools/tma_bench.cu) is what bounds a K step, and the wide
+    // tile has the best FLOP/byte -- then split-K (in-kernel fixup) until ~one wave of work items;
+    // deepest pipeline that fits; double-buffered TMEM when it fits.
     int bn = 16;
     for (int v : {256, 128, 64, 32, 16}) {
-        if (v > 16 && v / 2 >= d.k) continue;              // do not pad K by more than 2x
+        if (v > 16 && v / 2 >= d.k) continue;
         bn = v;
-        if (m_tiles * ((d.k + v - 1) / v) >= 120) break;
+        break;
     }
     c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c < 16) ? 1 : 0;
     c.genes[5] = 2; c.genes[6] = 128;
@@ -248,15 +252,14 @@ Config default_config(const ConvDesc &d, int family) {
     }
     UmmaGeom g;
     if (umma_geometry(d, c, &g, nullptr)) {
-        long long tiles = (long long)g.m_tiles * g.n_tiles;
-        if (tiles < 100) {
-            for (int sp : {2, 4, 8, 16}) {
-                Config t = c;
-                t.genes[2] = sp;
-                if (!config_valid(d, t, nullptr)) break;
-                c = t;
-                if (tiles * sp >= 120) break;
-            }
+        const long long tiles = (long long)g.m_tiles * g.n_tiles;
+        for (int sp : {2, 4, 8, 16}) {
+            if (tiles * (sp / 2) >= 120) break;
+            Config t = c;
+            t.genes[2] = sp;
+            UmmaGeom gt;
+            if (!config_valid(d, t, nullptr) || !umma_geometry(d, t, &gt, nullptr) || gt.kb_per_split < 4) break;
+            c = t;
         }
     }
     if (!config_valid(d, c, nullptr)) {   // shape too odd for the defaults: fall back to SIMT

@@ -223,6 +223,7 @@ struct WsLayout {
     size_t x_off = 0, x_bytes = 0;    // transformed / padded activations
     size_t w_off = 0, w_bytes = 0;    // packed weights
     size_t p_off = 0, p_bytes = 0;    // split-K partials
+    size_t c_off = 0, c_bytes = 0;    // split-K tile counters
     size_t hx_off = 0, hx_bytes = 0;  // run_host staging of x
     size_t hy_off = 0, hy_bytes = 0;  // run_host staging of y
     size_t total = 0;
@@ -246,6 +247,7 @@ static WsLayout ws_layout(const ConvDesc &d, const Config &cfg, bool host_stagin
         }
         if (g.splits > 1) {
             L.p_off = off; L.p_bytes = al256((size_t)g.splits * d.M() * d.k * 4); off += L.p_bytes;
+            L.c_off = off; L.c_bytes = al256((size_t)g.m_tiles * g.n_tiles * 4); off += L.c_bytes;
         }
     } else if (cfg.family == WPK_FAMILY_DW) {
         L.w_off = off; L.w_bytes = al256((size_t)d.c * d.r * d.s * e); off += L.w_bytes;
@@ -373,6 +375,17 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     UmmaLaunch U{};
     U.dtype = d.dtype; U.x = xk; U.w = wk; U.b = b; U.y = y;
     U.partial = (g.splits > 1) ? reinterpret_cast<float *>(ws + L.p_off) : nullptr;
+    if (g.splits > 1) {
+        // counters are self-resetting; zero them once per (workspace, layout) they live at
+        char *cptr = ws + L.c_off;
+        if (p.counters_at != cptr || p.counters_bytes != L.c_bytes) {
+            cudaMemsetAsync(cptr, 0, L.c_bytes, st);
+            ++launches;
+            p.counters_at = cptr;
+            p.counters_bytes = L.c_bytes;
+        }
+        U.counters = reinterpret_cast<int *>(cptr);
+    }
     U.N = d.n; U.H = d.h; U.W = d.w; U.K = d.k; U.R = d.r; U.S = d.s; U.P = d.p; U.Q = d.q;
     U.stride_h = d.sh; U.stride_w = d.sw; U.pad_h = d.ph; U.pad_w = d.pw; U.dil_h = d.dh; U.dil_w = d.dw;
     U.epilogue = d.epilogue; U.out_nchw = d.layout == WPK_NCHW; U.sm_count = sm; U.stream = stream; U.g = g;

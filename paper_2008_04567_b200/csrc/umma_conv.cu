@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -83,6 +84,7 @@ struct EpiCtx {
     uint8_t *sEpi;        // this warp's 2 x 4 KB staging buffers
     uint32_t ebuf;
     int lane;
+    int nbufs;
 };
 
 template <typename T>
@@ -119,7 +121,10 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx<T> &E, const CUtensorMap *t
         }
     }
     // staging buffer reuse: the TMA store issued two chunks ago must have finished reading it
-    if (E.lane == 0) ptx::bulk_wait_read<1>();
+    if (E.lane == 0) {
+        if (E.nbufs == 2) ptx::bulk_wait_read<1>();
+        else ptx::bulk_wait_read<0>();
+    }
     __syncwarp();
     uint8_t *bufp = E.sEpi + E.ebuf * 4096;
     const uint32_t buf = ptx::smem_u32(bufp) + (uint32_t)E.lane * 128;
@@ -133,7 +138,7 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx<T> &E, const CUtensorMap *t
         else ptx::tma_store_3d(tmY, bufp, k0, mrow, split);
         ptx::bulk_commit();
     }
-    E.ebuf ^= 1;
+    if (E.nbufs == 2) E.ebuf ^= 1;
 }
 
 template <typename T>
@@ -191,6 +196,95 @@ __device__ __forceinline__ void epi_chunk_direct(EpiCtx<T> &E, uint32_t taddr, i
     }
 }
 
+// In-kernel split-K fixup ("serial reduction by the last arriving split"): every split publishes its
+// fp32 partial tile, bumps the tile's counter; the CTA that completes the count sums all partials
+// in the fixed split order 0..S-1 (deterministic, independent of arrival order), applies bias+ReLU,
+// rounds once and stores the output, then resets the counter for the next launch.
+template <typename T>
+__device__ __noinline__ void splitk_fixup(const UmmaArgs &a, const float *sBias, volatile int *sFlag, const WorkPos &wp,
+                                          int nsub, int warp, int lane) {
+    if (a.epi_tma && lane == 0) ptx::bulk_wait_all();   // this warp's partial stores are complete
+    __syncwarp();
+    __threadfence();
+    ptx::named_bar_sync(1, 256);                         // all 8 epilogue warps published
+    const int tile = wp.mt * a.n_tiles + wp.nt;
+    if (warp == 4 && lane == 0) {
+        const int old = atomicAdd(a.counters + tile, 1);
+        *sFlag = (old == a.splits - 1) ? 1 : 0;
+    }
+    ptx::named_bar_sync(1, 256);
+    const bool last = (*sFlag != 0);
+    if (!last) return;
+    __threadfence();
+    // Final pass, coalesced: a warp sums 128 consecutive columns (4 per lane) of one output row over
+    // the splits (all splits' loads issued before the in-order sum).
+    T *y = static_cast<T *>(a.y);
+    const int n0 = wp.nt * a.bn;
+    const int ncols = min(a.bn, a.K - n0);
+    const int cblocks = (ncols + 127) / 128;
+    const int items = nsub * 128 * cblocks;
+    const long long MK = a.M * (long long)a.K;
+    const long long m0 = (long long)wp.mt * a.bm;
+    const bool vec = (a.K % 4) == 0;
+    for (int item = warp - 4; item < items; item += 8) {
+        const int r = item / cblocks, cb = item - (item / cblocks) * cblocks;
+        const long long m = m0 + r;
+        const int k = n0 + cb * 128 + lane * 4;
+        const bool ok = m < a.M && k < n0 + ncols;
+        const bool v4 = ok && vec && k + 3 < a.K;
+        float4 q[16];
+        const float *src = a.partial + m * a.K + k;
+#pragma unroll
+        for (int sp = 0; sp < 16; ++sp) {
+            q[sp] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (sp < a.splits && ok) {
+                const float *s = src + sp * MK;
+                if (v4) {
+                    q[sp] = __ldcg(reinterpret_cast<const float4 *>(s));
+                } else {
+                    q[sp].x = __ldcg(s);
+                    if (k + 1 < a.K) q[sp].y = __ldcg(s + 1);
+                    if (k + 2 < a.K) q[sp].z = __ldcg(s + 2);
+                    if (k + 3 < a.K) q[sp].w = __ldcg(s + 3);
+                }
+            }
+        }
+        if (!ok) continue;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int sp = 0; sp < 16; ++sp)
+            if (sp < a.splits) { v[0] += q[sp].x; v[1] += q[sp].y; v[2] += q[sp].z; v[3] += q[sp].w; }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            v[j] += sBias[min(k + j, a.K - 1)];
+            if (a.epilogue == 2) v[j] = fmaxf(v[j], 0.f);
+        }
+        if (a.out_nchw) {
+            const long long nimg = m / a.PQ;
+            const long long ob = nimg * (long long)a.K * a.PQ + (m - nimg * a.PQ);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (k + j < a.K) st_out(y + ob + (long long)(k + j) * a.PQ, v[j]);
+        } else {
+            T *dst = y + m * a.K + k;
+            if (v4) {
+                if constexpr (sizeof(T) == 2) {
+                    const uint32_t lo = pack2(v[0], v[1], (T *)nullptr), hi = pack2(v[2], v[3], (T *)nullptr);
+                    *reinterpret_cast<uint2 *>(dst) = make_uint2(lo, hi);
+                } else {
+                    *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (k + j < a.K) st_out(dst + j, v[j]);
+            }
+        }
+    }
+    ptx::named_bar_sync(1, 256);
+    if (warp == 4 && lane == 0) a.counters[tile] = 0;    // self-resetting for the next launch
+}
+
 // 12 warps: 0 = A producer, 1 = TMEM allocator + MMA issuer, 2 = B producer, 3 = spare,
 // 4..11 = epilogue (two groups of four; warp w reads TMEM lanes [32*(w%4), +32)).
 template <int DT>
@@ -216,6 +310,7 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t *tfull = bars + 16;      // [2]
     uint64_t *tempty = bars + 18;     // [2]
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 20);
+    volatile int *sFlag = reinterpret_cast<volatile int *>(bars + 21);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long *dbg = a.dbg ? a.dbg + blockIdx.x * 8 : nullptr;
@@ -246,7 +341,7 @@ __global__ void __launch_bounds__(384, 1)
     if (warp >= 4) {   // bias -> smem once (fp32); zero when there is no bias or for split-K partials
         const T *bias = static_cast<const T *>(a.bias);
         for (int k = threadIdx.x - 128; k < a.K; k += 256)
-            sBias[k] = (a.epilogue >= 1 && a.splits == 1) ? ld_bias(bias, k) : 0.f;
+            sBias[k] = (a.epilogue >= 1) ? ld_bias(bias, k) : 0.f;
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -339,7 +434,7 @@ __global__ void __launch_bounds__(384, 1)
         const int grp = (warp - 4) >> 2;       // 0 or 1
         uint32_t acc = 0, acc_phase = 0;
         const bool final_out = (a.splits == 1);
-        EpiCtx<T> E{&a, sBias, sEpi + (size_t)(warp - 4) * 8192, 0u, lane};
+        EpiCtx<T> E{&a, sBias, sEpi + (size_t)(warp - 4) * a.epi_bufs * 4096, 0u, lane, a.epi_bufs};
         const uint32_t acc_cols = (uint32_t)(nsub * a.bn);
         const int cw = a.epi_tma ? (final_out ? (int)(128 / sizeof(T)) : 32) : 16;
         const int nchunks = (a.bn + cw - 1) / cw;
@@ -367,8 +462,9 @@ __global__ void __launch_bounds__(384, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (dbg && warp == 4 && lane == 0 && w == blockIdx.x) dbg[4] = ptx::globaltimer();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);   // TMEM free: the MMA may start the next tile
             if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
+            if (!final_out) splitk_fixup<T>(a, sBias, sFlag, wp, nsub, warp, lane);
         }
         if (a.epi_tma && lane == 0) ptx::bulk_wait_all();
         if (dbg && warp == 4 && lane == 0) dbg[5] = ptx::globaltimer();
@@ -379,29 +475,6 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, a.tmem_cols);
-    }
-}
-
-// Deterministic split-K fixup: y = act(b + sum_{split=0..S-1} partial[split]) in fixed split order.
-template <typename T>
-__global__ void splitk_reduce_kernel(const float *__restrict__ partial, int splits, long long M, int K,
-                                     const T *__restrict__ bias, T *__restrict__ y, int epilogue, int out_nchw,
-                                     long long PQ) {
-    const long long total = M * K;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        float s = 0.f;
-        for (int sp = 0; sp < splits; ++sp) s += partial[sp * total + i];
-        const int k = (int)(i % K);
-        const long long m = i / K;
-        if (epilogue >= 1) s += ld_bias(bias, k);
-        if (epilogue == 2) s = fmaxf(s, 0.f);
-        long long o = i;
-        if (out_nchw) {
-            const long long n = m / PQ;
-            o = (n * K + k) * PQ + (m - n * PQ);
-        }
-        st_out(y + o, s);
     }
 }
 
@@ -575,9 +648,11 @@ launch:
     a.a_tiled = g.a_tiled;
     a.epi_tma = g.epi_tma;
     a.epi_off = (uint32_t)g.epi_off;
+    a.epi_bufs = g.epi_bufs;
     a.bias_off = (uint32_t)g.bias_off;
     a.bar_off = (uint32_t)g.bar_off;
     a.dbg = L.dbg;
+    a.counters = L.counters;
     cudaStream_t st = (cudaStream_t)L.stream;
     long long grid = (long long)L.sm_count * g.ctas_per_sm;
     if (grid > g.work) grid = g.work;
@@ -597,7 +672,7 @@ launch:
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = attr;
-    lc.numAttrs = 1;
+    lc.numAttrs = getenv("WPK_NO_PDL") ? 0 : 1;
     if (dt == DT_F16) WPK_LAUNCH_UMMA(DT_F16);
     else if (dt == DT_BF16) WPK_LAUNCH_UMMA(DT_BF16);
     else WPK_LAUNCH_UMMA(DT_TF32);
@@ -608,28 +683,6 @@ launch:
         return -1;
     }
     ++launches;
-    if (g.splits > 1) {
-        long long total = a.M * a.K;
-        int threads = 256;
-        long long blocks = (total + threads - 1) / threads;
-        if (blocks > (long long)L.sm_count * 16) blocks = (long long)L.sm_count * 16;
-        if (dt == DT_F16)
-            splitk_reduce_kernel<__half><<<(unsigned)blocks, threads, 0, st>>>(
-                L.partial, g.splits, a.M, a.K, (const __half *)L.b, (__half *)L.y, L.epilogue, L.out_nchw, a.PQ);
-        else if (dt == DT_BF16)
-            splitk_reduce_kernel<__nv_bfloat16><<<(unsigned)blocks, threads, 0, st>>>(
-                L.partial, g.splits, a.M, a.K, (const __nv_bfloat16 *)L.b, (__nv_bfloat16 *)L.y, L.epilogue,
-                L.out_nchw, a.PQ);
-        else
-            splitk_reduce_kernel<float><<<(unsigned)blocks, threads, 0, st>>>(
-                L.partial, g.splits, a.M, a.K, (const float *)L.b, (float *)L.y, L.epilogue, L.out_nchw, a.PQ);
-        ce = cudaGetLastError();
-        if (ce != cudaSuccess) {
-            *err = std::string("splitk_reduce launch: ") + cudaGetErrorString(ce);
-            return -1;
-        }
-        ++launches;
-    }
     return launches;
 }
 

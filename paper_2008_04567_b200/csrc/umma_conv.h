@@ -21,9 +21,10 @@ struct UmmaArgs {
     int bm, bn, bk, stages, acc_stages;
     uint32_t idesc, tmem_cols;
     int epilogue, out_nchw, vec_ok;
-    int a_tiled, epi_tma;
+    int a_tiled, epi_tma, epi_bufs;
     uint32_t epi_off, bias_off, bar_off;
     unsigned long long *dbg;        // optional per-CTA timeline (globaltimer ns), debug only
+    int *counters;                  // split-K arrival counters, one per output tile (self-resetting)
 };
 
 // Tensor maps of the last launch, reused while pointers and config are unchanged (host-side
@@ -43,6 +44,7 @@ struct UmmaLaunch {
     const void *b;
     void *y;
     float *partial;                  // split-K workspace (splits x M x K fp32) or nullptr
+    int *counters = nullptr;         // split-K tile counters (zeroed once per workspace)
     int N, H, W, K, R, S, P, Q;
     int stride_h, stride_w, pad_h, pad_w, dil_h, dil_w;
     int epilogue, out_nchw;

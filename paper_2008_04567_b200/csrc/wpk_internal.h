@@ -65,6 +65,7 @@ struct UmmaGeom {
     int cpad;           // channel count as stored for the kernel (C rounded up to the alignment)
     int a_mode;         // 0: TMA im2col (or tiled for 1x1), 1: explicit im2col matrix in the workspace
     int a_tiled;        // 1: A fetched by a plain 2-D TMA tile load (1x1, stride 1, pad 0), else im2col
+    int epi_bufs;       // staging buffers per epilogue warp (2 = double-buffered TMA stores)
     int epi_tma;        // 1: epilogue stages 32x128-byte tiles in smem and TMA-stores them
     size_t smem_bytes;
     size_t epi_off, bias_off, bar_off;   // byte offsets of the epilogue staging, bias, barriers
@@ -100,6 +101,8 @@ struct Plan {
     int packed_cfg_family = -1;
     int last_launches = 0;
     void *map_cache = nullptr;   // UmmaMapCache (umma_conv.h)
+    char *counters_at = nullptr; // split-K counters known to be zero at this address
+    size_t counters_bytes = 0;
     // tune stats
     double best_us = 0, tune_seconds = 0;
     int measured = 0, rounds = 0;

@@ -15,7 +15,7 @@ if len(sys.argv) > 2:
 x, w, b = workloads.generate(L, "bf16", "uniform", seed=1)
 xd = x.permute(0, 2, 3, 1).contiguous().cuda(); wd = w.permute(0, 2, 3, 1).contiguous().cuda(); bd = b.cuda()
 y = torch.empty(plan.y_shape(), dtype=xd.dtype, device="cuda")
-dbg = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(148 * 16, dtype=torch.int64, device="cuda")
 lib = _lib.load()
 lib.wpk_debug_set_timeline.argtypes = [ctypes.c_void_p]
 for i in range(3):
@@ -27,7 +27,7 @@ torch.sum(flush.view(torch.int32), dtype=torch.int64)
 plan.run(xd, wd, bd, y)
 torch.cuda.synchronize()
 lib.wpk_debug_set_timeline(None)
-t = dbg.view(148, 8).cpu().numpy().astype(np.float64)
+t = dbg.view(148, 16).cpu().numpy().astype(np.float64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 rel = (t[:, :7] - t0) / 1000.0
@@ -37,6 +37,18 @@ for i, n in enumerate(names):
     col = rel[:, i]
     col = col[col > -1e6]
     print(f"  {n:14s} min {col.min():8.2f}  median {np.median(col):8.2f}  max {col.max():8.2f} us")
+fx = t[:, 8:14]
+if (fx[:, 0] > 0).any():
+    sel = fx[:, 0] > 0
+    r = (fx[sel][:, [0, 1, 2, 3, 5]] - t0) / 1000.0
+    for i, n in enumerate(["fix_enter", "fix_bulkwait", "fix_bar1", "fix_flag", "fix_final_done"]):
+        col = r[:, i]
+        col = col[col > 0]
+        if len(col):
+            print(f"  {n:14s} min {col.min():8.2f}  median {np.median(col):8.2f}  max {col.max():8.2f} us  (n={len(col)})")
+    print("  final passes per CTA:", np.bincount(fx[sel][:, 4].astype(int)))
+    slow = np.argmax(t[:, 5])
+    print("  slowest CTA row (us):", np.round((t[slow, :14] - t0) / 1000.0, 2))
 
 # event-timed duration of the same launch vs the in-kernel span, and host cost of one run() call
 import time
