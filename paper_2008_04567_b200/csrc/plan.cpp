@@ -234,34 +234,25 @@ Config default_config(const ConvDesc &d, int family) {
         std::memcpy(c.genes, g, sizeof g);
         return c;
     }
-    // UMMA default: BLOCK_M 128 and the widest BLOCK_N (<= 256) that does not pad K by more than 2x
-    // -- per-SM L2->SMEM feed (~70 B/clk, tools/tma_bench.cu) is what bounds a K step, and the wide
-    // tile has the best FLOP/byte -- then split-K (in-kernel fixup) until ~one wave of work items;
-    // deepest pipeline that fits; double-buffered TMEM when it fits.
+    // UMMA default: BLOCK_M 128; BLOCK_N 128 when that still leaves < ~1 wave of 256-wide tiles
+    // (more SMs busy), else the widest (<= 256) that does not pad K by more than 2x -- per-SM L2->SMEM
+    // feed (~70 B/clk, tools/tma_bench.cu) bounds a K step and wide tiles have the best FLOP/byte.
     int bn = 16;
     for (int v : {256, 128, 64, 32, 16}) {
         if (v > 16 && v / 2 >= d.k) continue;
         bn = v;
         break;
     }
+    const long long mt = (d.M() + 127) / 128;
+    if (bn == 256 && mt * ((d.k + 255) / 256) < 120) bn = 128;
     c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c < 16) ? 1 : 0;
     c.genes[5] = 2; c.genes[6] = 128;
     for (int st = 8; st >= 2; --st) {
         c.genes[1] = st;
         if (config_valid(d, c, nullptr)) break;
     }
-    UmmaGeom g;
-    if (umma_geometry(d, c, &g, nullptr)) {
-        const long long tiles = (long long)g.m_tiles * g.n_tiles;
-        for (int sp : {2, 4, 8, 16}) {
-            if (tiles * (sp / 2) >= 120) break;
-            Config t = c;
-            t.genes[2] = sp;
-            UmmaGeom gt;
-            if (!config_valid(d, t, nullptr) || !umma_geometry(d, t, &gt, nullptr) || gt.kb_per_split < 4) break;
-            c = t;
-        }
-    }
+    // Split-K is left to the tuner: its fixup re-reads fp32 partials and is only a win for
+    // very deep, very narrow layers.
     if (!config_valid(d, c, nullptr)) {   // shape too odd for the defaults: fall back to SIMT
         return default_config(d, WPK_FAMILY_SIMT);
     }

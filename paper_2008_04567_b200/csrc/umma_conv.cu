@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(384, 1)
     volatile int *sFlag = reinterpret_cast<volatile int *>(bars + 21);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned long long *dbg = a.dbg ? a.dbg + blockIdx.x * 8 : nullptr;
+    unsigned long long *dbg = a.dbg ? a.dbg + blockIdx.x * 16 : nullptr;
     if (dbg && threadIdx.x == 0) dbg[0] = ptx::globaltimer();
 
     if (warp == 0 && lane == 0) {
