@@ -72,7 +72,8 @@ typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 
  *                     (T_x, T_y, T_z, Tile_x, Tile_y, Tile_z, Tile_rz), T_x*T_y*T_z<=1024
  *   WPK_FAMILY_UMMA : tcgen05 implicit GEMM, genes = (BLOCK_N, STAGES, SPLIT_K, RASTER,
  *                     A_MODE, ACC_STAGES, BLOCK_M); A_MODE 0 = TMA im2col producer (plain TMA
- *                     tiles for 1x1/s1/p0), 1 = explicit im2col matrix (small-C layers)
+ *                     tiles for 1x1/s1/p0), 1 = explicit im2col matrix in the workspace,
+ *                     2 = fused gather producer (im2col built in shared memory; small-C layers)
  *   WPK_FAMILY_DW   : depthwise (groups == C == K), genes = (VEC_C, PIX_PER_THREAD, THREADS,
  *                     -, -, -, -)                                                      */
 typedef enum { WPK_FAMILY_SIMT = 0, WPK_FAMILY_UMMA = 1, WPK_FAMILY_DW = 2, WPK_FAMILY_AUTO = -1 } wpk_family;

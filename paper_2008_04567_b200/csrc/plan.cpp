@@ -71,7 +71,7 @@ static Space make_space(int family) {
         sp.names = {"T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"};
     } else if (family == WPK_FAMILY_UMMA) {
         sp.dom = {{16, 32, 64, 96, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8}, {1, 2, 4, 8, 16},
-                  {0, 1}, {0, 1}, {1, 2}, {128, 256}};
+                  {0, 1}, {0, 1, 2}, {1, 2}, {128, 256}};
         sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "RASTER", "A_MODE", "ACC_STAGES", "BLOCK_M"};
     } else {
         sp.dom = {{1, 2, 4, 8}, {1, 2, 4}, {64, 128, 256, 512}, {1}, {0}, {0}, {0}};
@@ -131,12 +131,16 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->ctas_per_sm = 1;
     g->a_mode = cfg.genes[4];
     g->acc_stages = cfg.genes[5];
-    if (g->a_mode == 1) {
-        // explicit im2col: A = [M][R*S*C] materialised in the workspace, then a plain GEMM
+    if ((g->a_mode == 1 || g->a_mode == 2) && d.c >= 64)
+        return no("A_MODE 1/2 (explicit im2col / gather) is reserved for layers with C < 64");
+    if (g->a_mode == 1 || g->a_mode == 2) {
+        // explicit im2col (1: A = [M][R*S*C] materialised in the workspace, then a plain GEMM) or the
+        // fused gather producer (2: the same K order built directly in shared memory)
         g->cpad = round_up(d.r * d.s * d.c, 8);   // 8-element vectors in the im2col kernel
         g->c_blocks = (g->cpad + g->bk - 1) / g->bk;
         g->num_kb = g->c_blocks;
-        if ((double)d.M() * g->cpad * e > 4.0e9) return no("explicit im2col matrix larger than 4 GB");
+        if (g->a_mode == 1 && (double)d.M() * g->cpad * e > 4.0e9) return no("explicit im2col matrix larger than 4 GB");
+        if (g->a_mode == 2 && (double)d.n * d.c * d.h * d.w >= 2147483647.0) return no("gather producer needs < 2^31 input elements");
     } else {
         g->cpad = round_up(d.c, 16 / e);    // TMA global strides must be multiples of 16 B
         g->c_blocks = (g->cpad + g->bk - 1) / g->bk;
@@ -245,7 +249,7 @@ Config default_config(const ConvDesc &d, int family) {
     }
     const long long mt = (d.M() + 127) / 128;
     if (bn == 256 && mt * ((d.k + 255) / 256) < 120) bn = 128;
-    c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c < 16) ? 1 : 0;
+    c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c < 16) ? 2 : 0;
     c.genes[5] = 2; c.genes[6] = 128;
     for (int st = 8; st >= 2; --st) {
         c.genes[1] = st;

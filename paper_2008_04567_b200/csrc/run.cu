@@ -241,6 +241,8 @@ static WsLayout ws_layout(const ConvDesc &d, const Config &cfg, bool host_stagin
         if (g.a_mode == 1) {
             L.x_off = off; L.x_bytes = al256((size_t)d.M() * g.cpad * e); off += L.x_bytes;
             L.w_off = off; L.w_bytes = al256((size_t)d.k * g.cpad * e); off += L.w_bytes;
+        } else if (g.a_mode == 2) {
+            L.w_off = off; L.w_bytes = al256((size_t)d.k * g.cpad * e); off += L.w_bytes;
         } else if (d.layout == WPK_NCHW || g.cpad != d.c) {
             L.x_off = off; L.x_bytes = al256((size_t)d.n * d.h * d.w * g.cpad * e); off += L.x_bytes;
             L.w_off = off; L.w_bytes = al256((size_t)d.k * d.r * d.s * g.cpad * e); off += L.w_bytes;
@@ -339,10 +341,12 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     if (!umma_geometry(d, cfg, &g, &why)) { set_error("invalid UMMA config: " + why); return -1; }
     const void *xk = x, *wk = w;
     const int pack_kind = WPK_FAMILY_UMMA * 10 + g.a_mode;
-    if (g.a_mode == 1) {
-        launch_aux(4, x, ws + L.x_off, d, g.cpad, sm, st);
-        ++launches;
-        xk = ws + L.x_off;
+    if (g.a_mode == 1 || g.a_mode == 2) {
+        if (g.a_mode == 1) {
+            launch_aux(4, x, ws + L.x_off, d, g.cpad, sm, st);
+            ++launches;
+            xk = ws + L.x_off;
+        }
         if (p.packed_for != w || p.packed_cfg_family != pack_kind) {
             launch_aux(5, w, ws + L.w_off, d, g.cpad, sm, st);
             ++launches;
@@ -390,7 +394,9 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     U.stride_h = d.sh; U.stride_w = d.sw; U.pad_h = d.ph; U.pad_w = d.pw; U.dil_h = d.dh; U.dil_w = d.dw;
     U.epilogue = d.epilogue; U.out_nchw = d.layout == WPK_NCHW; U.sm_count = sm; U.stream = stream; U.g = g;
     U.a_rows = (g.a_mode == 1) ? d.M() : (long long)d.n * d.h * d.w;
-    U.b_rs = (g.a_mode == 1) ? 1 : d.r * d.s;
+    U.b_rs = (g.a_mode >= 1) ? 1 : d.r * d.s;
+    U.C = d.c;
+    U.x_nchw = (d.layout == WPK_NCHW);
     U.dbg = g_debug_timeline;
     if (!p.map_cache) p.map_cache = new UmmaMapCache();
     U.cache = static_cast<UmmaMapCache *>(p.map_cache);

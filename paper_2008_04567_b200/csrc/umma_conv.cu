@@ -226,58 +226,86 @@ __device__ __noinline__ void splitk_fixup(const UmmaArgs &a, const float *sBias,
     const long long MK = a.M * (long long)a.K;
     const long long m0 = (long long)wp.mt * a.bm;
     const bool vec = (a.K % 4) == 0;
-    for (int item = warp - 4; item < items; item += 8) {
-        const int r = item / cblocks, cb = item - (item / cblocks) * cblocks;
-        const long long m = m0 + r;
-        const int k = n0 + cb * 128 + lane * 4;
-        const bool ok = m < a.M && k < n0 + ncols;
-        const bool v4 = ok && vec && k + 3 < a.K;
-        float4 q[16];
-        const float *src = a.partial + m * a.K + k;
+    // 4 items x 4 splits of 16-byte loads in flight per lane (the fixup is L2-latency bound)
+    constexpr int U = 4;
+    for (int base = warp - 4; base < items; base += 8 * U) {
+        long long mm[U];
+        int kk[U];
+        bool ok[U];
+        float4 acc[U];
 #pragma unroll
-        for (int sp = 0; sp < 16; ++sp) {
-            q[sp] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (sp < a.splits && ok) {
-                const float *s = src + sp * MK;
-                if (v4) {
-                    q[sp] = __ldcg(reinterpret_cast<const float4 *>(s));
-                } else {
-                    q[sp].x = __ldcg(s);
-                    if (k + 1 < a.K) q[sp].y = __ldcg(s + 1);
-                    if (k + 2 < a.K) q[sp].z = __ldcg(s + 2);
-                    if (k + 3 < a.K) q[sp].w = __ldcg(s + 3);
+        for (int u = 0; u < U; ++u) {
+            const int item = base + u * 8;
+            const int r = item / cblocks, cb = item - (item / cblocks) * cblocks;
+            mm[u] = m0 + r;
+            kk[u] = n0 + cb * 128 + lane * 4;
+            ok[u] = item < items && mm[u] < a.M && kk[u] < n0 + ncols;
+            acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        bool all_v4 = vec;
+#pragma unroll
+        for (int u = 0; u < U; ++u) all_v4 = all_v4 && (!ok[u] || kk[u] + 3 < a.K);
+        if (all_v4) {
+            for (int sp0 = 0; sp0 < a.splits; sp0 += 4) {
+                float4 q[4][U];
+#pragma unroll
+                for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        q[s4][u] = (ok[u] && sp0 + s4 < a.splits)
+                            ? __ldcg(reinterpret_cast<const float4 *>(a.partial + (sp0 + s4) * MK + mm[u] * a.K + kk[u]))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        acc[u].x += q[s4][u].x; acc[u].y += q[s4][u].y; acc[u].z += q[s4][u].z; acc[u].w += q[s4][u].w;
+                    }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!ok[u]) continue;
+                for (int sp = 0; sp < a.splits; ++sp) {
+                    const float *s = a.partial + sp * MK + mm[u] * a.K + kk[u];
+                    acc[u].x += __ldcg(s);
+                    if (kk[u] + 1 < a.K) acc[u].y += __ldcg(s + 1);
+                    if (kk[u] + 2 < a.K) acc[u].z += __ldcg(s + 2);
+                    if (kk[u] + 3 < a.K) acc[u].w += __ldcg(s + 3);
                 }
             }
         }
-        if (!ok) continue;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int sp = 0; sp < 16; ++sp)
-            if (sp < a.splits) { v[0] += q[sp].x; v[1] += q[sp].y; v[2] += q[sp].z; v[3] += q[sp].w; }
+        for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+            const long long m = mm[u];
+            const int k = kk[u];
+            float v[4] = {acc[u].x, acc[u].y, acc[u].z, acc[u].w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            v[j] += sBias[min(k + j, a.K - 1)];
-            if (a.epilogue == 2) v[j] = fmaxf(v[j], 0.f);
-        }
-        if (a.out_nchw) {
-            const long long nimg = m / a.PQ;
-            const long long ob = nimg * (long long)a.K * a.PQ + (m - nimg * a.PQ);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (k + j < a.K) st_out(y + ob + (long long)(k + j) * a.PQ, v[j]);
-        } else {
-            T *dst = y + m * a.K + k;
-            if (v4) {
-                if constexpr (sizeof(T) == 2) {
-                    const uint32_t lo = pack2(v[0], v[1], (T *)nullptr), hi = pack2(v[2], v[3], (T *)nullptr);
-                    *reinterpret_cast<uint2 *>(dst) = make_uint2(lo, hi);
-                } else {
-                    *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
-                }
-            } else {
+            for (int j = 0; j < 4; ++j) {
+                v[j] += sBias[min(k + j, a.K - 1)];
+                if (a.epilogue == 2) v[j] = fmaxf(v[j], 0.f);
+            }
+            if (a.out_nchw) {
+                const long long nimg = m / a.PQ;
+                const long long ob = nimg * (long long)a.K * a.PQ + (m - nimg * a.PQ);
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    if (k + j < a.K) st_out(dst + j, v[j]);
+                    if (k + j < a.K) st_out(y + ob + (long long)(k + j) * a.PQ, v[j]);
+            } else {
+                T *dst = y + m * a.K + k;
+                if (vec && k + 3 < a.K) {
+                    if constexpr (sizeof(T) == 2) {
+                        const uint32_t lo = pack2(v[0], v[1], (T *)nullptr), hi = pack2(v[2], v[3], (T *)nullptr);
+                        *reinterpret_cast<uint2 *>(dst) = make_uint2(lo, hi);
+                    } else {
+                        *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (k + j < a.K) st_out(dst + j, v[j]);
+                }
             }
         }
     }
@@ -287,8 +315,8 @@ __device__ __noinline__ void splitk_fixup(const UmmaArgs &a, const float *sBias,
 
 // 12 warps: 0 = A producer, 1 = TMEM allocator + MMA issuer, 2 = B producer, 3 = spare,
 // 4..11 = epilogue (two groups of four; warp w reads TMEM lanes [32*(w%4), +32)).
-template <int DT>
-__global__ void __launch_bounds__(384, 1)
+template <int DT, bool kGather>
+__global__ void __launch_bounds__(kGather ? 512 : 384, 1)
     umma_conv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmY, const __grid_constant__ UmmaArgs a) {
     using T = typename OutT<DT>::T;
@@ -317,11 +345,11 @@ __global__ void __launch_bounds__(384, 1)
     if (dbg && threadIdx.x == 0) dbg[0] = ptx::globaltimer();
 
     if (warp == 0 && lane == 0) {
-        ptx::prefetch_tmap(&tmA);
+        if (!kGather) ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
         if (a.epi_tma) ptx::prefetch_tmap(&tmY);
         for (int s = 0; s < a.stages; ++s) {
-            ptx::mbar_init(&full[s], 2);       // A producer + B producer
+            ptx::mbar_init(&full[s], kGather ? 5 : 2);   // A (TMA, or 4 gather warps) + B producer
             ptx::mbar_init(&empty[s], 1);      // MMA commit
         }
         for (int s = 0; s < 2; ++s) {
@@ -351,7 +379,7 @@ __global__ void __launch_bounds__(384, 1)
 
     if (warp == 0 || warp == 2) {
         // ===================== TMA producers: warp 0 -> A (activations), warp 2 -> B (weights) ====
-        if (lane == 0) {
+        if (lane == 0 && !(kGather && warp == 0)) {
             const bool isA = (warp == 0);
             uint32_t stage = 0, phase = 0;
             const uint32_t tx = isA ? a_bytes : b_bytes;
@@ -394,6 +422,76 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
         }
+    } else if (kGather && warp >= 12) {
+        // ===================== gather producers (A_MODE 2): implicit im2col straight into the
+        // 128-byte-swizzled K-major A stage, for layers whose channel count is too small for TMA
+        // im2col boxes. kg = (r*S + s)*C + c; one thread owns BM/128 rows of every stage.
+        const int t = threadIdx.x - 384;                       // 0..127
+        const int RSC = a.R * a.S * a.C;
+        uint32_t stage = 0, phase = 0;
+        for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
+            const WorkPos wp = decode_work(w, a);
+            const int kb0 = wp.split * a.kb_per_split;
+            const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+            int rh0[2], rw0[2], rn[2];
+            bool rv[2];
+            for (int hh = 0; hh < nsub; ++hh) {
+                const long long m = (long long)wp.mt * a.bm + hh * 128 + t;
+                rv[hh] = m < a.M;
+                const long long mm = rv[hh] ? m : 0;
+                const int n = (int)(mm / a.PQ);
+                const int rem = (int)(mm - (long long)n * a.PQ);
+                const int p = rem / a.Q, q = rem - (rem / a.Q) * a.Q;
+                rn[hh] = n;
+                rh0[hh] = p * a.stride_h - a.pad_h;
+                rw0[hh] = q * a.stride_w - a.pad_w;
+            }
+            for (int kb = kb0; kb < kb1; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                for (int hh = 0; hh < nsub; ++hh) {
+                    const int row = hh * 128 + t;
+                    const uint32_t rbase = ptx::smem_u32(smA + stage * a_bytes) + (uint32_t)(row >> 3) * 1024u +
+                                           (uint32_t)(row & 7) * 128u;
+                    constexpr int PC = kTF32 ? 4 : 8;          // elements per 16-byte chunk
+                    int kg = kb * PC * 8;                      // first element of this 128-byte K block
+                    int c = kg % a.C, rs_ = kg / a.C;
+                    int s = rs_ % a.S, r = rs_ / a.S;
+                    // two chunks (16 independent loads) in flight at a time; 32-bit offsets
+#pragma unroll 1
+                    for (int j = 0; j < 8; j += 2) {
+                        int off[2 * PC];
+                        bool okv[2 * PC];
+#pragma unroll
+                        for (int e = 0; e < 2 * PC; ++e, ++kg) {
+                            const int hi = rh0[hh] + r * a.dil_h, wi = rw0[hh] + s * a.dil_w;
+                            okv[e] = rv[hh] && kg < RSC && hi >= 0 && hi < a.H && wi >= 0 && wi < a.W;
+                            off[e] = a.x_nchw ? ((rn[hh] * a.C + c) * a.H + hi) * a.W + wi
+                                              : ((rn[hh] * a.H + hi) * a.W + wi) * a.C + c;
+                            if (++c == a.C) { c = 0; if (++s == a.S) { s = 0; ++r; } }
+                        }
+                        uint32_t bits[2 * PC];
+#pragma unroll
+                        for (int e = 0; e < 2 * PC; ++e)
+                            bits[e] = !okv[e] ? 0u
+                                      : kTF32 ? __ldg(reinterpret_cast<const unsigned *>(a.x) + off[e])
+                                              : (uint32_t)__ldg(reinterpret_cast<const unsigned short *>(a.x) + off[e]);
+#pragma unroll
+                        for (int jj = 0; jj < 2; ++jj) {
+                            uint32_t wv[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                wv[q] = kTF32 ? bits[jj * 4 + q]
+                                              : (bits[jj * 8 + 2 * q] | (bits[jj * 8 + 2 * q + 1] << 16));
+                            ptx::st_shared_v4(rbase + ((uint32_t)((j + jj) ^ (row & 7)) << 4), wv[0], wv[1], wv[2], wv[3]);
+                        }
+                    }
+                }
+                ptx::fence_proxy_async_smem();                 // generic-proxy writes -> async-proxy (MMA) reads
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&full[stage]);
+                if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
+            }
+        }
     } else if (warp == 1) {
         // ===================== MMA issuer (single thread) =====================
         if (lane == 0) {
@@ -428,7 +526,7 @@ __global__ void __launch_bounds__(384, 1)
                 if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp >= 4 && warp < 12) {
         // ===================== epilogue warps 4..11 =====================
         const int quarter = warp & 3;          // TMEM lane quarter this warp may access
         const int grp = (warp - 4) >> 2;       // 0 or 1
@@ -462,6 +560,10 @@ __global__ void __launch_bounds__(384, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (dbg && warp == 4 && lane == 0 && w == blockIdx.x) dbg[4] = ptx::globaltimer();
+            if (dbg && warp == 4 && lane == 0) {   // per-tile epilogue completion times (first 8 tiles)
+                const long long it = (w - blockIdx.x) / gridDim.x;
+                if (it < 8) dbg[8 + it] = ptx::globaltimer();
+            }
             if (lane == 0) ptx::mbar_arrive(&tempty[acc]);   // TMEM free: the MMA may start the next tile
             if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
             if (!final_out) splitk_fixup<T>(a, sBias, sFlag, wp, nsub, warp, lane);
@@ -518,11 +620,11 @@ static uint32_t make_idesc(int dt, int bm, int bn) {
     return d;
 }
 
-template <int DT>
+template <int DT, bool G>
 static bool set_smem_attr() {
     static bool done = false;
     if (!done) {
-        if (cudaFuncSetAttribute(umma_conv_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+        if (cudaFuncSetAttribute(umma_conv_kernel<DT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
             cudaSuccess)
             return false;
         done = true;
@@ -553,7 +655,10 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
     }
     // ---- A: im2col view of x[N][H][W][Cp] (or a plain [N*H*W][Cp] matrix for 1x1/s1/p0) --------
     std::memset(&tmY, 0, sizeof tmY);
-    if (g.a_tiled) {
+    std::memset(&tmA, 0, sizeof tmA);
+    if (g.a_mode == 2) {
+        // gather producer: no A tensor map
+    } else if (g.a_tiled) {
         cuuint64_t dims[2] = {(cuuint64_t)g.cpad, (cuuint64_t)L.a_rows};
         cuuint64_t strides[1] = {(cuuint64_t)g.cpad * e};
         cuuint32_t box[2] = {(cuuint32_t)g.bk, (cuuint32_t)g.bm};
@@ -653,6 +758,9 @@ launch:
     a.bar_off = (uint32_t)g.bar_off;
     a.dbg = L.dbg;
     a.counters = L.counters;
+    a.x = L.x;
+    a.x_nchw = L.x_nchw;
+    a.C = L.C; a.H = L.H; a.W = L.W; a.R = L.R;
     cudaStream_t st = (cudaStream_t)L.stream;
     long long grid = (long long)L.sm_count * g.ctas_per_sm;
     if (grid > g.work) grid = g.work;
@@ -660,12 +768,17 @@ launch:
     cudaError_t ce = cudaSuccess;
 #define WPK_LAUNCH_UMMA(DTV)                                                                          \
     do {                                                                                              \
-        if (!set_smem_attr<DTV>()) { *err = "cudaFuncSetAttribute failed"; return -1; }               \
-        ce = cudaLaunchKernelEx(&lc, umma_conv_kernel<DTV>, tmA, tmB, tmY, a);                       \
+        if (g.a_mode == 2) {                                                                          \
+            if (!set_smem_attr<DTV, true>()) { *err = "cudaFuncSetAttribute failed"; return -1; }     \
+            ce = cudaLaunchKernelEx(&lc, umma_conv_kernel<DTV, true>, tmA, tmB, tmY, a);             \
+        } else {                                                                                      \
+            if (!set_smem_attr<DTV, false>()) { *err = "cudaFuncSetAttribute failed"; return -1; }    \
+            ce = cudaLaunchKernelEx(&lc, umma_conv_kernel<DTV, false>, tmA, tmB, tmY, a);            \
+        }                                                                                             \
     } while (0)
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3((unsigned)grid);
-    lc.blockDim = dim3(384);
+    lc.blockDim = dim3(g.a_mode == 2 ? 512 : 384);
     lc.dynamicSmemBytes = g.smem_bytes;
     lc.stream = st;
     cudaLaunchAttribute attr[1];

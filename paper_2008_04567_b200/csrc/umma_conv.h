@@ -25,6 +25,8 @@ struct UmmaArgs {
     uint32_t epi_off, bias_off, bar_off;
     unsigned long long *dbg;        // optional per-CTA timeline (globaltimer ns), debug only
     int *counters;                  // split-K arrival counters, one per output tile (self-resetting)
+    const void *x;                  // A_MODE 2 gather source (the caller's activations)
+    int x_nchw, C, H, W, R;
 };
 
 // Tensor maps of the last launch, reused while pointers and config are unchanged (host-side
@@ -53,6 +55,7 @@ struct UmmaLaunch {
     int sm_count;
     void *stream;
     unsigned long long *dbg = nullptr;
+    int C = 0, x_nchw = 0;
     UmmaMapCache *cache = nullptr;
     Config cfg;
     UmmaGeom g;

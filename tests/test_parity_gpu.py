@@ -67,7 +67,7 @@ def test_epilogues(dtype, epilogue):
 def _umma_space():
     bns = [16, 32, 64, 96, 128, 192, 256]
     out = []
-    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1], [0, 1], [1, 2],
+    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1], [0, 1, 2], [1, 2],
                                                           [128, 256]):
         out.append((bn, st, sp, ra, amode, acc, bm))
     return out
@@ -115,7 +115,8 @@ def test_umma_1x1_and_epilogue_paths(dtype, env, monkeypatch):
         for genes in [(64, 4, 1, 0, 0, 2, 128), (128, 3, 2, 1, 0, 2, 128), (256, 2, 4, 0, 0, 1, 128),
                       (32, 4, 1, 0, 0, 2, 128), (96, 5, 2, 0, 0, 2, 128), (192, 3, 1, 1, 0, 2, 128),
                       (64, 4, 1, 0, 1, 2, 128), (128, 4, 2, 0, 1, 2, 128), (64, 4, 1, 0, 0, 2, 256),
-                      (128, 3, 2, 0, 0, 1, 256), (96, 4, 1, 1, 0, 2, 256), (32, 4, 2, 0, 1, 2, 256)]:
+                      (128, 3, 2, 0, 0, 1, 256), (96, 4, 1, 1, 0, 2, 256), (32, 4, 2, 0, 1, 2, 256),
+                      (64, 4, 1, 0, 2, 2, 128), (128, 3, 2, 0, 2, 2, 256), (256, 2, 1, 0, 2, 1, 128)]:
             if not plan.config_valid(1, list(genes)):
                 continue
             plan.set_config(1, list(genes))
@@ -171,6 +172,28 @@ def test_run_host_matches_device():
     yd = plan.run(xl.cuda(), wl.cuda(), b.cuda())
     torch.cuda.synchronize()
     assert torch.equal(yh, yd.cpu())
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_gather_producer_small_c(dtype, layout):
+    """A_MODE 2 (fused im2col gather into swizzled smem) on small-C shapes incl. conv1-like 7x7/s2."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import to_layout, from_layout
+    for L in [ConvLayer("c3", 2, 3, 30, 30, 64, 7, 7, 2, 3), ConvLayer("c5", 1, 5, 17, 13, 40, 3, 3, 1, 1, 2),
+              ConvLayer("c24", 3, 24, 15, 15, 144, 1, 1, 2, 0)]:
+        x, w, b = workloads.generate(L, dtype, "int", seed=23)
+        ref = oracle_full(L, x, w, b)
+        plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, layout=layout, dtype=dtype)
+        xl, wl = to_layout(x, w, layout)
+        xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
+        for genes in [(64, 4, 1, 0, 2, 2, 128), (128, 3, 2, 1, 2, 2, 256), (32, 6, 1, 0, 2, 1, 128)]:
+            if not plan.config_valid(1, list(genes)):
+                continue
+            plan.set_config(1, list(genes))
+            y = plan.run(xl, wl, bc)
+            torch.cuda.synchronize()
+            assert_bit_exact(from_layout(y.cpu(), layout), ref)
 
 
 @pytest.mark.parametrize("layer", workloads.resnet50(32), ids=lambda l: l.name)

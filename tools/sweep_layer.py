@@ -9,14 +9,17 @@ from paper_2008_04567_b200 import Conv2dPlan
 from paper_2008_04567_b200.selector import time_fn
 
 name = sys.argv[1]
-L = next(l for l in workloads.resnet50(int(os.environ.get("BATCH", "32"))) if l.name == name)
-plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype="bf16")
-x, w, b = workloads.generate(L, "bf16", "uniform", seed=1)
+net = os.environ.get("NET", "resnet50")
+dt = os.environ.get("DT", "bf16")
+batch = int(os.environ.get("BATCH", {"resnet50": "32", "vgg16": "64", "mobilenet_v2": "1"}[net]))
+L = next(l for l in getattr(workloads, net)(batch) if l.name == name)
+plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups, layout="nhwc", dtype=dt)
+x, w, b = workloads.generate(L, dt, "uniform", seed=1)
 xd = x.permute(0, 2, 3, 1).contiguous().cuda(); wd = w.permute(0, 2, 3, 1).contiguous().cuda(); bd = b.cuda()
 y = torch.empty(plan.y_shape(), dtype=xd.dtype, device="cuda")
-fl = 2 * L.n * L.k * plan.p * plan.q * L.c * L.r * L.s
+fl = 2 * L.n * L.k * plan.p * plan.q * (L.c // L.groups) * L.r * L.s
 if len(sys.argv) > 2 and sys.argv[2] == "grid":
-    cfgs = [list(c) for c in itertools.product([64, 128, 256], [3, 4, 6], [1, 2, 4], [0], [0], [1, 2], [128, 256])]
+    cfgs = [list(c) for c in itertools.product([64, 128, 256], [3, 4, 6], [1], [0, 1], [0], [1, 2], [128, 256])]
 elif len(sys.argv) > 2:
     vals = [int(v) for v in sys.argv[2:]]
     cfgs = [vals[i:i + 7] for i in range(0, len(vals), 7)]
@@ -24,9 +27,9 @@ else:
     cfgs = [plan.config[1]]
 print(name, "default", plan.config)
 for g in cfgs:
-    if not plan.config_valid(1, g):
+    if not plan.config_valid(plan.config[0], g):
         continue
-    plan.set_config(1, g)
+    plan.set_config(plan.config[0], g)
     try:
         t = time_fn(lambda: plan.run(xd, wd, bd, y), warmup=3, reps=15)
         torch.cuda.synchronize()
