@@ -116,6 +116,8 @@ typedef struct {
     double rl_gamma, rl_mu, rl_clip, rl_c1, rl_c2, rl_lr, rl_keep_prob;
     int32_t rl_hidden[4];     /* 512, 1024, 1024, 512                                          */
     int32_t rl_alpha_mode;    /* 0 = the paper's alpha_t = (0.8 alpha + beta)/t, 1 = EMA        */
+    int32_t rl_adv_norm;      /* 1 = normalise advantages per update batch (default 1)          */
+    int32_t rl_restart_every; /* >0: envs restart from the best-ever config every N updates (1)  */
     int32_t max_seconds;      /* wall-clock cap for one tune (0 = none)                         */
 } wpk_tune_options;
 

@@ -63,6 +63,8 @@ class TuneOptions(ctypes.Structure):
         ("rl_keep_prob", ctypes.c_double),
         ("rl_hidden", ctypes.c_int32 * 4),
         ("rl_alpha_mode", ctypes.c_int32),
+        ("rl_adv_norm", ctypes.c_int32),
+        ("rl_restart_every", ctypes.c_int32),
         ("max_seconds", ctypes.c_int32),
     ]
 

@@ -288,6 +288,8 @@ void wpk_tune_options_init(wpk_tune_options *o) {
     o->rl_lr = 1e-4; o->rl_keep_prob = 0.85;
     o->rl_hidden[0] = 512; o->rl_hidden[1] = 1024; o->rl_hidden[2] = 1024; o->rl_hidden[3] = 512;
     o->rl_alpha_mode = 0;
+    o->rl_adv_norm = 1;
+    o->rl_restart_every = 1;
 }
 
 wpk_status wpk_conv2d_output_dims(const wpk_conv2d_shape *shape, int32_t *p, int32_t *q) {

@@ -332,6 +332,20 @@ wpk_status rl_search(TuneCtx &t) {
             vv.push_back(0.0);
             gae(B, br.data(), vv.data(), o.rl_gamma, o.rl_mu, adv.data());
         }
+        std::vector<double> vbase(bv);   // value-target base: V_target = A_raw + V_old (reading c20)
+        if (o.rl_adv_norm) {   // advantage normalisation (PPO reference implementations; DESIGN.md c24)
+            const std::vector<double> raw(adv);
+            double mu = 0, var = 0;
+            for (double v : adv) mu += v;
+            mu /= B;
+            for (double v : adv) var += (v - mu) * (v - mu);
+            const double sd = std::sqrt(var / B) + 1e-8;
+            for (double &v : adv) v = (v - mu) / sd;
+            for (int j = 0; j < B; ++j) vbase[j] = bv[j] + raw[j] - adv[j];   // keeps V_target unnormalised
+        }
+        // every rl_restart_every updates, environments restart from the best-ever config
+        if (o.rl_restart_every > 0 && t.have_best && t.rounds % o.rl_restart_every == 0)
+            for (int e = 0; e < E; ++e) cur[e] = t.best;
         // ---- PPO epochs over shuffled minibatches (dropout active in the update forward) ----
         const int mb = std::max(1, std::min(o.rl_minibatch, B));
         std::vector<int> idx(B);
@@ -347,7 +361,7 @@ wpk_status rl_search(TuneCtx &t) {
                 for (int i = 0; i < n; ++i) {
                     const int j = idx[s0 + i];
                     std::copy(&bobs[(size_t)j * 17], &bobs[(size_t)j * 17 + 17], &ob[(size_t)i * 17]);
-                    lp[i] = blogp[j]; ad[i] = adv[j]; vo[i] = bv[j]; ac[i] = bact[j];
+                    lp[i] = blogp[j]; ad[i] = adv[j]; vo[i] = vbase[j]; ac[i] = bact[j];
                 }
                 for (auto &mv : mask) mv = (uniform_co(rng.next()) < keep) ? 1.0 : 0.0;
                 last_loss = ppo_loss_grad(net, n, ob.data(), ac.data(), lp.data(), ad.data(), vo.data(), consts,

@@ -224,20 +224,21 @@ def test_gae_and_observation_match_oracle():
 
 # --- search behaviour on synthetic surfaces (SPEC.md:601-602 analogue) ---------------------------
 def test_searches_beat_random_on_synthetic_surfaces():
+    """SPEC.md:602 analogue: at an equal budget of 512 distinct evaluations, GA and RL best-ever
+    <= random best-ever in >= 90% of 20 paired trials (RL with the paper's constants, PAPER.md:95,
+    103, 121; episodes restart from the incumbent, reading c23b)."""
     doms = simt_space()
     wins_ga = wins_rl = 0
-    for seed in range(10):
-        rng = np.random.default_rng(seed)
+    for seed in range(20):
+        rng = np.random.default_rng(1000 + seed)
         star = [d[int(rng.integers(len(d)))] for d in doms]
         while not valid(star):
             star = [d[int(rng.integers(len(d)))] for d in doms]
         syn = [10.0] + list(rng.uniform(0.05, 1.0, 7)) + star
         kw = dict(eval_mode="synthetic", synthetic=syn, family="simt", seed=seed)
-        rnd = _plan().tune("random", 256, **kw).best_us
-        ga = _plan().tune("ga", 256, **kw).best_us
-        rl = _plan().tune("rl", 256, rl_hidden=[64, 64, 64, 64], rl_horizon=16, rl_envs=4, rl_lr=1e-3,
-                          rl_alpha_mode=1, **kw).best_us
+        rnd = _plan().tune("random", 512, **kw).best_us
+        ga = _plan().tune("ga", 512, **kw).best_us
+        rl = _plan().tune("rl", 512, rl_hidden=[64, 64, 64, 64], rl_horizon=16, rl_envs=4, **kw).best_us
         wins_ga += ga <= rnd
         wins_rl += rl <= rnd
-    assert wins_ga >= 9
-    print("rl wins", wins_rl)
+    assert wins_ga >= 18 and wins_rl >= 18, (wins_ga, wins_rl)
