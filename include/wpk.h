@@ -119,6 +119,11 @@ typedef struct {
     int32_t rl_adv_norm;      /* 1 = normalise advantages per update batch (default 1)          */
     int32_t rl_restart_every; /* >0: envs restart from the best-ever config every N updates (1)  */
     int32_t max_seconds;      /* wall-clock cap for one tune (0 = none)                         */
+    const char *cache_dir;    /* if set: tuning-result cache. One JSON file per key =
+                               * operator identity (shapes, filter, stride, padding;
+                               * plus dilation, groups, dtype, layout, epilogue) + family + device.
+                               * A hit whose recorded budget >= the request costs 0 evaluations.
+                               * Writes are atomic (temp file + rename).                        */
 } wpk_tune_options;
 
 typedef struct wpk_plan_s *wpk_plan;

@@ -157,7 +157,7 @@ def make_options(**kw) -> L.TuneOptions:
     L.load().wpk_tune_options_init(ctypes.byref(o))
     keep = []
     for k, v in kw.items():
-        if k in ("record_path", "replay_path", "log_path"):
+        if k in ("record_path", "replay_path", "log_path", "cache_dir"):
             v = v.encode() if v is not None else None
             keep.append(v)
         elif k == "eval_mode" and isinstance(v, str):

@@ -249,7 +249,7 @@ Config default_config(const ConvDesc &d, int family) {
     }
     const long long mt = (d.M() + 127) / 128;
     if (bn == 256 && mt * ((d.k + 255) / 256) < 120) bn = 128;
-    c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c < 16) ? 2 : 0;
+    c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c < 16) ? 1 : 0;
     c.genes[5] = 2; c.genes[6] = 128;
     for (int st = 8; st >= 2; --st) {
         c.genes[1] = st;

@@ -8,6 +8,10 @@
 // their fitness records are all-gathered through the wpk_exchange_fn callback (NCCL via torch in
 // practice); every rank then runs the identical deterministic searcher update.
 #include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <cctype>
+#include <cstdlib>
 
 #include <algorithm>
 #include <chrono>
@@ -400,6 +404,52 @@ static wpk_status random_search(TuneCtx &t) {
     return WPK_OK;
 }
 
+// ---------------------------------------------------------------------------------------------------
+// tuning-result cache ("a caching mechanism to reuse search results")
+// ---------------------------------------------------------------------------------------------------
+static std::string cache_key(const Plan &p, int family, int measured_mode) {
+    const ConvDesc &d = p.d;
+    char b[512];
+    std::string dev = "offline";
+    if (measured_mode) {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, p.device) == cudaSuccess) {
+            char t[400];
+            snprintf(t, sizeof t, "%.200s_sm%d_cc%d%d", prop.name, prop.multiProcessorCount, prop.major, prop.minor);
+            dev = t;
+            for (char &ch : dev)
+                if (!isalnum((unsigned char)ch)) ch = '_';
+        } else {
+            cudaGetLastError();
+        }
+    }
+    snprintf(b, sizeof b, "n%d_c%d_h%d_w%d_k%d_r%d_s%d_st%dx%d_p%dx%d_d%dx%d_g%d_l%d_e%d_t%d_f%d_", d.n, d.c, d.h, d.w,
+             d.k, d.r, d.s, d.sh, d.sw, d.ph, d.pw, d.dh, d.dw, d.g, d.layout, d.epilogue, d.dtype, family);
+    return std::string(b) + dev + "_abi" + std::to_string(WPK_ABI_VERSION);
+}
+
+static bool cache_lookup(const std::string &path, int budget, Config *cfg, double *beta) {
+    FILE *fp = fopen(path.c_str(), "r");
+    if (!fp) return false;
+    char buf[2048];
+    size_t n = fread(buf, 1, sizeof buf - 1, fp);
+    fclose(fp);
+    buf[n] = 0;
+    const char *bb = strstr(buf, "\"budget\"");
+    if (!bb || !(bb = strchr(bb, ':')) || atoi(bb + 1) < budget) return false;
+    return parse_record(buf, cfg, beta);
+}
+
+static void cache_store(const std::string &path, const Config &cfg, double beta, int budget, int search) {
+    const std::string tmp = path + ".tmp" + std::to_string((long long)getpid());
+    FILE *fp = fopen(tmp.c_str(), "w");
+    if (!fp) return;
+    fprintf(fp, "{\"family\": %d, \"genes\": %s, \"beta_us\": %s, \"budget\": %d, \"search\": %d}\n", cfg.family,
+            genes_json(cfg).c_str(), dbl(beta).c_str(), budget, search);
+    fclose(fp);
+    rename(tmp.c_str(), path.c_str());
+}
+
 }  // namespace wpk
 
 using namespace wpk;
@@ -427,6 +477,21 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
     t.sp = &family_space(t.family);
     t.budget = budget;
     t.t_start = wall_seconds();
+    std::string cpath;
+    if (t.o.cache_dir && t.o.cache_dir[0]) {
+        cpath = std::string(t.o.cache_dir) + "/" + cache_key(*p, t.family, t.o.eval_mode == WPK_EVAL_MEASURED) + ".json";
+        Config hit;
+        double hb;
+        if (cache_lookup(cpath, budget, &hit, &hb) && config_valid(p->d, hit, nullptr)) {
+            p->cfg = hit;
+            p->packed_for = nullptr;
+            p->best_us = hb;
+            p->measured = 0;
+            p->rounds = 0;
+            p->tune_seconds = wall_seconds() - t.t_start;
+            return WPK_OK;
+        }
+    }
     if (t.o.eval_mode == WPK_EVAL_REPLAY) {
         if (!t.o.replay_path || !load_replay(t, t.o.replay_path))
             return fail(WPK_ERR_INVALID_ARGUMENT, "replay mode needs a readable replay_path");
@@ -462,6 +527,7 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
     p->cfg = t.best;
     p->packed_for = nullptr;
     p->best_us = t.best_beta;
+    if (!cpath.empty() && t.o.rank == 0) cache_store(cpath, t.best, t.best_beta, budget, (int)search);
     p->measured = (int)t.order.size();
     p->rounds = t.rounds;
     p->tune_seconds = wall_seconds() - t.t_start;

@@ -242,3 +242,20 @@ def test_searches_beat_random_on_synthetic_surfaces():
         wins_ga += ga <= rnd
         wins_rl += rl <= rnd
     assert wins_ga >= 18 and wins_rl >= 18, (wins_ga, wins_rl)
+
+
+def test_tuning_cache_roundtrip(tmp_path):
+    """PAPER.md:179 result cache: a second tune of an identical operator costs 0 evaluations and
+    returns the stored config, across plan objects (i.e. across processes); a larger budget misses."""
+    syn = [10.0] + [0.5] * 7 + [8, 4, 2, 2, 1, 2, 4]
+    kw = dict(eval_mode="synthetic", synthetic=syn, family="simt", seed=1, cache_dir=str(tmp_path))
+    r1 = _plan().tune("ga", 200, **kw)
+    assert r1.measured > 0 and len(list(tmp_path.glob("*.json"))) == 1
+    r2 = _plan().tune("ga", 200, **kw)
+    assert r2.measured == 0 and r2.genes == r1.genes and r2.best_us == r1.best_us
+    r3 = _plan().tune("random", 100, **kw)          # smaller budget: hit
+    assert r3.measured == 0
+    r4 = _plan().tune("ga", 400, **kw)              # larger budget: miss, re-tune, overwrite
+    assert r4.measured > 0
+    other = Conv2dPlan(1, 4, 9, 9, 8, 3, 3, 1, 1, layout="nchw", dtype="f32", device=0)
+    assert other.tune("ga", 50, **kw).measured > 0  # different operator: miss
