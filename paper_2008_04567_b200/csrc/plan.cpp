@@ -71,8 +71,8 @@ static Space make_space(int family) {
         sp.names = {"T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"};
     } else if (family == WPK_FAMILY_UMMA) {
         sp.dom = {{16, 32, 64, 96, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8}, {1, 2, 4, 8, 16},
-                  {0, 1}, {0, 1, 2}, {1, 2}, {128, 256}};
-        sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "RASTER", "A_MODE", "ACC_STAGES", "BLOCK_M"};
+                  {0, 1, 2, 3}, {0, 1, 2}, {1, 2}, {128, 256}};
+        sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "MODE", "A_MODE", "ACC_STAGES", "BLOCK_M"};
     } else {
         sp.dom = {{1, 2, 4, 8}, {1, 2, 4}, {64, 128, 256, 512}, {1}, {0}, {0}, {0}};
         sp.names = {"VEC_C", "PIX_PER_THREAD", "THREADS", "-", "-", "-", "-"};
@@ -127,7 +127,8 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->bk = 128 / e;           // one 128-byte swizzle atom of K per stage
     g->stages = cfg.genes[1];
     g->splits = cfg.genes[2];
-    g->raster = cfg.genes[3];
+    g->raster = cfg.genes[3] & 1;
+    g->pair = (cfg.genes[3] >> 1) & 1;   // tcgen05 CTA pair (cta_group::2): 256-row tiles over two SMs
     g->ctas_per_sm = 1;
     g->a_mode = cfg.genes[4];
     g->acc_stages = cfg.genes[5];
@@ -152,7 +153,12 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->m_tiles = (int)((d.M() + g->bm - 1) / g->bm);
     g->n_tiles = (d.k + g->bn - 1) / g->bn;
     g->work = (long long)g->m_tiles * g->n_tiles * g->splits;
-    size_t stage = (size_t)g->bm * 128 + (size_t)g->bn * 128;
+    if (g->pair) {
+        if (g->bm != 256) return no("a CTA pair computes 256-row tiles (BLOCK_M must be 256)");
+        if (g->splits != 1) return no("CTA pairs do not support split-K");
+        if (g->a_mode == 2) return no("CTA pairs do not support the gather producer");
+    }
+    size_t stage = g->pair ? (size_t)128 * 128 + (size_t)(g->bn / 2) * 128 : (size_t)g->bm * 128 + (size_t)g->bn * 128;
     if (g->bm == 256 && g->a_mode == 0 && !(d.r == 1 && d.s == 1 && d.sh == 1 && d.sw == 1 && d.ph == 0 && d.pw == 0))
         ;   // a 256-pixel im2col box is one TMA (pixelsPerColumn <= 1024)
     // A operand: a 1x1 / stride-1 / unpadded conv is a plain GEMM on x viewed as [N*H*W][C]
@@ -176,7 +182,7 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     off += 256;
     g->smem_bytes = 1024 /*align slack*/ + off;
     if (g->smem_bytes > smem_cap) return no("STAGES x tile exceeds shared memory");
-    int cols = g->acc_stages * (g->bm / 128) * g->bn;
+    int cols = g->acc_stages * (g->pair ? 1 : g->bm / 128) * g->bn;
     int alloc = 32;
     while (alloc < cols) alloc <<= 1;
     g->tmem_cols = alloc;

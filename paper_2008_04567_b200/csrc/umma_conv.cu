@@ -24,6 +24,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -315,7 +316,7 @@ __device__ __noinline__ void splitk_fixup(const UmmaArgs &a, const float *sBias,
 
 // 12 warps: 0 = A producer, 1 = TMEM allocator + MMA issuer, 2 = B producer, 3 = spare,
 // 4..11 = epilogue (two groups of four; warp w reads TMEM lanes [32*(w%4), +32)).
-template <int DT, bool kGather>
+template <int DT, bool kGather, bool kPair>
 __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
     umma_conv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmY, const __grid_constant__ UmmaArgs a) {
@@ -325,9 +326,14 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
     uint8_t *smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
-    const uint32_t a_bytes = (uint32_t)a.bm * 128u;
-    const uint32_t b_bytes = (uint32_t)a.bn * 128u;
-    const int nsub = a.bm / 128;                                       // 128-row MMAs per tile
+    // CTA pair (cta_group::2): each CTA holds 128 rows of A and half of B; the pair computes 256 x BN
+    const uint32_t a_bytes = (uint32_t)(kPair ? 128 : a.bm) * 128u;
+    const uint32_t b_bytes = (uint32_t)(kPair ? a.bn / 2 : a.bn) * 128u;
+    const int nsub = kPair ? 1 : a.bm / 128;                           // 128-row MMAs per tile per CTA
+    const uint32_t crank = kPair ? ptx::cluster_ctarank() : 0u;
+    const bool leader = (crank == 0);
+    const long long wstart = kPair ? (long long)(blockIdx.x >> 1) : (long long)blockIdx.x;
+    const long long wstep = kPair ? (long long)(gridDim.x >> 1) : (long long)gridDim.x;
     uint8_t *smA = smem;
     uint8_t *smB = smem + (size_t)a.stages * a_bytes;
     uint8_t *sEpi = smem + a.epi_off;                                  // [8 warps][2][32 rows][128 B]
@@ -354,13 +360,18 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&tfull[s], 1);
-            ptx::mbar_init(&tempty[s], 8);     // 8 epilogue warps
+            ptx::mbar_init(&tempty[s], kPair ? 16 : 8);   // 8 epilogue warps (x2 CTAs for a pair)
         }
         ptx::fence_mbar_init();
     }
     if (warp == 1) {
-        ptx::tmem_alloc(tmem_holder, a.tmem_cols);
-        ptx::tmem_relinquish();
+        if (kPair) {
+            ptx::tmem_alloc2(tmem_holder, a.tmem_cols);
+            ptx::tmem_relinquish2();
+        } else {
+            ptx::tmem_alloc(tmem_holder, a.tmem_cols);
+            ptx::tmem_relinquish();
+        }
     }
     // Programmatic dependent launch: everything above overlapped the previous kernel's tail; inputs
     // (x, w, b) may be produced by it, so wait for its completion before the first global read.
@@ -373,6 +384,7 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if (kPair) ptx::cluster_sync();   // peer barriers initialised before any remote arrive / TMA
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     if (dbg && threadIdx.x == 0) dbg[1] = ptx::globaltimer();
@@ -384,10 +396,10 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
             uint32_t stage = 0, phase = 0;
             const uint32_t tx = isA ? a_bytes : b_bytes;
             uint8_t *dst0 = isA ? smA : smB;
-            for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
+            for (long long w = wstart; w < a.work; w += wstep) {
                 const WorkPos wp = decode_work(w, a);
-                const long long m0 = (long long)wp.mt * a.bm;
-                const int n0 = wp.nt * a.bn;
+                const long long m0 = (long long)wp.mt * a.bm + crank * 128;
+                const int n0 = wp.nt * a.bn + (int)crank * (a.bn / 2);
                 int wc = 0, hc = 0, nimg = 0;
                 if (isA && !a.a_tiled) {
                     nimg = (int)(m0 / a.PQ);
@@ -404,15 +416,27 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
                 int r = rs / a.S, s = rs % a.S;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], tx);
                     uint8_t *dst = dst0 + stage * tx;
-                    if (!isA)
-                        ptx::tma_load_3d(dst, &tmB, &full[stage], cb * a.bk, rs, n0);
-                    else if (a.a_tiled)
-                        ptx::tma_load_2d(dst, &tmA, &full[stage], cb * a.bk, (int)m0);
-                    else
-                        ptx::tma_load_im2col_4d(dst, &tmA, &full[stage], cb * a.bk, wc, hc, nimg,
-                                                (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                    if (kPair) {
+                        // both CTAs' bytes land on the leader's barrier; only the leader arms it
+                        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * tx);
+                        if (!isA)
+                            ptx::tma_load_3d_pair(dst, &tmB, &full[stage], cb * a.bk, rs, n0);
+                        else if (a.a_tiled)
+                            ptx::tma_load_2d_pair(dst, &tmA, &full[stage], cb * a.bk, (int)m0);
+                        else
+                            ptx::tma_load_im2col_4d_pair(dst, &tmA, &full[stage], cb * a.bk, wc, hc, nimg,
+                                                         (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                    } else {
+                        ptx::mbar_arrive_expect_tx(&full[stage], tx);
+                        if (!isA)
+                            ptx::tma_load_3d(dst, &tmB, &full[stage], cb * a.bk, rs, n0);
+                        else if (a.a_tiled)
+                            ptx::tma_load_2d(dst, &tmA, &full[stage], cb * a.bk, (int)m0);
+                        else
+                            ptx::tma_load_im2col_4d(dst, &tmA, &full[stage], cb * a.bk, wc, hc, nimg,
+                                                    (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                    }
                     if (++cb == a.c_blocks) {
                         cb = 0;
                         ++rs;
@@ -429,7 +453,7 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
         const int t = threadIdx.x - 384;                       // 0..127
         const int RSC = a.R * a.S * a.C;
         uint32_t stage = 0, phase = 0;
-        for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
+        for (long long w = wstart; w < a.work; w += wstep) {
             const WorkPos wp = decode_work(w, a);
             const int kb0 = wp.split * a.kb_per_split;
             const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
@@ -493,13 +517,13 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer (single thread) =====================
-        if (lane == 0) {
+        // ===================== MMA issuer (single thread; the leader CTA of a pair) =====================
+        if (lane == 0 && leader) {
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
             const uint64_t a_desc0 = ptx::sw128_kmajor_desc(ptx::smem_u32(smA));
             const uint64_t b_desc0 = ptx::sw128_kmajor_desc(ptx::smem_u32(smB));
             const uint32_t acc_cols = (uint32_t)(nsub * a.bn);
-            for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
+            for (long long w = wstart; w < a.work; w += wstep) {
                 const WorkPos wp = decode_work(w, a);
                 const int kb0 = wp.split * a.kb_per_split;
                 const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
@@ -512,16 +536,24 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
                     if (dbg && w == blockIdx.x && kb == kb0) dbg[2] = ptx::globaltimer();
                     const uint64_t ad = a_desc0 + (uint64_t)((stage * a_bytes) >> 4);
                     const uint64_t bd = b_desc0 + (uint64_t)((stage * b_bytes) >> 4);
-                    for (int h = 0; h < nsub; ++h) {
+                    if (kPair) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)   // 4 x 32 bytes of K per 128-byte stage (+2 desc units)
-                            ptx::umma<kTF32>(d_tmem + h * a.bn, ad + h * (16384 >> 4) + 2 * kk, bd + 2 * kk, a.idesc,
-                                             (kb > kb0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < 4; ++kk)
+                            ptx::umma2<kTF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        ptx::umma_commit2_multicast(&empty[stage]);   // frees the stage in both CTAs
+                    } else {
+                        for (int h = 0; h < nsub; ++h) {
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)   // 4 x 32 bytes of K per 128-byte stage (+2 desc units)
+                                ptx::umma<kTF32>(d_tmem + h * a.bn, ad + h * (16384 >> 4) + 2 * kk, bd + 2 * kk, a.idesc,
+                                                 (kb > kb0 || kk > 0) ? 1u : 0u);
+                        }
+                        ptx::umma_commit(&empty[stage]);   // frees this smem stage when the MMAs finish
                     }
-                    ptx::umma_commit(&empty[stage]);   // frees this smem stage when the MMAs finish
                     if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
                 }
-                ptx::umma_commit(&tfull[acc]);         // accumulator ready for the epilogue
+                if (kPair) ptx::umma_commit2_multicast(&tfull[acc]);   // both CTAs' accumulator halves ready
+                else ptx::umma_commit(&tfull[acc]);                     // accumulator ready for the epilogue
                 if (dbg && w == blockIdx.x) dbg[3] = ptx::globaltimer();
                 if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
             }
@@ -536,7 +568,7 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
         const uint32_t acc_cols = (uint32_t)(nsub * a.bn);
         const int cw = a.epi_tma ? (final_out ? (int)(128 / sizeof(T)) : 32) : 16;
         const int nchunks = (a.bn + cw - 1) / cw;
-        for (long long w = blockIdx.x; w < a.work; w += gridDim.x) {
+        for (long long w = wstart; w < a.work; w += wstep) {
             const WorkPos wp = decode_work(w, a);
             const int n0 = wp.nt * a.bn;
             ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -544,7 +576,7 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
             // slabs = (h, chunk) pairs; group g takes h == g when nsub == 2, else every other chunk
             for (int h = 0; h < nsub; ++h) {
                 if (nsub == 2 && h != grp) continue;
-                const int mrow = wp.mt * a.bm + h * 128 + quarter * 32;
+                const int mrow = wp.mt * a.bm + (int)crank * 128 + h * 128 + quarter * 32;
                 const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * acc_cols + h * a.bn;
                 for (int ci = (nsub == 2 ? 0 : grp); ci < nchunks; ci += (nsub == 2 ? 1 : 2)) {
                     const int c0 = ci * cw;
@@ -561,10 +593,13 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
             __syncwarp();
             if (dbg && warp == 4 && lane == 0 && w == blockIdx.x) dbg[4] = ptx::globaltimer();
             if (dbg && warp == 4 && lane == 0) {   // per-tile epilogue completion times (first 8 tiles)
-                const long long it = (w - blockIdx.x) / gridDim.x;
+                const long long it = (w - wstart) / wstep;
                 if (it < 8) dbg[8 + it] = ptx::globaltimer();
             }
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);   // TMEM free: the MMA may start the next tile
+            if (lane == 0) {                                  // TMEM free: the MMA may start the next tile
+                if (kPair) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+                else ptx::mbar_arrive(&tempty[acc]);
+            }
             if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
             if (!final_out) splitk_fixup<T>(a, sBias, sFlag, wp, nsub, warp, lane);
         }
@@ -573,10 +608,12 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
     }
 
     __syncthreads();
+    if (kPair) ptx::cluster_sync();   // the peer no longer touches our barriers / TMEM
     if (dbg && threadIdx.x == 0) dbg[6] = ptx::globaltimer();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, a.tmem_cols);
+        if (kPair) ptx::tmem_dealloc2(tmem_base, a.tmem_cols);
+        else ptx::tmem_dealloc(tmem_base, a.tmem_cols);
     }
 }
 
@@ -620,11 +657,11 @@ static uint32_t make_idesc(int dt, int bm, int bn) {
     return d;
 }
 
-template <int DT, bool G>
+template <int DT, bool G, bool PAIR>
 static bool set_smem_attr() {
     static bool done = false;
     if (!done) {
-        if (cudaFuncSetAttribute(umma_conv_kernel<DT, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+        if (cudaFuncSetAttribute(umma_conv_kernel<DT, G, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
             cudaSuccess)
             return false;
         done = true;
@@ -661,7 +698,7 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
     } else if (g.a_tiled) {
         cuuint64_t dims[2] = {(cuuint64_t)g.cpad, (cuuint64_t)L.a_rows};
         cuuint64_t strides[1] = {(cuuint64_t)g.cpad * e};
-        cuuint32_t box[2] = {(cuuint32_t)g.bk, (cuuint32_t)g.bm};
+        cuuint32_t box[2] = {(cuuint32_t)g.bk, (cuuint32_t)(g.pair ? 128 : g.bm)};
         cuuint32_t estr[2] = {1, 1};
         CUresult r = encode_tiled()(&tmA, tdt, 2, const_cast<void *>(L.x), dims, strides, box, estr,
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -678,7 +715,7 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
         int upper[2] = {L.pad_w - (L.S - 1) * L.dil_w, L.pad_h - (L.R - 1) * L.dil_h};
         cuuint32_t estr[4] = {1, (cuuint32_t)L.stride_w, (cuuint32_t)L.stride_h, 1};
         CUresult r = encode_im2col()(&tmA, tdt, 4, const_cast<void *>(L.x), dims, strides, lower, upper,
-                                     (cuuint32_t)g.bk, (cuuint32_t)g.bm, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                     (cuuint32_t)g.bk, (cuuint32_t)(g.pair ? 128 : g.bm), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
@@ -716,7 +753,7 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
     {
         cuuint64_t dims[3] = {(cuuint64_t)g.cpad, (cuuint64_t)L.b_rs, (cuuint64_t)L.K};
         cuuint64_t strides[2] = {(cuuint64_t)g.cpad * e, (cuuint64_t)g.cpad * e * L.b_rs};
-        cuuint32_t box[3] = {(cuuint32_t)g.bk, 1, (cuuint32_t)g.bn};
+        cuuint32_t box[3] = {(cuuint32_t)g.bk, 1, (cuuint32_t)(g.pair ? g.bn / 2 : g.bn)};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = encode_tiled()(&tmB, tdt, 3, const_cast<void *>(L.w), dims, strides, box, estr,
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -745,7 +782,7 @@ launch:
     a.c_blocks = g.c_blocks; a.num_kb = g.num_kb; a.kb_per_split = g.kb_per_split; a.splits = g.splits;
     a.m_tiles = g.m_tiles; a.n_tiles = g.n_tiles; a.raster = g.raster; a.work = g.work;
     a.bm = g.bm; a.bn = g.bn; a.bk = g.bk; a.stages = g.stages; a.acc_stages = g.acc_stages;
-    a.idesc = make_idesc(dt, 128, g.bn);   // every MMA is 128 x BN (BLOCK_M 256 = two of them)
+    a.idesc = make_idesc(dt, g.pair ? 256 : 128, g.bn);   // 1-CTA: 128 x BN (BLOCK_M 256 = two); pair: 256 x BN
     a.tmem_cols = (uint32_t)g.tmem_cols;
     a.epilogue = L.epilogue;
     a.out_nchw = L.out_nchw;
@@ -764,16 +801,20 @@ launch:
     cudaStream_t st = (cudaStream_t)L.stream;
     long long grid = (long long)L.sm_count * g.ctas_per_sm;
     if (grid > g.work) grid = g.work;
+    if (g.pair) grid = 2 * std::min<long long>(g.work, L.sm_count / 2);
     int launches = 0;
     cudaError_t ce = cudaSuccess;
 #define WPK_LAUNCH_UMMA(DTV)                                                                          \
     do {                                                                                              \
         if (g.a_mode == 2) {                                                                          \
-            if (!set_smem_attr<DTV, true>()) { *err = "cudaFuncSetAttribute failed"; return -1; }     \
-            ce = cudaLaunchKernelEx(&lc, umma_conv_kernel<DTV, true>, tmA, tmB, tmY, a);             \
+            if (!set_smem_attr<DTV, true, false>()) { *err = "cudaFuncSetAttribute failed"; return -1; } \
+            ce = cudaLaunchKernelEx(&lc, umma_conv_kernel<DTV, true, false>, tmA, tmB, tmY, a);      \
+        } else if (g.pair) {                                                                          \
+            if (!set_smem_attr<DTV, false, true>()) { *err = "cudaFuncSetAttribute failed"; return -1; } \
+            ce = cudaLaunchKernelEx(&lc, umma_conv_kernel<DTV, false, true>, tmA, tmB, tmY, a);      \
         } else {                                                                                      \
-            if (!set_smem_attr<DTV, false>()) { *err = "cudaFuncSetAttribute failed"; return -1; }    \
-            ce = cudaLaunchKernelEx(&lc, umma_conv_kernel<DTV, false>, tmA, tmB, tmY, a);            \
+            if (!set_smem_attr<DTV, false, false>()) { *err = "cudaFuncSetAttribute failed"; return -1; } \
+            ce = cudaLaunchKernelEx(&lc, umma_conv_kernel<DTV, false, false>, tmA, tmB, tmY, a);     \
         }                                                                                             \
     } while (0)
     cudaLaunchConfig_t lc{};
@@ -781,11 +822,22 @@ launch:
     lc.blockDim = dim3(g.a_mode == 2 ? 512 : 384);
     lc.dynamicSmemBytes = g.smem_bytes;
     lc.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int nattr = 0;
+    if (!getenv("WPK_NO_PDL")) {
+        attr[nattr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[nattr].val.programmaticStreamSerializationAllowed = 1;
+        ++nattr;
+    }
+    if (g.pair) {   // the two CTAs of a tcgen05 CTA pair form a cluster
+        attr[nattr].id = cudaLaunchAttributeClusterDimension;
+        attr[nattr].val.clusterDim.x = 2;
+        attr[nattr].val.clusterDim.y = 1;
+        attr[nattr].val.clusterDim.z = 1;
+        ++nattr;
+    }
     lc.attrs = attr;
-    lc.numAttrs = getenv("WPK_NO_PDL") ? 0 : 1;
+    lc.numAttrs = nattr;
     if (dt == DT_F16) WPK_LAUNCH_UMMA(DT_F16);
     else if (dt == DT_BF16) WPK_LAUNCH_UMMA(DT_BF16);
     else WPK_LAUNCH_UMMA(DT_TF32);

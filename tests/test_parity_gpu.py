@@ -67,8 +67,8 @@ def test_epilogues(dtype, epilogue):
 def _umma_space():
     bns = [16, 32, 64, 96, 128, 192, 256]
     out = []
-    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1], [0, 1, 2], [1, 2],
-                                                          [128, 256]):
+    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1, 2, 3], [0, 1, 2],
+                                                          [1, 2], [128, 256]):
         out.append((bn, st, sp, ra, amode, acc, bm))
     return out
 
@@ -116,13 +116,39 @@ def test_umma_1x1_and_epilogue_paths(dtype, env, monkeypatch):
                       (32, 4, 1, 0, 0, 2, 128), (96, 5, 2, 0, 0, 2, 128), (192, 3, 1, 1, 0, 2, 128),
                       (64, 4, 1, 0, 1, 2, 128), (128, 4, 2, 0, 1, 2, 128), (64, 4, 1, 0, 0, 2, 256),
                       (128, 3, 2, 0, 0, 1, 256), (96, 4, 1, 1, 0, 2, 256), (32, 4, 2, 0, 1, 2, 256),
-                      (64, 4, 1, 0, 2, 2, 128), (128, 3, 2, 0, 2, 2, 256), (256, 2, 1, 0, 2, 1, 128)]:
+                      (64, 4, 1, 0, 2, 2, 128), (128, 3, 2, 0, 2, 2, 256), (256, 2, 1, 0, 2, 1, 128),
+                      (128, 4, 1, 2, 0, 2, 256), (256, 3, 1, 3, 0, 2, 256), (64, 4, 1, 2, 1, 2, 256),
+                      (32, 4, 1, 2, 0, 1, 256), (192, 3, 1, 2, 0, 2, 256)]:
             if not plan.config_valid(1, list(genes)):
                 continue
             plan.set_config(1, list(genes))
             y = plan.run(xl, wl, bc)
             torch.cuda.synchronize()
             assert_bit_exact(from_layout(y.cpu(), "nhwc"), ref)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_cta_pair_configs(dtype):
+    """tcgen05 CTA pairs (cta_group::2): 3x3 and strided shapes with M and K tails."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import to_layout, from_layout
+    for L in [ConvLayer("p3", 2, 64, 17, 19, 160, 3, 3, 1, 1), ConvLayer("p3s2", 3, 128, 15, 15, 96, 3, 3, 2, 1)]:
+        x, w, b = workloads.generate(L, dtype, "int", seed=29)
+        ref = oracle_full(L, x, w, b)
+        plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype=dtype)
+        xl, wl = to_layout(x, w, "nhwc")
+        xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
+        n = 0
+        for bn, st, mode, acc in itertools.product([32, 64, 128, 256], [2, 4], [2, 3], [1, 2]):
+            genes = [bn, st, 1, mode, 0, acc, 256]
+            if not plan.config_valid(1, genes):
+                continue
+            plan.set_config(1, genes)
+            y = plan.run(xl, wl, bc)
+            torch.cuda.synchronize()
+            assert_bit_exact(from_layout(y.cpu(), "nhwc"), ref)
+            n += 1
+        assert n >= 8
 
 
 def test_simt_every_tile_template():
