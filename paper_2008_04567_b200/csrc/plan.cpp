@@ -141,6 +141,7 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
         g->c_blocks = (g->cpad + g->bk - 1) / g->bk;
         g->num_kb = g->c_blocks;
         if (g->a_mode == 1 && (double)d.M() * g->cpad * e > 4.0e9) return no("explicit im2col matrix larger than 4 GB");
+        if (g->a_mode == 1 && (size_t)128 * g->cpad * e > 48 * 1024) return no("explicit im2col row block exceeds 48 KB of smem");
         if (g->a_mode == 2 && (double)d.n * d.c * d.h * d.w >= 2147483647.0) return no("gather producer needs < 2^31 input elements");
     } else {
         g->cpad = round_up(d.c, 16 / e);    // TMA global strides must be multiples of 16 B
@@ -255,8 +256,11 @@ Config default_config(const ConvDesc &d, int family) {
     }
     const long long mt = (d.M() + 127) / 128;
     if (bn == 256 && mt * ((d.k + 255) / 256) < 120) bn = 128;
+    // large layers: a tcgen05 CTA pair (256 x BLOCK_N over two SMs) halves B traffic per SM
+    const bool big = ((d.M() + 255) / 256) * ((d.k + bn - 1) / bn) >= 2 * 148 && bn >= 128 && d.c >= 64;
     c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c < 16) ? 1 : 0;
     c.genes[5] = 2; c.genes[6] = 128;
+    if (big) { c.genes[3] = 2; c.genes[6] = 256; }
     for (int st = 8; st >= 2; --st) {
         c.genes[1] = st;
         if (config_valid(d, c, nullptr)) break;

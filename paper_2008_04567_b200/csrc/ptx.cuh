@@ -74,6 +74,12 @@ __device__ __forceinline__ void tma_load_3d(void *smem, const CUtensorMap *m, ui
         "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *m, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load_im2col_4d(void *smem, const CUtensorMap *m, uint64_t *bar, int c,
                                                    int w, int h, int n, uint16_t off_w, uint16_t off_h) {
     asm volatile(

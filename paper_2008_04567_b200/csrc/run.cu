@@ -62,36 +62,44 @@ __global__ void pack_krsc_kernel(const T *__restrict__ w, T *__restrict__ out, i
         out[i] = v;
     }
 }
-// Explicit im2col (A_MODE 1): A[m][kg], kg = (r*S + s)*C + c for kg < R*S*C, else 0. One thread
-// builds one output row: (n, p, q) decoded once, taps walked incrementally, 16-byte stores.
+// Explicit im2col (A_MODE 1): A[m][kg], kg = (r*S + s)*C + c for kg < R*S*C, else 0. A block of 128
+// threads builds 128 consecutive rows in shared memory (one row per thread, taps walked
+// incrementally), then writes the contiguous 128 x kgp block to global memory with coalesced
+// 16-byte stores.
 template <typename T>
 __global__ void im2col_kernel(const T *__restrict__ x, T *__restrict__ out, int N, int C, int H, int W, int P, int Q,
                               int R, int S, int sh, int sw, int ph, int pw, int dh, int dw, int kgp, int nchw) {
-    constexpr int VEC = 16 / sizeof(T);
+    extern __shared__ uint4 im2col_smem[];
+    T *rows = reinterpret_cast<T *>(im2col_smem);
     const long long M = (long long)N * P * Q;
-    for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < M; m += (long long)gridDim.x * blockDim.x) {
-        const int q = (int)(m % Q);
-        const long long t = m / Q;
-        const int p = (int)(t % P);
-        const int n = (int)(t / P);
-        const int h0 = p * sh - ph, w0 = q * sw - pw;
-        T *dst = out + m * kgp;
-        int r = 0, s = 0, c = 0;
-        for (int kv = 0; kv < kgp; kv += VEC) {
-            T v[VEC];
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) {
+    const int kg_real = R * S * C;
+    for (long long m0 = (long long)blockIdx.x * 128; m0 < M; m0 += (long long)gridDim.x * 128) {
+        const long long m = m0 + threadIdx.x;
+        T *row = rows + (size_t)threadIdx.x * kgp;
+        if (m < M) {
+            const int q = (int)(m % Q);
+            const long long t = m / Q;
+            const int p = (int)(t % P);
+            const int n = (int)(t / P);
+            const int h0 = p * sh - ph, w0 = q * sw - pw;
+            int r = 0, s = 0, c = 0;
+            for (int kg = 0; kg < kgp; ++kg) {
                 T val = T(0.f);
-                if (r < R) {
+                if (kg < kg_real) {
                     const int hi = h0 + r * dh, wi = w0 + s * dw;
                     if (hi >= 0 && hi < H && wi >= 0 && wi < W)
                         val = nchw ? x[(((long long)n * C + c) * H + hi) * W + wi] : x[(((long long)n * H + hi) * W + wi) * C + c];
                     if (++c == C) { c = 0; if (++s == S) { s = 0; ++r; } }
                 }
-                v[j] = val;
+                row[kg] = val;
             }
-            *reinterpret_cast<uint4 *>(dst + kv) = *reinterpret_cast<uint4 *>(v);
         }
+        __syncthreads();
+        const long long nrows = (M - m0 < 128) ? (M - m0) : 128;
+        const long long n16 = nrows * kgp * (long long)sizeof(T) / 16;
+        uint4 *dst = reinterpret_cast<uint4 *>(out + m0 * kgp);
+        for (long long i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = im2col_smem[i];
+        __syncthreads();
     }
 }
 // Weights for explicit im2col: out[k][(r*S+s)*C + c] (zero padded to kgp) from KCRS or KRSC.
@@ -140,7 +148,7 @@ static void launch_aux_t(int which, const void *src, void *dst, const ConvDesc &
         nhwc_pad_kernel<T><<<grid_for((long long)d.n * d.h * d.w * cp, sm), 256, 0, st>>>(
             (const T *)src, (T *)dst, (long long)d.n * d.h * d.w, d.c, cp);
     else if (which == 4)
-        im2col_kernel<T><<<grid_for(d.M(), sm), 256, 0, st>>>((const T *)src, (T *)dst, d.n, d.c, d.h, d.w, d.p,
+        im2col_kernel<T><<<grid_for(d.M() * 2, sm), 128, (size_t)128 * cp * sizeof(T), st>>>((const T *)src, (T *)dst, d.n, d.c, d.h, d.w, d.p,
                                                                      d.q, d.r, d.s, d.sh, d.sw, d.ph, d.pw, d.dh, d.dw,
                                                                      cp, d.layout == WPK_NCHW);
     else if (which == 5)

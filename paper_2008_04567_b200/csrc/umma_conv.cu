@@ -373,15 +373,25 @@ __global__ void __launch_bounds__(kGather ? 512 : 384, 1)
             ptx::tmem_relinquish();
         }
     }
-    // Programmatic dependent launch: everything above overlapped the previous kernel's tail; inputs
-    // (x, w, b) may be produced by it, so wait for its completion before the first global read.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // Programmatic dependent launch: this prologue overlaps the previous kernel's tail. Weights and
+    // bias are inference constants, so the bias is staged and the first weight tiles of
+    // this CTA are prefetched into L2 before waiting; activations (which the previous layer may
+    // produce) are only read after griddepcontrol.wait.
     if (warp >= 4) {   // bias -> smem once (fp32); zero when there is no bias or for split-K partials
         const T *bias = static_cast<const T *>(a.bias);
         for (int k = threadIdx.x - 128; k < a.K; k += 256)
             sBias[k] = (a.epilogue >= 1) ? ld_bias(bias, k) : 0.f;
     }
+    if (warp == 2 && lane == 0 && wstart < a.work) {
+        const WorkPos wp = decode_work(wstart, a);
+        const int n0 = wp.nt * a.bn + (int)crank * (kPair ? a.bn / 2 : 0);
+        const int kb0 = wp.split * a.kb_per_split;
+        const int kb1 = min(a.num_kb, kb0 + min(a.kb_per_split, a.stages));
+        for (int kb = kb0; kb < kb1; ++kb)
+            ptx::tma_prefetch_3d(&tmB, (kb % a.c_blocks) * a.bk, kb / a.c_blocks, n0);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     ptx::tc_fence_before();
     __syncthreads();
     if (kPair) ptx::cluster_sync();   // peer barriers initialised before any remote arrive / TMA
