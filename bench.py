@@ -159,7 +159,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="wpk", choices=["wpk", "reference"])
     ap.add_argument("--batch", type=int, default=32, help="images per GPU")
-    ap.add_argument("--tune-budget", type=int, default=24, help="distinct configs measured per unique layer")
+    ap.add_argument("--tune-budget", type=int, default=48, help="distinct configs measured per unique layer")
     ap.add_argument("--search", default="ga", choices=["ga", "rl", "random", "none"])
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -134,8 +134,14 @@ struct GpuBench {
             cudaEventElapsedTime(&ms, e0, e1);
             t.push_back(ms * 1000.f);
         }
+        // Event timestamps on this part advance in ~2 us steps, so a median of quantised samples is
+        // itself quantised; the mean of the middle half keeps the median's robustness to outliers
+        // while resolving differences below one timer step (launch jitter dithers the samples).
         std::sort(t.begin(), t.end());
-        return t[t.size() / 2];
+        const size_t lo = t.size() / 4, hi = t.size() - t.size() / 4;
+        double s = 0;
+        for (size_t i = lo; i < hi; ++i) s += t[i];
+        return s / (double)(hi - lo);
     }
 };
 
