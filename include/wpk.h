@@ -120,6 +120,8 @@ typedef struct {
     int32_t rl_adv_norm;      /* 1 = normalise advantages per update batch (default 1)          */
     int32_t rl_restart_every; /* >0: envs restart from the best-ever config every N updates (1)  */
     int32_t max_seconds;      /* wall-clock cap for one tune (0 = none)                         */
+    int32_t seed_default;     /* 1 (default): the plan's expert default config is one of the first
+                               * candidates (GA individual 0, RL env 0, first random sample)      */
     const char *cache_dir;    /* if set: tuning-result cache. One JSON file per key =
                                * operator identity (shapes, filter, stride, padding;
                                * plus dilation, groups, dtype, layout, epilogue) + family + device.

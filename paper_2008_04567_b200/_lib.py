@@ -66,6 +66,7 @@ class TuneOptions(ctypes.Structure):
         ("rl_adv_norm", ctypes.c_int32),
         ("rl_restart_every", ctypes.c_int32),
         ("max_seconds", ctypes.c_int32),
+        ("seed_default", ctypes.c_int32),
         ("cache_dir", ctypes.c_char_p),
     ]
 

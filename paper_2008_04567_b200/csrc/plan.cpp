@@ -261,9 +261,14 @@ Config default_config(const ConvDesc &d, int family) {
     c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c < 16) ? 1 : 0;
     c.genes[5] = 2; c.genes[6] = 128;
     if (big) { c.genes[3] = 2; c.genes[6] = 256; }
-    for (int st = 8; st >= 2; --st) {
-        c.genes[1] = st;
-        if (config_valid(d, c, nullptr)) break;
+    for (int am : {c.genes[4], 2, 0}) {   // small C: explicit im2col, else the gather producer
+        c.genes[4] = am;
+        bool ok = false;
+        for (int st = 8; st >= 2 && !ok; --st) {
+            c.genes[1] = st;
+            ok = config_valid(d, c, nullptr);
+        }
+        if (ok) break;
     }
     // Split-K is left to the tuner: its fixup re-reads fp32 partials and is only a win for
     // very deep, very narrow layers.
@@ -300,6 +305,7 @@ void wpk_tune_options_init(wpk_tune_options *o) {
     o->rl_alpha_mode = 0;
     o->rl_adv_norm = 1;
     o->rl_restart_every = 1;
+    o->seed_default = 1;
 }
 
 wpk_status wpk_conv2d_output_dims(const wpk_conv2d_shape *shape, int32_t *p, int32_t *q) {

@@ -239,6 +239,7 @@ wpk_status rl_search(TuneCtx &t) {
     Rng r0(o.seed, 0);
     for (int e = 0; e < E; ++e)
         if (!sample_valid(t, r0, &cur[e])) return fail(WPK_ERR_EXHAUSTED, "RL: no valid initial config");
+    if (o.seed_default && t.has_default) cur[0] = t.default_cfg;   // env 0 starts from the expert default
     t.measure_batch(cur);
     if (t.err != WPK_OK) return t.err;
     std::vector<double> alpha(E, 0.0);

@@ -314,6 +314,9 @@ static wpk_status ga_search(TuneCtx &t) {
         if (!sample_valid(t, rng, &c)) return fail(WPK_ERR_EXHAUSTED, "GA Step1: no valid config sampled");
         pop.push_back(c);
     }
+    // The expert template default replaces the first random individual, so a search
+    // never returns something slower than the untuned plan (opt-out: seed_default = 0).
+    if (o.seed_default && t.has_default) pop[0] = t.default_cfg;
     for (int gen = 0;; ++gen) {
         t.measure_batch(pop);                                 // Step2 (memoised, sharded)
         if (t.err != WPK_OK) return t.err;
@@ -390,6 +393,7 @@ static wpk_status ga_search(TuneCtx &t) {
 static wpk_status random_search(TuneCtx &t) {
     Rng rng(t.o.seed, 0);
     long long draws = 0;
+    if (t.o.seed_default && t.has_default) t.measure_batch({t.default_cfg});
     const long long limit = 100LL * std::max(t.budget, 1);
     const int batch = std::max(1, t.o.ga_pop);
     while (!t.exhausted() && draws < limit && !t.time_up()) {
@@ -482,6 +486,11 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
     if (!family_applicable(p->d, t.family, &why)) return fail(WPK_ERR_INVALID_ARGUMENT, "family not applicable: " + why);
     t.sp = &family_space(t.family);
     t.budget = budget;
+    {
+        Config dc = default_config(p->d, t.family);
+        t.has_default = (dc.family == t.family) && config_valid(p->d, dc, nullptr);
+        t.default_cfg = dc;
+    }
     t.t_start = wall_seconds();
     std::string cpath;
     if (t.o.cache_dir && t.o.cache_dir[0]) {

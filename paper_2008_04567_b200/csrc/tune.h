@@ -32,6 +32,8 @@ struct TuneCtx {
     Config best;
     double best_beta = 1e300;
     int rounds = 0;
+    bool has_default = false;
+    Config default_cfg;
 
     bool exhausted() const { return (int)order.size() >= budget; }
     bool valid(const Config &c) const { return config_valid(plan->d, c, nullptr); }

@@ -61,6 +61,7 @@ def _plan():
 
 def _run_cpp(search, budget, seed, replay, log, **kw):
     plan = _plan()
+    kw.setdefault("seed_default", 0)   # the oracle knows nothing of the plan's default config
     res = plan.tune(search, budget, seed=seed, eval_mode="replay", replay_path=replay, log_path=log,
                     family="simt", **kw)
     return plan, res
@@ -106,7 +107,7 @@ def _worker(rank, world, port, path, budget, search, out):
     plan = Conv2dPlan(**SHAPE, layout="nchw", dtype="f32", device=0)
     log = out + f".log{rank}"
     res = plan.tune(search, budget, seed=4, eval_mode="replay", replay_path=path, log_path=log, family="simt",
-                    rank=rank, world=world, **wdist.make_exchange())
+                    rank=rank, world=world, seed_default=0, **wdist.make_exchange())
     with open(out + f".{rank}", "w") as f:
         json.dump({"genes": res.genes, "best": res.best_us, "measured": res.measured}, f)
     dist.barrier()
