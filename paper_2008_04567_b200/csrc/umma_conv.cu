@@ -93,14 +93,20 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx<T> &E, const CUtensorMap *t
                                               int split, bool final_out) {
     const UmmaArgs &a = *E.a;
     uint32_t pk[32];
+    // all TMEM loads of the 128-byte chunk in flight at once, one wait
+    uint32_t raw[64];
+    const int nsub = (final_out && sizeof(T) == 2) ? 4 : 2;
+#pragma unroll
+    for (int sub = 0; sub < 4; ++sub)
+        if (sub < nsub) ptx::tmem_ld16_nowait(taddr + sub * 16, raw + sub * 16);
+    ptx::tmem_wait_ld();
     if (final_out && sizeof(T) == 2) {
 #pragma unroll
         for (int sub = 0; sub < 4; ++sub) {
             float v[16];
-            ptx::tmem_ld16(taddr + sub * 16, v);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                v[j] += E.sBias[min(k0 + sub * 16 + j, a.K - 1)];
+                v[j] = __uint_as_float(raw[sub * 16 + j]) + E.sBias[min(k0 + sub * 16 + j, a.K - 1)];
                 if (a.epilogue == 2) v[j] = fmaxf(v[j], 0.f);
             }
 #pragma unroll
@@ -108,17 +114,13 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx<T> &E, const CUtensorMap *t
         }
     } else {
 #pragma unroll
-        for (int sub = 0; sub < 2; ++sub) {
-            float v[16];
-            ptx::tmem_ld16(taddr + sub * 16, v);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                if (final_out) {
-                    v[j] += E.sBias[min(k0 + sub * 16 + j, a.K - 1)];
-                    if (a.epilogue == 2) v[j] = fmaxf(v[j], 0.f);
-                }
-                pk[sub * 16 + j] = __float_as_uint(v[j]);
+        for (int j = 0; j < 32; ++j) {
+            float v = __uint_as_float(raw[j]);
+            if (final_out) {
+                v += E.sBias[min(k0 + j, a.K - 1)];
+                if (a.epilogue == 2) v = fmaxf(v, 0.f);
             }
+            pk[j] = __float_as_uint(v);
         }
     }
     // staging buffer reuse: the TMA store issued two chunks ago must have finished reading it
