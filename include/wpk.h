@@ -101,7 +101,8 @@ typedef struct {
     int32_t rank, world;      /* this process's rank and the number of ranks (default 0, 1)    */
     wpk_exchange_fn exchange; /* required when world > 1                                        */
     void *exchange_ctx;
-    int32_t warmup, reps;     /* timing protocol: W untimed + R event-timed reps, median (3, 11) */
+    int32_t warmup, reps;     /* timing protocol: W untimed + R reps (1..1024) bracketed by device
+                                 globaltimer stamps, interquartile mean (defaults 3, 11) */
     int32_t l2_flush;         /* 1: overwrite a >= 2x L2 buffer before every timed rep (default) */
     int32_t eval_mode;        /* wpk_eval_mode (default MEASURED)                               */
     int32_t family;           /* wpk_family to search; WPK_FAMILY_AUTO = the plan's default      */

@@ -71,7 +71,7 @@ static Space make_space(int family) {
         sp.names = {"T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"};
     } else if (family == WPK_FAMILY_UMMA) {
         sp.dom = {{16, 32, 64, 96, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8}, {1, 2, 4, 8, 16},
-                  {0, 1, 2, 3}, {0, 1, 2}, {1, 2}, {128, 256}};
+                  {0, 1, 2, 3}, {0, 1, 2, 3}, {1, 2, 4}, {128, 256}};
         sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "MODE", "A_MODE", "ACC_STAGES", "BLOCK_M"};
     } else {
         sp.dom = {{1, 2, 4, 8}, {1, 2, 4}, {64, 128, 256, 512}, {1}, {0}, {0}, {0}};
@@ -132,9 +132,23 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->ctas_per_sm = 1;
     g->a_mode = cfg.genes[4];
     g->acc_stages = cfg.genes[5];
+    g->seg_sp = 0;
     if ((g->a_mode == 1 || g->a_mode == 2) && d.c >= 64)
         return no("A_MODE 1/2 (explicit im2col / gather) is reserved for layers with C < 64");
-    if (g->a_mode == 1 || g->a_mode == 2) {
+    if (g->a_mode == 3) {
+        // pixel-segment gather (C <= 4): activations stored NHWC with 4 channels per pixel (8 or 16
+        // bytes); K row = (r, s', c) with s' padded to Sp so that one 16-byte smem chunk holds whole
+        // pixels of a single filter row; weights for s' >= S and c >= C are zero.
+        if (d.c > 4) return no("A_MODE 3 (pixel-segment gather) needs C <= 4");
+        if (d.r > 30 || d.s > 30) return no("A_MODE 3 needs R, S <= 30 (validity bitmasks)");
+        if (g->stages < 3) return no("A_MODE 3 keeps two stages of copies in flight: STAGES >= 3");
+        if ((double)d.n * d.h * d.w * 4 >= 2147483647.0) return no("segment gather needs < 2^31 input elements");
+        const int ppc = 16 / (4 * e);                         // pixels per 16-byte chunk: 2 (16-bit), 1 (tf32)
+        g->seg_sp = round_up(d.s, ppc);
+        g->cpad = d.r * g->seg_sp * 4;
+        g->c_blocks = (g->cpad + g->bk - 1) / g->bk;
+        g->num_kb = g->c_blocks;
+    } else if (g->a_mode == 1 || g->a_mode == 2) {
         // explicit im2col (1: A = [M][R*S*C] materialised in the workspace, then a plain GEMM) or the
         // fused gather producer (2: the same K order built directly in shared memory)
         g->cpad = round_up(d.r * d.s * d.c, 8);   // 8-element vectors in the im2col kernel
@@ -154,10 +168,10 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->m_tiles = (int)((d.M() + g->bm - 1) / g->bm);
     g->n_tiles = (d.k + g->bn - 1) / g->bn;
     g->work = (long long)g->m_tiles * g->n_tiles * g->splits;
+    if (g->work >= 2147483647LL / 2) return no("too many work items (tiles x splits >= 2^30)");
     if (g->pair) {
         if (g->bm != 256) return no("a CTA pair computes 256-row tiles (BLOCK_M must be 256)");
-        if (g->splits != 1) return no("CTA pairs do not support split-K");
-        if (g->a_mode == 2) return no("CTA pairs do not support the gather producer");
+        if (g->a_mode >= 2) return no("CTA pairs do not support the gather producers");
     }
     size_t stage = g->pair ? (size_t)128 * 128 + (size_t)(g->bn / 2) * 128 : (size_t)g->bm * 128 + (size_t)g->bn * 128;
     if (g->bm == 256 && g->a_mode == 0 && !(d.r == 1 && d.s == 1 && d.sh == 1 && d.sw == 1 && d.ph == 0 && d.pw == 0))
@@ -166,19 +180,21 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->a_tiled = (g->a_mode == 1 || (d.r == 1 && d.s == 1 && d.sh == 1 && d.sw == 1 && d.ph == 0 && d.pw == 0 &&
                                       g->cpad == d.c && !getenv("WPK_A_IM2COL"))) ? 1 : 0;
     // epilogue through shared memory + TMA store: NHWC output, whole 128-byte column chunks
-    const int out_elem = (g->splits > 1) ? 4 : e;
-    const int cw = 128 / out_elem;
-    g->epi_tma = (d.layout == WPK_NHWC && g->bn % cw == 0 && ((long long)d.k * out_elem) % 16 == 0 &&
+    // (split-K: the owner split stores the output the same way; the others store fp32 partials in
+    // 32-column chunks, which always divide a 128-byte output chunk)
+    const int cw = 128 / e;
+    g->epi_tma = (d.layout == WPK_NHWC && g->bn % cw == 0 && ((long long)d.k * e) % 16 == 0 &&
                   !getenv("WPK_EPI_DIRECT")) ? 1 : 0;
     const size_t smem_cap = 227 * 1024;
-    const size_t fixed = 1024 /*align slack*/ + ((size_t)d.k * 4 + 15) / 16 * 16 /*bias*/ + 256 /*barriers*/;
+    const size_t bias_bytes = (size_t)round_up(d.k, 256) * 4;   // fp32, zero-padded past K
+    const size_t fixed = 1024 /*align slack*/ + bias_bytes + 256 /*barriers*/;
     // 8 epilogue warps x {2, else 1} staging buffers x 32 rows x 128 B
     g->epi_bufs = (g->epi_tma && (size_t)g->stages * stage + 8 * 2 * 4096 + fixed <= smem_cap) ? 2 : 1;
     size_t off = (size_t)g->stages * stage;
     g->epi_off = off;
     if (g->epi_tma) off += (size_t)8 * g->epi_bufs * 4096;
     g->bias_off = off;
-    off += ((size_t)d.k * 4 + 15) / 16 * 16;
+    off += bias_bytes;
     g->bar_off = off;
     off += 256;
     g->smem_bytes = 1024 /*align slack*/ + off;
@@ -258,7 +274,7 @@ Config default_config(const ConvDesc &d, int family) {
     if (bn == 256 && mt * ((d.k + 255) / 256) < 120) bn = 128;
     // large layers: a tcgen05 CTA pair (256 x BLOCK_N over two SMs) halves B traffic per SM
     const bool big = ((d.M() + 255) / 256) * ((d.k + bn - 1) / bn) >= 2 * 148 && bn >= 128 && d.c >= 64;
-    c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c < 16) ? 1 : 0;
+    c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c <= 4) ? 3 : (d.c < 16) ? 1 : 0;
     c.genes[5] = 2; c.genes[6] = 128;
     if (big) { c.genes[3] = 2; c.genes[6] = 256; }
     for (int am : {c.genes[4], 2, 0}) {   // small C: explicit im2col, else the gather producer

@@ -119,6 +119,23 @@ __global__ void pack_flat_kernel(const T *__restrict__ w, T *__restrict__ out, i
         out[i] = v;
     }
 }
+// Weights for the pixel-segment gather (A_MODE 3): out[k][(r*Sp + s)*4 + c], zero for s >= S, c >= C
+// and beyond R*Sp*4 (up to kgp).
+template <typename T>
+__global__ void pack_seg_kernel(const T *__restrict__ w, T *__restrict__ out, int K, int C, int R, int S, int Sp,
+                                int kgp, int src_kcrs) {
+    const long long total = (long long)K * kgp;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int kg = (int)(i % kgp);
+        const int k = (int)(i / kgp);
+        const int c = kg & 3, rs = kg >> 2, r = rs / Sp, s = rs % Sp;
+        T v = T(0.f);
+        if (r < R && s < S && c < C)
+            v = src_kcrs ? w[(((long long)k * C + c) * R + r) * S + s] : w[(((long long)k * R + r) * S + s) * C + c];
+        out[i] = v;
+    }
+}
 // Depthwise weights [C][R][S] (both layouts, C/g = 1) -> [R][S][C].
 template <typename T>
 __global__ void pack_rsc_kernel(const T *__restrict__ w, T *__restrict__ out, int C, int R, int S) {
@@ -140,8 +157,12 @@ static unsigned grid_for(long long total, int sm) {
 }
 
 template <typename T>
-static void launch_aux_t(int which, const void *src, void *dst, const ConvDesc &d, int cp, int sm, cudaStream_t st) {
-    if (which == 0)
+static void launch_aux_t(int which, const void *src, void *dst, const ConvDesc &d, int cp, int sm, cudaStream_t st,
+                         int sp) {
+    if (which == 6)
+        pack_seg_kernel<T><<<grid_for((long long)d.k * cp, sm), 256, 0, st>>>((const T *)src, (T *)dst, d.k, d.c, d.r,
+                                                                              d.s, sp, cp, d.layout == WPK_NCHW);
+    else if (which == 0)
         nchw_to_nhwc_pad_kernel<T><<<grid_for((long long)d.n * d.h * d.w * cp, sm), 256, 0, st>>>(
             (const T *)src, (T *)dst, d.n, d.c, d.h, d.w, cp);
     else if (which == 1)
@@ -162,10 +183,11 @@ static void launch_aux_t(int which, const void *src, void *dst, const ConvDesc &
                                                                                      d.r, d.s);
 }
 
-static void launch_aux(int which, const void *src, void *dst, const ConvDesc &d, int cp, int sm, cudaStream_t st) {
-    if (d.dtype == WPK_BF16) launch_aux_t<__nv_bfloat16>(which, src, dst, d, cp, sm, st);
-    else if (d.dtype == WPK_F16) launch_aux_t<__half>(which, src, dst, d, cp, sm, st);
-    else launch_aux_t<float>(which, src, dst, d, cp, sm, st);
+static void launch_aux(int which, const void *src, void *dst, const ConvDesc &d, int cp, int sm, cudaStream_t st,
+                       int sp = 0) {
+    if (d.dtype == WPK_BF16) launch_aux_t<__nv_bfloat16>(which, src, dst, d, cp, sm, st, sp);
+    else if (d.dtype == WPK_F16) launch_aux_t<__half>(which, src, dst, d, cp, sm, st, sp);
+    else launch_aux_t<float>(which, src, dst, d, cp, sm, st, sp);
 }
 
 // Deterministic pseudo-random fill in [-1, 1) (tuning buffers; values do not affect timing much).
@@ -198,6 +220,17 @@ __global__ void l2_flush_read_kernel(const uint4 *__restrict__ p, size_t n16, un
         acc ^= v.x ^ v.y ^ v.z ^ v.w;
     }
     if (acc == 0x9E3779B9u) *sink = acc;   // practically never; keeps the loads alive
+}
+
+// Device timestamp (globaltimer, ns; 256-ns steps on this part vs ~2-us CUDA-event steps) for the
+// tuner's candidate timing.
+__global__ void timestamp_kernel(unsigned long long *dst) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *dst = t;
+}
+void timestamp_device(unsigned long long *dst, void *stream) {
+    timestamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dst);
 }
 
 void l2_flush_device(const void *buf, size_t bytes, void *sink, void *stream) {
@@ -251,13 +284,18 @@ static WsLayout ws_layout(const ConvDesc &d, const Config &cfg, bool host_stagin
             L.w_off = off; L.w_bytes = al256((size_t)d.k * g.cpad * e); off += L.w_bytes;
         } else if (g.a_mode == 2) {
             L.w_off = off; L.w_bytes = al256((size_t)d.k * g.cpad * e); off += L.w_bytes;
+        } else if (g.a_mode == 3) {
+            if (d.layout == WPK_NCHW || d.c != 4) {
+                L.x_off = off; L.x_bytes = al256((size_t)d.n * d.h * d.w * 4 * e); off += L.x_bytes;
+            }
+            L.w_off = off; L.w_bytes = al256((size_t)d.k * g.cpad * e); off += L.w_bytes;
         } else if (d.layout == WPK_NCHW || g.cpad != d.c) {
             L.x_off = off; L.x_bytes = al256((size_t)d.n * d.h * d.w * g.cpad * e); off += L.x_bytes;
             L.w_off = off; L.w_bytes = al256((size_t)d.k * d.r * d.s * g.cpad * e); off += L.w_bytes;
         }
         if (g.splits > 1) {
             L.p_off = off; L.p_bytes = al256((size_t)g.splits * d.M() * d.k * 4); off += L.p_bytes;
-            L.c_off = off; L.c_bytes = al256((size_t)g.m_tiles * g.n_tiles * 4); off += L.c_bytes;
+            L.c_off = off; L.c_bytes = al256((size_t)g.m_tiles * g.n_tiles * (g.pair ? 2 : 1) * 4); off += L.c_bytes;
         }
     } else if (cfg.family == WPK_FAMILY_DW) {
         L.w_off = off; L.w_bytes = al256((size_t)d.c * d.r * d.s * e); off += L.w_bytes;
@@ -349,7 +387,20 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     if (!umma_geometry(d, cfg, &g, &why)) { set_error("invalid UMMA config: " + why); return -1; }
     const void *xk = x, *wk = w;
     const int pack_kind = WPK_FAMILY_UMMA * 10 + g.a_mode;
-    if (g.a_mode == 1 || g.a_mode == 2) {
+    if (g.a_mode == 3) {
+        if (d.layout == WPK_NCHW || d.c != 4) {   // activations -> NHWC, 4 channels per pixel
+            launch_aux(d.layout == WPK_NCHW ? 0 : 1, x, ws + L.x_off, d, 4, sm, st);
+            ++launches;
+            xk = ws + L.x_off;
+        }
+        if (p.packed_for != w || p.packed_cfg_family != pack_kind) {
+            launch_aux(6, w, ws + L.w_off, d, g.cpad, sm, st, g.seg_sp);
+            ++launches;
+            p.packed_for = w;
+            p.packed_cfg_family = pack_kind;
+        }
+        wk = ws + L.w_off;
+    } else if (g.a_mode == 1 || g.a_mode == 2) {
         if (g.a_mode == 1) {
             launch_aux(4, x, ws + L.x_off, d, g.cpad, sm, st);
             ++launches;
@@ -403,8 +454,8 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     U.epilogue = d.epilogue; U.out_nchw = d.layout == WPK_NCHW; U.sm_count = sm; U.stream = stream; U.g = g;
     U.a_rows = (g.a_mode == 1) ? d.M() : (long long)d.n * d.h * d.w;
     U.b_rs = (g.a_mode >= 1) ? 1 : d.r * d.s;
-    U.C = d.c;
-    U.x_nchw = (d.layout == WPK_NCHW);
+    U.C = (g.a_mode == 3) ? 4 : d.c;                          // channels per stored pixel
+    U.x_nchw = (g.a_mode == 3) ? 0 : (d.layout == WPK_NCHW);
     U.dbg = g_debug_timeline;
     if (!p.map_cache) p.map_cache = new UmmaMapCache();
     U.cache = static_cast<UmmaMapCache *>(p.map_cache);

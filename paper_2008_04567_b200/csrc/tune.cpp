@@ -27,6 +27,7 @@
 namespace wpk {
 
 void fill_random_device(void *p, size_t n, int dtype, uint64_t seed, void *stream);   // run.cu
+void timestamp_device(unsigned long long *dst, void *stream);                          // run.cu
 void l2_flush_device(const void *buf, size_t bytes, void *sink, void *stream);          // run.cu
 
 double wall_seconds() {
@@ -57,11 +58,12 @@ void log_line(TuneCtx &t, const std::string &s) {
 }
 
 // ---------------------------------------------------------------------------------------------------
-// measured evaluator (W warm-ups + R event-timed reps, median; L2 flushed before each rep)
+// measured evaluator (W warm-ups + R device-timestamped reps, interquartile mean; L2 flushed before each rep)
 // ---------------------------------------------------------------------------------------------------
 struct GpuBench {
     cudaStream_t st = nullptr;
     void *x = nullptr, *w = nullptr, *b = nullptr, *y = nullptr, *ws = nullptr, *flush = nullptr;
+    unsigned long long *stamps = nullptr;   // [2 * reps] device timestamps
     size_t ws_bytes = 0, flush_bytes = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     bool ok = false;
@@ -83,6 +85,7 @@ struct GpuBench {
         if (cudaMalloc(&flush, flush_bytes + 256)) return fail_("cudaMalloc of the L2 flush buffer");
         cudaMemsetAsync(flush, 1, flush_bytes + 256, st);
         if (cudaEventCreate(&e0) || cudaEventCreate(&e1)) return fail_("events");
+        if (cudaMalloc(&stamps, 2 * 1024 * sizeof(unsigned long long))) return fail_("cudaMalloc of timestamps");
         if (cudaStreamSynchronize(st)) return fail_("init sync");
         ok = true;
         return true;
@@ -93,7 +96,7 @@ struct GpuBench {
         return false;
     }
     ~GpuBench() {
-        for (void *ptr : {x, w, b, y, ws, flush})
+        for (void *ptr : {x, w, b, y, ws, flush, (void *)stamps})
             if (ptr) cudaFree(ptr);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
@@ -123,20 +126,24 @@ struct GpuBench {
         for (int i = 0; i < warmup; ++i)
             if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes) < 0) return INFINITY;
         if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
+        // Each rep is bracketed by two 1-thread kernels that write %globaltimer (256-ns steps; CUDA
+        // events on this part advance in ~2-us steps, too coarse for 5-30 us layers). The constant
+        // launch latency of the closing stamp is the same for every candidate of a layer.
         std::vector<float> t;
+        std::vector<unsigned long long> hs(2 * (size_t)reps);
         for (int i = 0; i < reps; ++i) {
             if (l2flush) l2_flush_device(flush, flush_bytes, (char *)flush + flush_bytes, st);
-            cudaEventRecord(e0, st);
+            timestamp_device(stamps + 2 * i, st);
             if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes) < 0) return INFINITY;
-            cudaEventRecord(e1, st);
+            timestamp_device(stamps + 2 * i + 1, st);
             if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
-            float ms = 0;
-            cudaEventElapsedTime(&ms, e0, e1);
-            t.push_back(ms * 1000.f);
         }
-        // Event timestamps on this part advance in ~2 us steps, so a median of quantised samples is
-        // itself quantised; the mean of the middle half keeps the median's robustness to outliers
-        // while resolving differences below one timer step (launch jitter dithers the samples).
+        if (cudaMemcpy(hs.data(), stamps, hs.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            *fatal = true;
+            return INFINITY;
+        }
+        for (int i = 0; i < reps; ++i) t.push_back((float)((double)(hs[2 * i + 1] - hs[2 * i]) * 1e-3));
+        // mean of the middle half: the median's robustness to outliers, finer than one timer step
         std::sort(t.begin(), t.end());
         const size_t lo = t.size() / 4, hi = t.size() - t.size() / 4;
         double s = 0;
@@ -480,7 +487,7 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
     }
     if (t.o.world < 1 || t.o.rank < 0 || t.o.rank >= t.o.world) return fail(WPK_ERR_INVALID_ARGUMENT, "bad rank/world");
     if (t.o.world > 1 && !t.o.exchange) return fail(WPK_ERR_INVALID_ARGUMENT, "world > 1 needs an exchange callback");
-    if (t.o.reps < 1 || t.o.warmup < 0) return fail(WPK_ERR_INVALID_ARGUMENT, "bad timing protocol");
+    if (t.o.reps < 1 || t.o.reps > 1024 || t.o.warmup < 0) return fail(WPK_ERR_INVALID_ARGUMENT, "bad timing protocol");
     t.family = (t.o.family == WPK_FAMILY_AUTO) ? default_family(p->d) : t.o.family;
     std::string why;
     if (!family_applicable(p->d, t.family, &why)) return fail(WPK_ERR_INVALID_ARGUMENT, "family not applicable: " + why);

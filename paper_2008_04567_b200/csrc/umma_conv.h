@@ -4,10 +4,19 @@
 #include <string>
 
 #include <cuda.h>
+#include <cuda_runtime.h>
 
 #include "wpk_internal.h"
 
 namespace wpk {
+
+enum { DT_F16 = 0, DT_BF16 = 1, DT_TF32 = 2 };
+// A producer kinds: TMA (im2col / tiled), TMA for a CTA pair, element gather (A_MODE 2),
+// pixel-segment gather (A_MODE 3)
+enum { AK_TMA = 0, AK_PAIR = 1, AK_GATHER = 2, AK_SEG = 3 };
+// epilogue kinds: final output via TMA store, split-K partials via TMA store (+ in-kernel fixup),
+// direct global stores (NCHW output or K not a multiple of the 128-byte chunk; final or partial)
+enum { EK_TMA = 0, EK_SPLIT = 1, EK_DIRECT = 2 };
 
 struct UmmaArgs {
     const void *bias;
@@ -27,6 +36,9 @@ struct UmmaArgs {
     int *counters;                  // split-K arrival counters, one per output tile (self-resetting)
     const void *x;                  // A_MODE 2 gather source (the caller's activations)
     int x_nchw, C, H, W, R;
+    int a_mode, seg_sp;             // A_MODE 3: pixel-segment gather, filter columns padded to seg_sp
+    int kpad_bias;                  // staged bias length (K rounded up to 256, zero-padded)
+    int dbg_flags;                  // experiments only (WPK_DBG_FLAGS): 1 = gather zero-fills, 2 = no y stores
 };
 
 // Tensor maps of the last launch, reused while pointers and config are unchanged (host-side
@@ -36,7 +48,7 @@ struct UmmaMapCache {
     const void *x = nullptr, *w = nullptr;
     void *y = nullptr, *partial = nullptr;
     Config cfg;
-    CUtensorMap a, b, yy;
+    CUtensorMap a, b, yy, pp;
 };
 
 struct UmmaLaunch {
@@ -63,5 +75,13 @@ struct UmmaLaunch {
 
 // Returns the number of kernel launches issued (1 or 2), or -1 with *err set.
 int umma_launch(const UmmaLaunch &L, std::string *err);
+
+// Per-dtype kernel instantiations (umma_conv_{f16,bf16,tf32}.cu): launch variant (ak, ek).
+cudaError_t umma_launch_f16(int ak, int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
+                            const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a);
+cudaError_t umma_launch_bf16(int ak, int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
+                             const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a);
+cudaError_t umma_launch_tf32(int ak, int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
+                             const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a);
 
 }  // namespace wpk

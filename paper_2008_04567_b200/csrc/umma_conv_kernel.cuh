@@ -1,0 +1,858 @@
+// KB1: implicit-GEMM forward convolution on 5th-generation tensor cores (tcgen05 / TMEM / TMA).
+//
+// GEMM view:  D[m, k] = sum_kg A[m, kg] * B[k, kg]
+//   m  = (n, p, q) output pixel (M = N*P*Q),   k = output channel,
+//   kg = (r, s, c) reduction index, c innermost (NHWC activations, KRSC weights).
+//   A[m, (r,s,c)] = x[n, p*sh - ph + r*dh, q*sw - pw + s*dw, c]  (0 outside) -- never materialised:
+//   each K block (one filter tap (r,s) x BK channels) is fetched by ONE TMA im2col load of 128
+//   output pixels x BK channels (the hardware walks the pixels, applies stride, zero-fills padding).
+//   B[k, (r,s,c)] = w[k, r, s, c]: TMA tiled load of BLOCK_N x BK from the [K][R*S][C] weights.
+// Both operands land in shared memory in the canonical K-major 128-byte-swizzle layout (BK =
+// 128 bytes of K per stage), consumed by tcgen05.mma (kind::f16 for bf16/fp16, kind::tf32) issued
+// by one thread; the fp32 accumulator lives in TMEM (1, 2 or 4 accumulator stages), so the
+// epilogue of tile i overlaps the main loop of tiles i+1...
+//
+// The kernel is a template over (dtype, A producer kind, epilogue kind) so that each launched
+// variant carries only the code it runs: the warps of one SM sub-partition execute different
+// roles at once, and a kernel image larger than the instruction caches stalls them all
+// ("no instruction" stalls measured with ncu on the first, single-variant version).
+//
+// Warp roles (384 threads, 512 with gather producers): warp 0 = A TMA producer, warp 1 = TMEM
+// allocator + MMA issuer, warp 2 = B TMA producer, warp 3 spare, warps 4-11 = epilogue
+// (tcgen05.ld -> +bias -> ReLU -> round -> swizzled smem -> TMA store), warps 12-15 = gather
+// producers (A_MODE 2/3). Persistent grid: CTAs loop over work items (tile, split) with a static
+// round-robin schedule; RASTER picks which GEMM dimension varies fastest.
+//
+// The fused epilogue realises the paper's operator fusion ("write one CUDA kernel
+// function for the fused operator"; SPEC.md:136 relu(bias_add(conv))).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+#include "umma_conv.h"
+
+namespace wpk {
+
+template <int DT> struct OutT;
+template <> struct OutT<DT_F16> { using T = __half; };
+template <> struct OutT<DT_BF16> { using T = __nv_bfloat16; };
+template <> struct OutT<DT_TF32> { using T = float; };
+
+__device__ __forceinline__ float ld_bias(const __half *b, int k) { return __half2float(b[k]); }
+__device__ __forceinline__ float ld_bias(const __nv_bfloat16 *b, int k) { return __bfloat162float(b[k]); }
+__device__ __forceinline__ float ld_bias(const float *b, int k) { return b[k]; }
+
+__device__ __forceinline__ uint32_t pack2(float a, float b, __half *) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b, __nv_bfloat16 *) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ uint32_t pack2(float, float, float *) { return 0u; }   // unused (fp32 out)
+__device__ __forceinline__ void st_out(__half *p, float v) { *p = __float2half_rn(v); }
+__device__ __forceinline__ void st_out(__nv_bfloat16 *p, float v) { *p = __float2bfloat16_rn(v); }
+__device__ __forceinline__ void st_out(float *p, float v) { *p = v; }
+
+struct WorkPos {
+    int mt, nt, split;
+};
+__device__ __forceinline__ WorkPos decode_work(long long w, const UmmaArgs &a) {
+    WorkPos r;
+    const int wi = (int)w;   // work counts are < 2^31 (plan validation)
+    r.split = wi % a.splits;
+    const int t = wi / a.splits;
+    if (a.raster == 0) {
+        r.mt = t / a.n_tiles;
+        r.nt = t - r.mt * a.n_tiles;
+    } else {
+        r.nt = t / a.m_tiles;
+        r.mt = t - r.nt * a.m_tiles;
+    }
+    return r;
+}
+
+// bias + ReLU for 4 consecutive columns (bias staged in smem as fp32, zero-padded past K)
+__device__ __forceinline__ void bias_relu4(float *v, const float *sBias, int k, bool relu) {
+    const float4 b = *reinterpret_cast<const float4 *>(sBias + k);
+    v[0] += b.x; v[1] += b.y; v[2] += b.z; v[3] += b.w;
+    if (relu) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = fmaxf(v[j], 0.f);
+    }
+}
+
+// Epilogue state of one warp: its staging buffers (2 x 4 KB = 32 rows x 128 B, or 1).
+struct EpiCtx {
+    const float *sBias;
+    uint8_t *sEpi;
+    uint32_t ebuf;
+    int lane;
+    int nbufs;
+};
+
+// 32 rows x 128 bytes (packed in pk, one row per lane) -> 128-byte-swizzled smem staging buffer ->
+// TMA store: FINAL into the output [M][K], else into the fp32 partials [split][M][K].
+template <bool FINAL>
+__device__ __forceinline__ void stage_and_store(EpiCtx &E, const UmmaArgs &a, const CUtensorMap *tmY, const uint32_t *pk,
+                                                int k0, int mrow, int split) {
+    // staging buffer reuse: the TMA store issued two chunks ago must have finished reading it
+    if (E.lane == 0) {
+        if (E.nbufs == 2) ptx::bulk_wait_read<1>();
+        else ptx::bulk_wait_read<0>();
+    }
+    __syncwarp();
+    uint8_t *bufp = E.sEpi + E.ebuf * 4096;
+    const uint32_t buf = ptx::smem_u32(bufp) + (uint32_t)E.lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        ptx::st_shared_v4(buf + ((uint32_t)(j ^ (E.lane & 7)) << 4), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (E.lane == 0 && !(a.dbg_flags & 2)) {
+        if constexpr (FINAL) ptx::tma_store_2d(tmY, bufp, k0, mrow);
+        else ptx::tma_store_3d(tmY, bufp, k0, mrow, split);
+        ptx::bulk_commit();
+    }
+    if (E.nbufs == 2) E.ebuf ^= 1;
+}
+
+// One 32-row x 128-byte chunk through smem + TMA store. FINAL: +bias, ReLU, RN-round to T (64
+// columns for 16-bit T, 32 for fp32); else fp32 split-K partials (32 columns) into [split][M][K].
+template <typename T, bool FINAL>
+__device__ __forceinline__ void epi_chunk_tma(EpiCtx &E, const UmmaArgs &a, const CUtensorMap *tmY, uint32_t taddr,
+                                              int k0, int mrow, int split) {
+    constexpr bool k16 = FINAL && sizeof(T) == 2;
+    uint32_t raw[k16 ? 64 : 32];
+    ptx::tmem_ld32_nowait(taddr, raw);
+    if constexpr (k16) ptx::tmem_ld32_nowait(taddr + 32, raw + 32);
+    ptx::tmem_wait_ld();
+    uint32_t pk[32];
+    if constexpr (k16) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            float v[4] = {__uint_as_float(raw[4 * q]), __uint_as_float(raw[4 * q + 1]), __uint_as_float(raw[4 * q + 2]),
+                          __uint_as_float(raw[4 * q + 3])};
+            bias_relu4(v, E.sBias, k0 + 4 * q, a.epilogue == 2);
+            pk[2 * q] = pack2(v[0], v[1], (T *)nullptr);
+            pk[2 * q + 1] = pack2(v[2], v[3], (T *)nullptr);
+        }
+    } else if constexpr (FINAL) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            float v[4] = {__uint_as_float(raw[4 * q]), __uint_as_float(raw[4 * q + 1]), __uint_as_float(raw[4 * q + 2]),
+                          __uint_as_float(raw[4 * q + 3])};
+            bias_relu4(v, E.sBias, k0 + 4 * q, a.epilogue == 2);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pk[4 * q + j] = __float_as_uint(v[j]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pk[j] = raw[j];
+    }
+    stage_and_store<FINAL>(E, a, tmY, pk, k0, mrow, split);
+}
+
+// Split-K owner chunk (the last split of a tile): sums the other splits' fp32 partials (read from
+// L2) and its own accumulator (TMEM) in the fixed split order 0..S-1, then +bias, ReLU, one RN
+// rounding and the TMA store of the final output. 32 columns at a time.
+template <typename T>
+__device__ __forceinline__ void epi_chunk_owner(EpiCtx &E, const UmmaArgs &a, const CUtensorMap *tmY, uint32_t taddr,
+                                                int k0, int mrow) {
+    constexpr int CW = 128 / sizeof(T);          // columns per 128-byte output chunk (64 or 32)
+    const long long m = (long long)mrow + E.lane;
+    const bool mok = m < a.M;
+    const long long MK = a.M * (long long)a.K;
+    const float *prow = a.partial + m * a.K;
+    const int nprev = a.splits - 1;
+    uint32_t pk[32];
+#pragma unroll
+    for (int half = 0; half < CW / 32; ++half) {
+        const int kh = k0 + half * 32;
+        uint32_t raw[32];
+        ptx::tmem_ld32_nowait(taddr + half * 32, raw);
+        float acc[32];
+        for (int sp = 0; sp < nprev; ++sp) {
+            float4 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                v[q] = (mok && kh + 4 * q < a.K) ? __ldcg(reinterpret_cast<const float4 *>(prow + sp * MK + kh + 4 * q))
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (sp == 0) {
+                    acc[4 * q] = v[q].x; acc[4 * q + 1] = v[q].y; acc[4 * q + 2] = v[q].z; acc[4 * q + 3] = v[q].w;
+                } else {
+                    acc[4 * q] += v[q].x; acc[4 * q + 1] += v[q].y; acc[4 * q + 2] += v[q].z; acc[4 * q + 3] += v[q].w;
+                }
+            }
+        }
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            float v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = acc[4 * q + j] + __uint_as_float(raw[4 * q + j]);
+            bias_relu4(v, E.sBias, kh + 4 * q, a.epilogue == 2);
+            if constexpr (sizeof(T) == 2) {
+                pk[half * 16 + 2 * q] = pack2(v[0], v[1], (T *)nullptr);
+                pk[half * 16 + 2 * q + 1] = pack2(v[2], v[3], (T *)nullptr);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) pk[4 * q + j] = __float_as_uint(v[j]);
+            }
+        }
+    }
+    stage_and_store<true>(E, a, tmY, pk, k0, mrow, 0);
+}
+
+// Direct-store epilogue for one 32-row x 16-column chunk (NCHW output, unaligned K, partials).
+template <typename T>
+__device__ __noinline__ void epi_chunk_direct(const UmmaArgs &a, const float *sBias, uint32_t taddr, int k0,
+                                              long long m, int split, bool final_out) {
+    float v[16];
+    ptx::tmem_ld16(taddr, v);
+    if (m >= a.M) return;
+    const bool full16 = (k0 + 16 <= a.K);
+    if (!final_out) {
+        float *dst = a.partial + ((long long)split * a.M + m) * a.K + k0;
+        if (full16 && a.vec_ok) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+                *reinterpret_cast<float4 *>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+            for (int j = 0; j < 16; ++j)
+                if (k0 + j < a.K) dst[j] = v[j];
+        }
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bias_relu4(v + 4 * q, sBias, k0 + 4 * q, a.epilogue == 2);
+    T *y = static_cast<T *>(a.y);
+    if (a.out_nchw) {
+        const long long nimg = m / a.PQ;
+        const long long base = nimg * (long long)a.K * a.PQ + (m - nimg * a.PQ);
+        for (int j = 0; j < 16; ++j)
+            if (k0 + j < a.K) st_out(y + base + (long long)(k0 + j) * a.PQ, v[j]);
+        return;
+    }
+    T *dst = y + m * a.K + k0;
+    if (full16 && a.vec_ok) {
+        if constexpr (sizeof(T) == 2) {
+            uint32_t u[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) u[j] = pack2(v[2 * j], v[2 * j + 1], (T *)nullptr);
+            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(u[0], u[1], u[2], u[3]);
+            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(u[4], u[5], u[6], u[7]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+                *reinterpret_cast<float4 *>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+    } else {
+        for (int j = 0; j < 16; ++j)
+            if (k0 + j < a.K) st_out(dst + j, v[j]);
+    }
+}
+
+// In-kernel split-K fixup ("serial reduction by the last arriving split"): every split publishes its
+// fp32 partial tile, bumps the tile's counter; the CTA that completes the count sums all partials
+// in the fixed split order 0..S-1 (deterministic, independent of arrival order), applies bias+ReLU,
+// rounds once and stores the output, then resets the counter for the next launch. For a CTA pair
+// each CTA owns its 128 rows of the 256-row tile and has its own counter.
+template <typename T>
+__device__ __noinline__ void splitk_fixup(const UmmaArgs &a, const float *sBias, volatile int *sFlag, const WorkPos &wp,
+                                          int nsub, int warp, int lane, uint32_t crank, int pair) {
+    if (a.epi_tma && lane == 0) ptx::bulk_wait_all();   // this warp's partial stores are complete
+    __syncwarp();
+    __threadfence();
+    ptx::named_bar_sync(1, 256);                         // all 8 epilogue warps published
+    const int tile = (wp.mt * a.n_tiles + wp.nt) * (pair ? 2 : 1) + (int)crank;
+    if (warp == 4 && lane == 0) {
+        const int old = atomicAdd(a.counters + tile, 1);
+        *sFlag = (old == a.splits - 1) ? 1 : 0;
+    }
+    ptx::named_bar_sync(1, 256);
+    const bool last = (*sFlag != 0);
+    if (!last) return;
+    __threadfence();
+    // Final pass, coalesced: a warp sums 128 consecutive columns (4 per lane) of one output row over
+    // the splits (all splits' loads issued before the in-order sum).
+    T *y = static_cast<T *>(a.y);
+    const int n0 = wp.nt * a.bn;
+    const int ncols = min(a.bn, a.K - n0);
+    const int cblocks = (ncols + 127) / 128;
+    const int items = nsub * 128 * cblocks;
+    const long long MK = a.M * (long long)a.K;
+    const long long m0 = (long long)wp.mt * a.bm + crank * 128;
+    const bool vec = (a.K % 4) == 0;
+    // 4 items x 4 splits of 16-byte loads in flight per lane (the fixup is L2-latency bound)
+    constexpr int U = 4;
+    for (int base = warp - 4; base < items; base += 8 * U) {
+        long long mm[U];
+        int kk[U];
+        bool ok[U];
+        float4 acc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int item = base + u * 8;
+            const int r = item / cblocks, cb = item - (item / cblocks) * cblocks;
+            mm[u] = m0 + r;
+            kk[u] = n0 + cb * 128 + lane * 4;
+            ok[u] = item < items && mm[u] < a.M && kk[u] < n0 + ncols;
+            acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        bool all_v4 = vec;
+#pragma unroll
+        for (int u = 0; u < U; ++u) all_v4 = all_v4 && (!ok[u] || kk[u] + 3 < a.K);
+        if (all_v4) {
+            for (int sp0 = 0; sp0 < a.splits; sp0 += 4) {
+                float4 q[4][U];
+#pragma unroll
+                for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        q[s4][u] = (ok[u] && sp0 + s4 < a.splits)
+                            ? __ldcg(reinterpret_cast<const float4 *>(a.partial + (sp0 + s4) * MK + mm[u] * a.K + kk[u]))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        acc[u].x += q[s4][u].x; acc[u].y += q[s4][u].y; acc[u].z += q[s4][u].z; acc[u].w += q[s4][u].w;
+                    }
+            }
+        } else {
+            for (int u = 0; u < U; ++u) {
+                if (!ok[u]) continue;
+                for (int sp = 0; sp < a.splits; ++sp) {
+                    const float *s = a.partial + sp * MK + mm[u] * a.K + kk[u];
+                    acc[u].x += __ldcg(s);
+                    if (kk[u] + 1 < a.K) acc[u].y += __ldcg(s + 1);
+                    if (kk[u] + 2 < a.K) acc[u].z += __ldcg(s + 2);
+                    if (kk[u] + 3 < a.K) acc[u].w += __ldcg(s + 3);
+                }
+            }
+        }
+        for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+            const long long m = mm[u];
+            const int k = kk[u];
+            float v[4] = {acc[u].x, acc[u].y, acc[u].z, acc[u].w};
+            bias_relu4(v, sBias, k, a.epilogue == 2);
+            if (a.out_nchw) {
+                const long long nimg = m / a.PQ;
+                const long long ob = nimg * (long long)a.K * a.PQ + (m - nimg * a.PQ);
+                for (int j = 0; j < 4; ++j)
+                    if (k + j < a.K) st_out(y + ob + (long long)(k + j) * a.PQ, v[j]);
+            } else {
+                T *dst = y + m * a.K + k;
+                if (vec && k + 3 < a.K) {
+                    if constexpr (sizeof(T) == 2) {
+                        const uint32_t lo = pack2(v[0], v[1], (T *)nullptr), hi = pack2(v[2], v[3], (T *)nullptr);
+                        *reinterpret_cast<uint2 *>(dst) = make_uint2(lo, hi);
+                    } else {
+                        *reinterpret_cast<float4 *>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+                    }
+                } else {
+                    for (int j = 0; j < 4; ++j)
+                        if (k + j < a.K) st_out(dst + j, v[j]);
+                }
+            }
+        }
+    }
+    ptx::named_bar_sync(1, 256);
+    if (warp == 4 && lane == 0) a.counters[tile] = 0;    // self-resetting for the next launch
+}
+
+// A_MODE 2 producer: element gather (small C, NHWC or NCHW x) straight into the 128-byte-swizzled
+// K-major A stage; kg = (r*S + s)*C + c; thread t owns rows t and 128 + t of every stage.
+template <bool kTF32>
+__device__ __forceinline__ void element_gather(const UmmaArgs &a, uint8_t *smA, uint32_t a_bytes, uint64_t *full,
+                                               uint64_t *empty, int nsub, long long wstart, long long wstep, int t,
+                                               int lane) {
+    const int RSC = a.R * a.S * a.C;
+    uint32_t stage = 0, phase = 0;
+    for (long long w = wstart; w < a.work; w += wstep) {
+        const WorkPos wp = decode_work(w, a);
+        const int kb0 = wp.split * a.kb_per_split;
+        const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+        int rh0[2], rw0[2], rn[2];
+        bool rv[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const long long m = (long long)wp.mt * a.bm + hh * 128 + t;
+            rv[hh] = hh < nsub && m < a.M;
+            const long long mm = rv[hh] ? m : 0;
+            const int n = (int)(mm / a.PQ);
+            const int rem = (int)(mm - (long long)n * a.PQ);
+            const int p = rem / a.Q, q = rem - (rem / a.Q) * a.Q;
+            rn[hh] = n;
+            rh0[hh] = p * a.stride_h - a.pad_h;
+            rw0[hh] = q * a.stride_w - a.pad_w;
+        }
+        for (int kb = kb0; kb < kb1; ++kb) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                if (hh >= nsub) break;
+                const int row = hh * 128 + t;
+                const uint32_t rbase = ptx::smem_u32(smA + stage * a_bytes) + (uint32_t)(row >> 3) * 1024u +
+                                       (uint32_t)(row & 7) * 128u;
+                constexpr int PC = kTF32 ? 4 : 8;          // elements per 16-byte chunk
+                int kg = kb * PC * 8;                      // first element of this 128-byte K block
+                int c = kg % a.C, rs_ = kg / a.C;
+                int s = rs_ % a.S, r = rs_ / a.S;
+                // two chunks (16 independent loads) in flight at a time; 32-bit offsets
+#pragma unroll 1
+                for (int j = 0; j < 8; j += 2) {
+                    int off[2 * PC];
+                    bool okv[2 * PC];
+#pragma unroll
+                    for (int e = 0; e < 2 * PC; ++e, ++kg) {
+                        const int hi = rh0[hh] + r * a.dil_h, wi = rw0[hh] + s * a.dil_w;
+                        okv[e] = rv[hh] && kg < RSC && hi >= 0 && hi < a.H && wi >= 0 && wi < a.W;
+                        off[e] = a.x_nchw ? ((rn[hh] * a.C + c) * a.H + hi) * a.W + wi
+                                          : ((rn[hh] * a.H + hi) * a.W + wi) * a.C + c;
+                        if (++c == a.C) { c = 0; if (++s == a.S) { s = 0; ++r; } }
+                    }
+                    uint32_t bits[2 * PC];
+#pragma unroll
+                    for (int e = 0; e < 2 * PC; ++e)
+                        bits[e] = !okv[e] ? 0u
+                                  : kTF32 ? __ldg(reinterpret_cast<const unsigned *>(a.x) + off[e])
+                                          : (uint32_t)__ldg(reinterpret_cast<const unsigned short *>(a.x) + off[e]);
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj) {
+                        uint32_t wv[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            wv[q] = kTF32 ? bits[jj * 4 + q] : (bits[jj * 8 + 2 * q] | (bits[jj * 8 + 2 * q + 1] << 16));
+                        ptx::st_shared_v4(rbase + ((uint32_t)((j + jj) ^ (row & 7)) << 4), wv[0], wv[1], wv[2], wv[3]);
+                    }
+                }
+            }
+            ptx::fence_proxy_async_smem();                 // generic-proxy writes -> async-proxy (MMA) reads
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&full[stage]);
+            if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
+        }
+    }
+}
+
+// A_MODE 3 producer: pixel-segment gather (C <= 4, x NHWC with 4 channels per pixel). K row =
+// (r, s', c), s' < Sp; a 16-byte smem chunk holds PPC whole pixels of one filter row, so every
+// chunk is PPC aligned 8/16-byte cp.async copies (zero-filled outside the image and for s' >= S /
+// r >= R). The copies of a stage are asynchronous: a thread keeps up to LAG stages in flight and
+// signals a stage full only after cp.async.wait_group + a proxy fence, so the global-load latency
+// overlaps across stages with no registers held. Thread t owns rows t and 128 + t of every stage.
+template <bool kTF32, int LAG>
+__device__ __forceinline__ void segment_gather(const UmmaArgs &a, uint8_t *smA, uint32_t a_bytes, uint64_t *full,
+                                               uint64_t *empty, int nsub, long long wstart, long long wstep, int t,
+                                               int lane) {
+    constexpr int PPC = kTF32 ? 1 : 2;                 // pixels per 16-byte chunk
+    constexpr int PB = 16 / PPC;                       // bytes per stored pixel
+    const int chunks_per_r = a.seg_sp / PPC;
+    const int rstep = a.dil_h * a.W * PB;              // bytes between filter rows
+    const int sstep = a.dil_w * PB;                    // bytes between filter columns
+    const char *xb = static_cast<const char *>(a.x);
+    uint32_t stage = 0, phase = 0;
+    uint32_t pend[LAG];                                // stages issued but not yet signalled (FIFO)
+    int npend = 0;
+    for (long long w = wstart; w < a.work; w += wstep) {
+        const WorkPos wp = decode_work(w, a);
+        // per row: byte offset of tap (0,0) and validity bitmasks over filter rows / columns
+        long long roff[2];
+        uint32_t rmask[2], smask[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            roff[hh] = 0; rmask[hh] = 0u; smask[hh] = 0u;
+            const long long m = (long long)wp.mt * a.bm + hh * 128 + t;
+            if (hh < nsub && m < a.M) {
+                const int n = (int)(m / a.PQ);
+                const int rem = (int)(m - (long long)n * a.PQ);
+                const int p = rem / a.Q, q = rem - (rem / a.Q) * a.Q;
+                const int h0 = p * a.stride_h - a.pad_h, w0 = q * a.stride_w - a.pad_w;
+                roff[hh] = (((long long)n * a.H + h0) * a.W + w0) * PB;
+                for (int r = 0; r < a.R; ++r) {
+                    const int hi = h0 + r * a.dil_h;
+                    if (hi >= 0 && hi < a.H) rmask[hh] |= 1u << r;
+                }
+                for (int c = 0; c < a.S; ++c) {
+                    const int wi = w0 + c * a.dil_w;
+                    if (wi >= 0 && wi < a.W) smask[hh] |= 1u << c;
+                }
+            }
+        }
+        const int kb0 = wp.split * a.kb_per_split;
+        const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            const int cj = kb * 8;
+            const int r0 = cj / chunks_per_r, s00 = (cj - r0 * chunks_per_r) * PPC;
+#pragma unroll 1
+            for (int hh = 0; hh < nsub; ++hh) {
+                const int row = hh * 128 + t;
+                const uint32_t rbase = ptx::smem_u32(smA + stage * a_bytes) + (uint32_t)(row >> 3) * 1024u +
+                                       (uint32_t)(row & 7) * 128u;
+                const long long ro = hh ? roff[1] : roff[0];
+                const uint32_t rmk = hh ? rmask[1] : rmask[0], smk = hh ? smask[1] : smask[0];
+                int r = r0, s0 = s00;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const char *src = xb + ro + (long long)(r * rstep + s0 * sstep);
+                    // bit e: pixel s0 + e valid (r >= R or s >= S: mask bit 0)
+                    uint32_t ok = (0u - ((rmk >> r) & 1u)) & (smk >> s0);
+                    if (a.dbg_flags & 1) ok = 0u;
+                    const uint32_t dst = rbase + ((uint32_t)(j ^ (row & 7)) << 4);
+                    if constexpr (PPC == 1) {
+                        ptx::cp_async_16(dst, (ok & 1u) ? src : xb, (ok & 1u) ? 16u : 0u);
+                    } else {
+                        ptx::cp_async_8(dst, (ok & 1u) ? src : xb, (ok & 1u) ? 8u : 0u);
+                        ptx::cp_async_8(dst + 8, (ok & 2u) ? src + sstep : xb, (ok & 2u) ? 8u : 0u);
+                    }
+                    s0 += PPC;
+                    if (s0 == a.seg_sp) { s0 = 0; ++r; }
+                }
+            }
+            ptx::cp_async_commit();
+            if (npend == LAG) {                          // oldest stage's copies done -> signal it
+                ptx::cp_async_wait<LAG>();
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&full[pend[0]]);
+#pragma unroll
+                for (int i = 0; i + 1 < LAG; ++i) pend[i] = pend[i + 1];
+                --npend;
+            }
+            pend[npend++] = stage;
+            if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
+        }
+    }
+    ptx::cp_async_wait<0>();
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0)
+        for (int i = 0; i < npend; ++i) ptx::mbar_arrive(&full[pend[i]]);
+}
+
+// 12 warps (16 with gather producers): 0 = A producer, 1 = TMEM allocator + MMA issuer,
+// 2 = B producer, 3 = spare, 4..11 = epilogue (two groups of four; warp w reads TMEM lanes
+// [32*(w%4), +32)), 12..15 = gather producers.
+template <int DT, int AK, int EK>
+__global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
+    umma_conv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmP,
+                     const __grid_constant__ UmmaArgs a) {
+    using T = typename OutT<DT>::T;
+    constexpr bool kTF32 = (DT == DT_TF32);
+    constexpr bool kPair = (AK == AK_PAIR);
+    constexpr bool kGather = (AK >= AK_GATHER);
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = ptx::smem_u32(smem_raw);
+    uint8_t *smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+    // CTA pair (cta_group::2): each CTA holds 128 rows of A and half of B; the pair computes 256 x BN
+    const uint32_t a_bytes = (uint32_t)(kPair ? 128 : a.bm) * 128u;
+    const uint32_t b_bytes = (uint32_t)(kPair ? a.bn / 2 : a.bn) * 128u;
+    const int nsub = kPair ? 1 : a.bm / 128;                           // 128-row MMAs per tile per CTA
+    const uint32_t crank = kPair ? ptx::cluster_ctarank() : 0u;
+    const bool leader = (crank == 0);
+    const long long wstart = kPair ? (long long)(blockIdx.x >> 1) : (long long)blockIdx.x;
+    const long long wstep = kPair ? (long long)(gridDim.x >> 1) : (long long)gridDim.x;
+    uint8_t *smA = smem;
+    uint8_t *smB = smem + (size_t)a.stages * a_bytes;
+    uint8_t *sEpi = smem + a.epi_off;                                  // [8 warps][2][32 rows][128 B]
+    float *sBias = reinterpret_cast<float *>(smem + a.bias_off);      // [Kpad]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.bar_off);
+    uint64_t *full = bars;            // [8]
+    uint64_t *empty = bars + 8;       // [8]
+    uint64_t *tfull = bars + 16;      // [4]
+    uint64_t *tempty = bars + 20;     // [4]
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 24);
+    volatile int *sFlag = reinterpret_cast<volatile int *>(bars + 25);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long *dbg = a.dbg ? a.dbg + blockIdx.x * 64 : nullptr;
+    if (dbg && threadIdx.x == 0) dbg[0] = ptx::globaltimer();
+
+    if (warp == 0 && lane == 0) {
+        if (!kGather) ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        if (EK != EK_DIRECT) ptx::prefetch_tmap(&tmY);
+        if (EK == EK_SPLIT) ptx::prefetch_tmap(&tmP);
+        for (int s = 0; s < a.stages; ++s) {
+            ptx::mbar_init(&full[s], kGather ? 5 : 2);   // A (TMA, or 4 gather warps) + B producer
+            ptx::mbar_init(&empty[s], 1);      // MMA commit
+        }
+        for (int s = 0; s < a.acc_stages; ++s) {
+            ptx::mbar_init(&tfull[s], 1);
+            ptx::mbar_init(&tempty[s], kPair ? 16 : 8);   // 8 epilogue warps (x2 CTAs for a pair)
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) {
+        if (kPair) {
+            ptx::tmem_alloc2(tmem_holder, a.tmem_cols);
+            ptx::tmem_relinquish2();
+        } else {
+            ptx::tmem_alloc(tmem_holder, a.tmem_cols);
+            ptx::tmem_relinquish();
+        }
+    }
+    // Programmatic dependent launch: this prologue overlaps the previous kernel's tail. Weights and
+    // bias are inference constants, so the bias is staged, and the B producer starts
+    // streaming weight tiles into shared memory, before the previous grid has finished; only the
+    // threads that read activations (A producers) or write the output (epilogue) execute
+    // griddepcontrol.wait.
+    if (warp >= 4 && warp < 12) {   // bias -> smem once (fp32, zero past K); zero without bias
+        const T *bias = static_cast<const T *>(a.bias);
+        for (int k = threadIdx.x - 128; k < a.kpad_bias; k += 256)
+            sBias[k] = (a.epilogue >= 1 && k < a.K) ? ld_bias(bias, k) : 0.f;
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (kPair) ptx::cluster_sync();   // peer barriers initialised before any remote arrive / TMA
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    if (dbg && threadIdx.x == 0) dbg[1] = ptx::globaltimer();
+
+    if (warp == 0 || warp == 2) {
+        // ===================== TMA producers: warp 0 -> A (activations), warp 2 -> B (weights) ====
+        if (lane == 0 && !(kGather && warp == 0)) {
+            const bool isA = (warp == 0);
+            if (isA) asm volatile("griddepcontrol.wait;" ::: "memory");
+            uint32_t stage = 0, phase = 0;
+            const uint32_t tx = isA ? a_bytes : b_bytes;
+            uint8_t *dst0 = isA ? smA : smB;
+            for (long long w = wstart; w < a.work; w += wstep) {
+                const WorkPos wp = decode_work(w, a);
+                const long long m0 = (long long)wp.mt * a.bm + crank * 128;
+                const int n0 = wp.nt * a.bn + (int)crank * (a.bn / 2);
+                int wc = 0, hc = 0, nimg = 0;
+                if (isA && !a.a_tiled) {
+                    nimg = (int)(m0 / a.PQ);
+                    const int rem = (int)(m0 - (long long)nimg * a.PQ);
+                    const int p = rem / a.Q, q = rem - (rem / a.Q) * a.Q;
+                    wc = q * a.stride_w - a.pad_w;
+                    hc = p * a.stride_h - a.pad_h;
+                }
+                const int kb0 = wp.split * a.kb_per_split;
+                const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+                // (r, s, c-block) of kb0, then advanced incrementally (no divisions in the k loop)
+                int cb = kb0 % a.c_blocks;
+                int rs = kb0 / a.c_blocks;
+                int r = rs / a.S, s = rs % a.S;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t *dst = dst0 + stage * tx;
+                    if constexpr (kPair) {
+                        // both CTAs' bytes land on the leader's barrier; only the leader arms it
+                        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * tx);
+                        if (!isA)
+                            ptx::tma_load_3d_pair(dst, &tmB, &full[stage], cb * a.bk, rs, n0);
+                        else if (a.a_tiled)
+                            ptx::tma_load_2d_pair(dst, &tmA, &full[stage], cb * a.bk, (int)m0);
+                        else
+                            ptx::tma_load_im2col_4d_pair(dst, &tmA, &full[stage], cb * a.bk, wc, hc, nimg,
+                                                         (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                    } else {
+                        ptx::mbar_arrive_expect_tx(&full[stage], tx);
+                        if (!isA)
+                            ptx::tma_load_3d(dst, &tmB, &full[stage], cb * a.bk, rs, n0);
+                        else if (a.a_tiled)
+                            ptx::tma_load_2d(dst, &tmA, &full[stage], cb * a.bk, (int)m0);
+                        else
+                            ptx::tma_load_im2col_4d(dst, &tmA, &full[stage], cb * a.bk, wc, hc, nimg,
+                                                    (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                    }
+                    if (++cb == a.c_blocks) {
+                        cb = 0;
+                        ++rs;
+                        if (++s == a.S) { s = 0; ++r; }
+                    }
+                    if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (kGather && warp >= 12) {
+        // ===================== gather producers (A_MODE 2 / 3) =====================
+        const int t = threadIdx.x - 384;                       // 0..127
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if constexpr (AK == AK_SEG) {
+            segment_gather<kTF32, 2>(a, smA, a_bytes, full, empty, nsub, wstart, wstep, t, lane);   // STAGES >= 3
+        } else if constexpr (AK == AK_GATHER) {
+            element_gather<kTF32>(a, smA, a_bytes, full, empty, nsub, wstart, wstep, t, lane);
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (single thread; the leader CTA of a pair) =====================
+        if (lane == 0 && leader) {
+            uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+            const uint64_t a_desc0 = ptx::sw128_kmajor_desc(ptx::smem_u32(smA));
+            const uint64_t b_desc0 = ptx::sw128_kmajor_desc(ptx::smem_u32(smB));
+            const uint32_t acc_cols = (uint32_t)(nsub * a.bn);
+            for (long long w = wstart; w < a.work; w += wstep) {
+                const WorkPos wp = decode_work(w, a);
+                const int kb0 = wp.split * a.kb_per_split;
+                const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const long long dit = (w - wstart) / wstep;     // debug: per-tile events of the first 8 tiles
+                if (dbg && dit < 8) dbg[16 + dit * 6 + 0] = ptx::globaltimer();
+                const uint32_t d_tmem = tmem_base + acc * acc_cols;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    if (dbg && w == wstart && kb == kb0) dbg[2] = ptx::globaltimer();
+                    if (dbg && dit < 8 && kb == kb0) dbg[16 + dit * 6 + 1] = ptx::globaltimer();
+                    const uint64_t ad = a_desc0 + (uint64_t)((stage * a_bytes) >> 4);
+                    const uint64_t bd = b_desc0 + (uint64_t)((stage * b_bytes) >> 4);
+                    if constexpr (kPair) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            ptx::umma2<kTF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        ptx::umma_commit2_multicast(&empty[stage]);   // frees the stage in both CTAs
+                    } else {
+                        for (int h = 0; h < nsub; ++h) {
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)   // 4 x 32 bytes of K per 128-byte stage (+2 desc units)
+                                ptx::umma<kTF32>(d_tmem + h * a.bn, ad + h * (16384 >> 4) + 2 * kk, bd + 2 * kk, a.idesc,
+                                                 (kb > kb0 || kk > 0) ? 1u : 0u);
+                        }
+                        ptx::umma_commit(&empty[stage]);   // frees this smem stage when the MMAs finish
+                    }
+                    if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
+                }
+                if constexpr (kPair) ptx::umma_commit2_multicast(&tfull[acc]);   // both CTAs' halves ready
+                else ptx::umma_commit(&tfull[acc]);                               // accumulator ready
+                if (dbg && w == wstart) dbg[3] = ptx::globaltimer();
+                if (dbg && dit < 8) dbg[16 + dit * 6 + 2] = ptx::globaltimer();
+                if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else if (warp >= 4 && warp < 12) {
+        // ===================== epilogue warps 4..11 =====================
+        asm volatile("griddepcontrol.wait;" ::: "memory");   // y may still be in use upstream
+        const int quarter = warp & 3;          // TMEM lane quarter this warp may access
+        const int grp = (warp - 4) >> 2;       // 0 or 1
+        uint32_t acc = 0, acc_phase = 0;
+        EpiCtx E{sBias, sEpi + (size_t)(warp - 4) * a.epi_bufs * 4096, 0u, lane, a.epi_bufs};
+        const uint32_t acc_cols = (uint32_t)(nsub * a.bn);
+        constexpr int cwf = (EK == EK_DIRECT) ? 16 : (int)(128 / sizeof(T));   // final-output chunk width
+        constexpr int cwp = (EK == EK_DIRECT) ? 16 : 32;                        // fp32-partial chunk width
+        for (long long w = wstart; w < a.work; w += wstep) {
+            const WorkPos wp = decode_work(w, a);
+            const int n0 = wp.nt * a.bn;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const long long dit = (w - wstart) / wstep;
+            if (dbg && warp == 4 && lane == 0 && dit < 8) dbg[16 + dit * 6 + 3] = ptx::globaltimer();
+            // split-K (EK_SPLIT): the tile's last split owns the output; it waits until the other
+            // splits have published their partials (they precede it in the static schedule, so they
+            // are resident or done: no deadlock), then reduces them in split order.
+            const bool owner = (EK != EK_SPLIT) || wp.split == a.splits - 1;
+            const int ctile = (wp.mt * a.n_tiles + wp.nt) * (kPair ? 2 : 1) + (int)crank;
+            if (EK == EK_SPLIT && owner) {
+                if (warp == 4 && lane == 0) {
+                    while (ptx::ld_acquire_gpu(a.counters + ctile) < a.splits - 1) __nanosleep(32);
+                }
+                ptx::named_bar_sync(1, 256);
+            }
+            const int cw = owner ? cwf : cwp;
+            const int nchunks = (a.bn + cw - 1) / cw;
+            // slabs = (h, chunk) pairs; group g takes h == g when nsub == 2, else every other chunk
+            for (int h = 0; h < nsub; ++h) {
+                if (nsub == 2 && h != grp) continue;
+                const int mrow = wp.mt * a.bm + (int)crank * 128 + h * 128 + quarter * 32;
+                const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * acc_cols + h * a.bn;
+                for (int ci = (nsub == 2 ? 0 : grp); ci < nchunks; ci += (nsub == 2 ? 1 : 2)) {
+                    const int c0 = ci * cw;
+                    const int k0 = n0 + c0;
+                    if (k0 >= a.K) break;   // warp-uniform
+                    if constexpr (EK == EK_TMA) {
+                        epi_chunk_tma<T, true>(E, a, &tmY, tbase + c0, k0, mrow, 0);
+                    } else if constexpr (EK == EK_SPLIT) {
+                        if (owner) epi_chunk_owner<T>(E, a, &tmY, tbase + c0, k0, mrow);
+                        else epi_chunk_tma<T, false>(E, a, &tmP, tbase + c0, k0, mrow, wp.split);
+                    } else {
+                        epi_chunk_direct<T>(a, sBias, tbase + c0, k0, (long long)mrow + lane, wp.split, a.splits == 1);
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (dbg && warp == 4 && lane == 0 && w == wstart) dbg[4] = ptx::globaltimer();
+            if (dbg && warp == 4 && lane == 0 && dit < 8) {
+                dbg[8 + dit] = ptx::globaltimer();
+                dbg[16 + dit * 6 + 4] = ptx::globaltimer();
+            }
+            if (lane == 0) {                                  // TMEM free: the MMA may start the next tile
+                if constexpr (kPair) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+                else ptx::mbar_arrive(&tempty[acc]);
+            }
+            if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
+            if constexpr (EK == EK_SPLIT) {
+                if (!owner) {   // publish: partial stores complete and visible, then count this split in
+                    if (lane == 0) ptx::bulk_wait_all();
+                    __syncwarp();
+                    __threadfence();
+                    ptx::named_bar_sync(1, 256);
+                    if (warp == 4 && lane == 0) atomicAdd(a.counters + ctile, 1);
+                } else {        // all 8 warps have consumed the partials: reset for the next launch
+                    ptx::named_bar_sync(1, 256);
+                    if (warp == 4 && lane == 0) a.counters[ctile] = 0;
+                }
+            }
+            if (EK == EK_DIRECT && a.splits > 1) splitk_fixup<T>(a, sBias, sFlag, wp, nsub, warp, lane, crank, kPair ? 1 : 0);
+        }
+        if (EK != EK_DIRECT && lane == 0) ptx::bulk_wait_all();
+        if (dbg && warp == 4 && lane == 0) dbg[5] = ptx::globaltimer();
+    }
+
+    __syncthreads();
+    if (kPair) ptx::cluster_sync();   // the peer no longer touches our barriers / TMEM
+    if (dbg && threadIdx.x == 0) dbg[6] = ptx::globaltimer();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        if (kPair) ptx::tmem_dealloc2(tmem_base, a.tmem_cols);
+        else ptx::tmem_dealloc(tmem_base, a.tmem_cols);
+    }
+}
+
+// ---- launch of one (dtype) instantiation family -----------------------------------------------
+template <int DT, int AK, int EK>
+static cudaError_t launch_variant(cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
+                                  const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    return cudaLaunchKernelEx(&lc, umma_conv_kernel<DT, AK, EK>, tmA, tmB, tmY, tmP, a);
+}
+
+template <int DT, int AK>
+static cudaError_t launch_ak(int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
+                             const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
+    if (ek == EK_TMA) return launch_variant<DT, AK, EK_TMA>(lc, tmA, tmB, tmY, tmP, a);
+    if (ek == EK_SPLIT) return launch_variant<DT, AK, EK_SPLIT>(lc, tmA, tmB, tmY, tmP, a);
+    return launch_variant<DT, AK, EK_DIRECT>(lc, tmA, tmB, tmY, tmP, a);
+}
+
+template <int DT>
+cudaError_t umma_launch_dt(int ak, int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
+                           const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
+    if (ak == AK_PAIR) return launch_ak<DT, AK_PAIR>(ek, lc, tmA, tmB, tmY, tmP, a);
+    if (ak == AK_GATHER) return launch_ak<DT, AK_GATHER>(ek, lc, tmA, tmB, tmY, tmP, a);
+    if (ak == AK_SEG) return launch_ak<DT, AK_SEG>(ek, lc, tmA, tmB, tmY, tmP, a);
+    return launch_ak<DT, AK_TMA>(ek, lc, tmA, tmB, tmY, tmP, a);
+}
+
+}  // namespace wpk

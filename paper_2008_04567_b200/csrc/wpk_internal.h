@@ -64,7 +64,9 @@ struct UmmaGeom {
     long long work;
     int cpad;           // channel count as stored for the kernel (C rounded up to the alignment)
     int pair;           // 1: tcgen05 CTA pair (cta_group::2, cluster of 2), 256 x BLOCK_N tiles
-    int a_mode;         // 0: TMA im2col (or tiled for 1x1), 1: explicit im2col matrix in the workspace
+    int a_mode;         // 0: TMA im2col (or tiled for 1x1), 1: explicit im2col matrix in the workspace,
+                        // 2: element gather into smem, 3: pixel-segment gather (C <= 4)
+    int seg_sp;         // A_MODE 3: filter columns per row padded to whole 16-byte chunks
     int a_tiled;        // 1: A fetched by a plain 2-D TMA tile load (1x1, stride 1, pad 0), else im2col
     int epi_bufs;       // staging buffers per epilogue warp (2 = double-buffered TMA stores)
     int epi_tma;        // 1: epilogue stages 32x128-byte tiles in smem and TMA-stores them

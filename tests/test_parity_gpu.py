@@ -68,7 +68,7 @@ def _umma_space():
     bns = [16, 32, 64, 96, 128, 192, 256]
     out = []
     for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1, 2, 3], [0, 1, 2],
-                                                          [1, 2], [128, 256]):
+                                                          [1, 2, 4], [128, 256]):
         out.append((bn, st, sp, ra, amode, acc, bm))
     return out
 
@@ -129,7 +129,8 @@ def test_umma_1x1_and_epilogue_paths(dtype, env, monkeypatch):
 
 @pytest.mark.parametrize("dtype", ["bf16", "tf32"])
 def test_cta_pair_configs(dtype):
-    """tcgen05 CTA pairs (cta_group::2): 3x3 and strided shapes with M and K tails."""
+    """tcgen05 CTA pairs (cta_group::2): 3x3 and strided shapes with M and K tails, with split-K
+    (per-CTA-half fixup counters) and 1/2/4 accumulator stages."""
     from paper_2008_04567_b200 import Conv2dPlan
     from _util import to_layout, from_layout
     for L in [ConvLayer("p3", 2, 64, 17, 19, 160, 3, 3, 1, 1), ConvLayer("p3s2", 3, 128, 15, 15, 96, 3, 3, 2, 1)]:
@@ -139,8 +140,8 @@ def test_cta_pair_configs(dtype):
         xl, wl = to_layout(x, w, "nhwc")
         xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
         n = 0
-        for bn, st, mode, acc in itertools.product([32, 64, 128, 256], [2, 4], [2, 3], [1, 2]):
-            genes = [bn, st, 1, mode, 0, acc, 256]
+        for bn, st, mode, acc, sp in itertools.product([32, 64, 128, 256], [2, 4], [2, 3], [1, 2, 4], [1, 2, 4]):
+            genes = [bn, st, sp, mode, 0, acc, 256]
             if not plan.config_valid(1, genes):
                 continue
             plan.set_config(1, genes)
@@ -220,6 +221,34 @@ def test_gather_producer_small_c(dtype, layout):
             y = plan.run(xl, wl, bc)
             torch.cuda.synchronize()
             assert_bit_exact(from_layout(y.cpu(), layout), ref)
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+@pytest.mark.parametrize("dtype", ["bf16", "f16", "tf32"])
+def test_segment_gather_small_c(dtype, layout):
+    """A_MODE 3 (pixel-segment gather, C <= 4): conv1-like 7x7/s2, VGG conv1_1-like 3x3/s1,
+    MobileNet stem-like 3x3/s2, C=1 with dilation, C=4 5x5/s3, ragged M and K tails."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import to_layout, from_layout
+    for L in [ConvLayer("c3s2", 2, 3, 30, 30, 64, 7, 7, 2, 3), ConvLayer("c3s1", 1, 3, 19, 21, 72, 3, 3, 1, 1),
+              ConvLayer("stem", 3, 3, 17, 17, 32, 3, 3, 2, 1), ConvLayer("c1d2", 2, 1, 23, 20, 40, 3, 3, 1, 2, 2),
+              ConvLayer("c4s3", 1, 4, 31, 29, 24, 5, 5, 3, 0), ConvLayer("c2", 1, 2, 9, 9, 16, 2, 4, 1, 1)]:
+        x, w, b = workloads.generate(L, dtype, "int", seed=29)
+        ref = oracle_full(L, x, w, b)
+        plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, layout=layout, dtype=dtype)
+        xl, wl = to_layout(x, w, layout)
+        xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
+        ran = 0
+        for genes in [(64, 4, 1, 0, 3, 2, 128), (128, 3, 2, 1, 3, 2, 256), (32, 6, 1, 0, 3, 1, 128),
+                      (16, 3, 1, 0, 3, 4, 256)]:
+            if not plan.config_valid(1, list(genes)):
+                continue
+            plan.set_config(1, list(genes))
+            y = plan.run(xl, wl, bc)
+            torch.cuda.synchronize()
+            assert_bit_exact(from_layout(y.cpu(), layout), ref)
+            ran += 1
+        assert ran >= 2, L.name
 
 
 @pytest.mark.parametrize("layer", workloads.resnet50(32), ids=lambda l: l.name)
