@@ -132,7 +132,7 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->ctas_per_sm = 1;
     g->a_mode = cfg.genes[4];
     g->acc_stages = cfg.genes[5];
-    g->seg_sp = 0;
+    g->seg_sp = 0; g->seg_hp = 0; g->seg_wp = 0; g->seg_fast = 0; g->seg_two = 0;
     if ((g->a_mode == 1 || g->a_mode == 2) && d.c >= 64)
         return no("A_MODE 1/2 (explicit im2col / gather) is reserved for layers with C < 64");
     if (g->a_mode == 3) {
@@ -140,12 +140,23 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
         // bytes); K row = (r, s', c) with s' padded to Sp so that one 16-byte smem chunk holds whole
         // pixels of a single filter row; weights for s' >= S and c >= C are zero.
         if (d.c > 4) return no("A_MODE 3 (pixel-segment gather) needs C <= 4");
-        if (d.r > 30 || d.s > 30) return no("A_MODE 3 needs R, S <= 30 (validity bitmasks)");
         if (g->stages < 3) return no("A_MODE 3 keeps two stages of copies in flight: STAGES >= 3");
         if ((double)d.n * d.h * d.w * 4 >= 2147483647.0) return no("segment gather needs < 2^31 input elements");
         const int ppc = 16 / (4 * e);                         // pixels per 16-byte chunk: 2 (16-bit), 1 (tf32)
         g->seg_sp = round_up(d.s, ppc);
         g->cpad = d.r * g->seg_sp * 4;
+        // the activations are re-laid into an explicitly zero-padded image (no bounds checks in
+        // the gather); the extra columns cover the dummy filter columns s' in [S, Sp)
+        g->seg_hp = d.h + 2 * d.ph;
+        // one 16-byte copy per chunk when its PPC pixels are adjacent (dil_w 1); with an odd stride a
+        // second copy of the image shifted by one pixel keeps every chunk 16-byte aligned (rows of
+        // odd q*stride_w read the shifted copy)
+        g->seg_fast = (ppc == 1) || d.dw == 1;
+        g->seg_two = (ppc == 2 && d.dw == 1 && d.sw % 2 == 1) ? 1 : 0;
+        g->seg_wp = round_up(d.w + 2 * d.pw + (g->seg_sp - d.s) * d.dw + g->seg_two, 2);   // even: 16-B rows
+        if ((long long)d.n * g->seg_hp > 65535) return no("segment gather re-layout grid: N * (H + 2 pad_h) > 65535");
+        if ((double)d.n * g->seg_hp * g->seg_wp * 4 * (1 + g->seg_two) >= 2147483647.0)
+            return no("segment gather needs < 2^31 padded elements");
         g->c_blocks = (g->cpad + g->bk - 1) / g->bk;
         g->num_kb = g->c_blocks;
     } else if (g->a_mode == 1 || g->a_mode == 2) {

@@ -119,6 +119,34 @@ __global__ void pack_flat_kernel(const T *__restrict__ w, T *__restrict__ out, i
         out[i] = v;
     }
 }
+// Activations for the pixel-segment gather (A_MODE 3): out[n][h'][w'][4], the image placed at
+// (ph, pw) of an Hp x Wp zero canvas, channels >= C zero. Grid (column blocks, N*Hp rows, copies):
+// one thread per padded pixel, no divisions. The second copy (odd stride, 16-bit) is shifted right
+// by one pixel.
+template <typename T>
+__global__ void seg_pad_kernel(const T *__restrict__ x, T *__restrict__ out, int N, int C, int H, int W, int Hp,
+                               int Wp, int ph, int pw, int nchw) {
+    const int wq = blockIdx.x * blockDim.x + threadIdx.x;
+    if (wq >= Wp) return;
+    const int nh = blockIdx.y;                      // n * Hp + hq
+    const int shift = blockIdx.z;
+    const int n = nh / Hp, hq = nh - n * Hp;
+    const int h = hq - ph, w = wq - pw - shift;
+    T v[4] = {T(0.f), T(0.f), T(0.f), T(0.f)};
+    if (h >= 0 && h < H && w >= 0 && w < W) {
+        for (int c = 0; c < C; ++c)
+            v[c] = nchw ? x[(((long long)n * C + c) * H + h) * W + w] : x[(((long long)n * H + h) * W + w) * C + c];
+    }
+    const long long i = ((long long)shift * N * Hp + nh) * Wp + wq;
+    if constexpr (sizeof(T) == 2) {
+        uint2 u;
+        u.x = (uint32_t)(*reinterpret_cast<uint16_t *>(&v[0])) | ((uint32_t)(*reinterpret_cast<uint16_t *>(&v[1])) << 16);
+        u.y = (uint32_t)(*reinterpret_cast<uint16_t *>(&v[2])) | ((uint32_t)(*reinterpret_cast<uint16_t *>(&v[3])) << 16);
+        reinterpret_cast<uint2 *>(out)[i] = u;
+    } else {
+        reinterpret_cast<float4 *>(out)[i] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
 // Weights for the pixel-segment gather (A_MODE 3): out[k][(r*Sp + s)*4 + c], zero for s >= S, c >= C
 // and beyond R*Sp*4 (up to kgp).
 template <typename T>
@@ -159,7 +187,10 @@ static unsigned grid_for(long long total, int sm) {
 template <typename T>
 static void launch_aux_t(int which, const void *src, void *dst, const ConvDesc &d, int cp, int sm, cudaStream_t st,
                          int sp) {
-    if (which == 6)
+    if (which == 7 || which == 8)   // 8: two copies; cp = padded height, sp = padded width
+        seg_pad_kernel<T><<<dim3((sp + 127) / 128, d.n * cp, which - 6), 128, 0, st>>>(
+            (const T *)src, (T *)dst, d.n, d.c, d.h, d.w, cp, sp, d.ph, d.pw, d.layout == WPK_NCHW);
+    else if (which == 6)
         pack_seg_kernel<T><<<grid_for((long long)d.k * cp, sm), 256, 0, st>>>((const T *)src, (T *)dst, d.k, d.c, d.r,
                                                                               d.s, sp, cp, d.layout == WPK_NCHW);
     else if (which == 0)
@@ -285,9 +316,7 @@ static WsLayout ws_layout(const ConvDesc &d, const Config &cfg, bool host_stagin
         } else if (g.a_mode == 2) {
             L.w_off = off; L.w_bytes = al256((size_t)d.k * g.cpad * e); off += L.w_bytes;
         } else if (g.a_mode == 3) {
-            if (d.layout == WPK_NCHW || d.c != 4) {
-                L.x_off = off; L.x_bytes = al256((size_t)d.n * d.h * d.w * 4 * e); off += L.x_bytes;
-            }
+            L.x_off = off; L.x_bytes = al256((size_t)d.n * g.seg_hp * g.seg_wp * 4 * e * (1 + g.seg_two)); off += L.x_bytes;
             L.w_off = off; L.w_bytes = al256((size_t)d.k * g.cpad * e); off += L.w_bytes;
         } else if (d.layout == WPK_NCHW || g.cpad != d.c) {
             L.x_off = off; L.x_bytes = al256((size_t)d.n * d.h * d.w * g.cpad * e); off += L.x_bytes;
@@ -388,11 +417,10 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     const void *xk = x, *wk = w;
     const int pack_kind = WPK_FAMILY_UMMA * 10 + g.a_mode;
     if (g.a_mode == 3) {
-        if (d.layout == WPK_NCHW || d.c != 4) {   // activations -> NHWC, 4 channels per pixel
-            launch_aux(d.layout == WPK_NCHW ? 0 : 1, x, ws + L.x_off, d, 4, sm, st);
-            ++launches;
-            xk = ws + L.x_off;
-        }
+        // activations -> zero-padded NHWC image with 4 channels per pixel
+        launch_aux(g.seg_two ? 8 : 7, x, ws + L.x_off, d, g.seg_hp, sm, st, g.seg_wp);
+        ++launches;
+        xk = ws + L.x_off;
         if (p.packed_for != w || p.packed_cfg_family != pack_kind) {
             launch_aux(6, w, ws + L.w_off, d, g.cpad, sm, st, g.seg_sp);
             ++launches;
@@ -455,6 +483,7 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     U.a_rows = (g.a_mode == 1) ? d.M() : (long long)d.n * d.h * d.w;
     U.b_rs = (g.a_mode >= 1) ? 1 : d.r * d.s;
     U.C = (g.a_mode == 3) ? 4 : d.c;                          // channels per stored pixel
+    if (g.a_mode == 3) { U.H = g.seg_hp; U.W = g.seg_wp; }    // the gather walks the padded image
     U.x_nchw = (g.a_mode == 3) ? 0 : (d.layout == WPK_NCHW);
     U.dbg = g_debug_timeline;
     if (!p.map_cache) p.map_cache = new UmmaMapCache();

@@ -182,7 +182,7 @@ launch:
     a.x = L.x;
     a.x_nchw = L.x_nchw;
     a.C = L.C; a.H = L.H; a.W = L.W; a.R = L.R;
-    a.a_mode = g.a_mode; a.seg_sp = g.seg_sp;
+    a.a_mode = g.a_mode; a.seg_sp = g.seg_sp; a.seg_fast = g.seg_fast; a.seg_two = g.seg_two;
     a.kpad_bias = (L.K + 255) / 256 * 256;
     a.dbg_flags = getenv("WPK_DBG_FLAGS") ? atoi(getenv("WPK_DBG_FLAGS")) : 0;
     cudaStream_t st = (cudaStream_t)L.stream;

@@ -36,7 +36,8 @@ struct UmmaArgs {
     int *counters;                  // split-K arrival counters, one per output tile (self-resetting)
     const void *x;                  // A_MODE 2 gather source (the caller's activations)
     int x_nchw, C, H, W, R;
-    int a_mode, seg_sp;             // A_MODE 3: pixel-segment gather, filter columns padded to seg_sp
+    int a_mode, seg_sp, seg_fast;   // A_MODE 3: pixel-segment gather, filter columns padded to seg_sp
+    int seg_two;                    // A_MODE 3: shifted second image copy for odd stride_w
     int kpad_bias;                  // staged bias length (K rounded up to 256, zero-padded)
     int dbg_flags;                  // experiments only (WPK_DBG_FLAGS): 1 = gather zero-fills, 2 = no y stores
 };

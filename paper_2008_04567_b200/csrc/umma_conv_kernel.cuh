@@ -444,13 +444,15 @@ __device__ __forceinline__ void element_gather(const UmmaArgs &a, uint8_t *smA, 
     }
 }
 
-// A_MODE 3 producer: pixel-segment gather (C <= 4, x NHWC with 4 channels per pixel). K row =
-// (r, s', c), s' < Sp; a 16-byte smem chunk holds PPC whole pixels of one filter row, so every
-// chunk is PPC aligned 8/16-byte cp.async copies (zero-filled outside the image and for s' >= S /
-// r >= R). The copies of a stage are asynchronous: a thread keeps up to LAG stages in flight and
-// signals a stage full only after cp.async.wait_group + a proxy fence, so the global-load latency
-// overlaps across stages with no registers held. Thread t owns rows t and 128 + t of every stage.
-template <bool kTF32, int LAG>
+// A_MODE 3 producer: pixel-segment gather (C <= 4). x is re-laid as a zero-padded NHWC image
+// with 4 channels per pixel (a.H x a.W = padded size), so every tap is in bounds. K row =
+// (r, s', c), s' < Sp; a 16-byte smem chunk holds PPC whole pixels of one filter row. FAST: the
+// chunk is one aligned 16-byte cp.async (tf32; 16-bit with dil_w 1, rows of odd q*stride_w reading
+// a copy of the image shifted by one pixel); else two 8-byte copies. The copies of a stage
+// are asynchronous: a thread keeps up to LAG stages in flight and signals a stage full only after
+// cp.async.wait_group + a proxy fence, so the load latency overlaps across stages with no
+// registers held. Thread t owns rows t and 128 + t of every stage.
+template <bool kTF32, bool FAST, int LAG>
 __device__ __forceinline__ void segment_gather(const UmmaArgs &a, uint8_t *smA, uint32_t a_bytes, uint64_t *full,
                                                uint64_t *empty, int nsub, long long wstart, long long wstep, int t,
                                                int lane) {
@@ -459,64 +461,65 @@ __device__ __forceinline__ void segment_gather(const UmmaArgs &a, uint8_t *smA, 
     const int chunks_per_r = a.seg_sp / PPC;
     const int rstep = a.dil_h * a.W * PB;              // bytes between filter rows
     const int sstep = a.dil_w * PB;                    // bytes between filter columns
+    const long long img_bytes = (long long)a.M / a.PQ * a.H * a.W * PB;   // N * Hp * Wp pixels
     const char *xb = static_cast<const char *>(a.x);
+    const uint32_t swz = (uint32_t)(t & 7) << 4;       // rows t and 128 + t share the swizzle phase
     uint32_t stage = 0, phase = 0;
     uint32_t pend[LAG];                                // stages issued but not yet signalled (FIFO)
     int npend = 0;
     for (long long w = wstart; w < a.work; w += wstep) {
         const WorkPos wp = decode_work(w, a);
-        // per row: byte offset of tap (0,0) and validity bitmasks over filter rows / columns
-        long long roff[2];
-        uint32_t rmask[2], smask[2];
+        // per row: pointer to tap (0,0) in the padded image (nullptr: row past M, zero-filled)
+        const char *rptr[2];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
-            roff[hh] = 0; rmask[hh] = 0u; smask[hh] = 0u;
+            rptr[hh] = nullptr;
             const long long m = (long long)wp.mt * a.bm + hh * 128 + t;
-            if (hh < nsub && m < a.M) {
+            if (hh < nsub && m < a.M && !(a.dbg_flags & 1)) {
                 const int n = (int)(m / a.PQ);
                 const int rem = (int)(m - (long long)n * a.PQ);
                 const int p = rem / a.Q, q = rem - (rem / a.Q) * a.Q;
-                const int h0 = p * a.stride_h - a.pad_h, w0 = q * a.stride_w - a.pad_w;
-                roff[hh] = (((long long)n * a.H + h0) * a.W + w0) * PB;
-                for (int r = 0; r < a.R; ++r) {
-                    const int hi = h0 + r * a.dil_h;
-                    if (hi >= 0 && hi < a.H) rmask[hh] |= 1u << r;
-                }
-                for (int c = 0; c < a.S; ++c) {
-                    const int wi = w0 + c * a.dil_w;
-                    if (wi >= 0 && wi < a.W) smask[hh] |= 1u << c;
-                }
+                const int col = q * a.stride_w;
+                const int sh = (a.seg_two && (col & 1)) ? 1 : 0;   // shifted copy keeps chunks aligned
+                rptr[hh] = xb + sh * img_bytes + (((long long)n * a.H + p * a.stride_h) * a.W + col + sh) * PB;
             }
         }
         const int kb0 = wp.split * a.kb_per_split;
         const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
-            ptx::mbar_wait(&empty[stage], phase ^ 1);
-            const int cj = kb * 8;
-            const int r0 = cj / chunks_per_r, s00 = (cj - r0 * chunks_per_r) * PPC;
-#pragma unroll 1
-            for (int hh = 0; hh < nsub; ++hh) {
-                const int row = hh * 128 + t;
-                const uint32_t rbase = ptx::smem_u32(smA + stage * a_bytes) + (uint32_t)(row >> 3) * 1024u +
-                                       (uint32_t)(row & 7) * 128u;
-                const long long ro = hh ? roff[1] : roff[0];
-                const uint32_t rmk = hh ? rmask[1] : rmask[0], smk = hh ? smask[1] : smask[0];
-                int r = r0, s0 = s00;
+            // chunk offsets of this K block (uniform over rows); bit j of vmask: chunk j is a real tap
+            int off[8];
+            uint32_t vmask = 0;
+            {
+                const int cj = kb * 8;
+                int r = cj / chunks_per_r, s0 = (cj - r * chunks_per_r) * PPC;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const char *src = xb + ro + (long long)(r * rstep + s0 * sstep);
-                    // bit e: pixel s0 + e valid (r >= R or s >= S: mask bit 0)
-                    uint32_t ok = (0u - ((rmk >> r) & 1u)) & (smk >> s0);
-                    if (a.dbg_flags & 1) ok = 0u;
-                    const uint32_t dst = rbase + ((uint32_t)(j ^ (row & 7)) << 4);
-                    if constexpr (PPC == 1) {
-                        ptx::cp_async_16(dst, (ok & 1u) ? src : xb, (ok & 1u) ? 16u : 0u);
-                    } else {
-                        ptx::cp_async_8(dst, (ok & 1u) ? src : xb, (ok & 1u) ? 8u : 0u);
-                        ptx::cp_async_8(dst + 8, (ok & 2u) ? src + sstep : xb, (ok & 2u) ? 8u : 0u);
-                    }
+                    off[j] = r * rstep + s0 * sstep;
+                    if (r < a.R) vmask |= 1u << j;
                     s0 += PPC;
                     if (s0 == a.seg_sp) { s0 = 0; ++r; }
+                }
+            }
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            const uint32_t sbase = ptx::smem_u32(smA + stage * a_bytes) + (uint32_t)(t >> 3) * 1024u +
+                                   (uint32_t)(t & 7) * 128u;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                if (hh >= nsub) break;
+                const uint32_t rbase = sbase + (uint32_t)hh * 16384u;     // row 128 + t: 16 atoms further
+                const char *rp = rptr[hh];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const bool ok = rp != nullptr && ((vmask >> j) & 1u);
+                    const char *src = ok ? rp + off[j] : xb;
+                    const uint32_t dst = rbase + (((uint32_t)j << 4) ^ swz);
+                    if constexpr (FAST) {
+                        ptx::cp_async_16(dst, src, ok ? 16u : 0u);
+                    } else {
+                        ptx::cp_async_8(dst, src, ok ? 8u : 0u);
+                        ptx::cp_async_8(dst + 8, ok ? src + sstep : xb, ok ? 8u : 0u);
+                    }
                 }
             }
             ptx::cp_async_commit();
@@ -685,7 +688,21 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
         const int t = threadIdx.x - 384;                       // 0..127
         asm volatile("griddepcontrol.wait;" ::: "memory");
         if constexpr (AK == AK_SEG) {
-            segment_gather<kTF32, 2>(a, smA, a_bytes, full, empty, nsub, wstart, wstep, t, lane);   // STAGES >= 3
+            // LAG = STAGES - 1 stages of copies in flight per thread
+#define WPK_SEG(L)                                                                                          \
+    do {                                                                                                  \
+        if (a.seg_fast) segment_gather<kTF32, true, L>(a, smA, a_bytes, full, empty, nsub, wstart, wstep, t, lane); \
+        else segment_gather<kTF32, false, L>(a, smA, a_bytes, full, empty, nsub, wstart, wstep, t, lane);        \
+    } while (0)
+            switch (a.stages) {
+                case 3: WPK_SEG(2); break;
+                case 4: WPK_SEG(3); break;
+                case 5: WPK_SEG(4); break;
+                case 6: WPK_SEG(5); break;
+                case 7: WPK_SEG(6); break;
+                default: WPK_SEG(7); break;
+            }
+#undef WPK_SEG
         } else if constexpr (AK == AK_GATHER) {
             element_gather<kTF32>(a, smA, a_bytes, full, empty, nsub, wstart, wstep, t, lane);
         }

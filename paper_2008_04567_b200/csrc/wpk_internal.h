@@ -67,6 +67,9 @@ struct UmmaGeom {
     int a_mode;         // 0: TMA im2col (or tiled for 1x1), 1: explicit im2col matrix in the workspace,
                         // 2: element gather into smem, 3: pixel-segment gather (C <= 4)
     int seg_sp;         // A_MODE 3: filter columns per row padded to whole 16-byte chunks
+    int seg_hp, seg_wp; // A_MODE 3: zero-padded image height / width (pixels of 4 channels)
+    int seg_fast;       // A_MODE 3: every 16-byte chunk is one aligned copy (tf32, or 16-bit with dil_w 1)
+    int seg_two;        // A_MODE 3: a second, one-pixel-shifted image copy (16-bit, odd stride_w)
     int a_tiled;        // 1: A fetched by a plain 2-D TMA tile load (1x1, stride 1, pad 0), else im2col
     int epi_bufs;       // staging buffers per epilogue warp (2 = double-buffered TMA stores)
     int epi_tma;        // 1: epilogue stages 32x128-byte tiles in smem and TMA-stores them
