@@ -164,6 +164,13 @@ WPK_API wpk_status wpk_conv2d_run(wpk_plan plan, const void *x, const void *w, c
 WPK_API wpk_status wpk_conv2d_run_host(wpk_plan plan, const void *x_host, const void *w, const void *b,
                                void *y_host, void *stream);
 
+/* Same as run_host without the final synchronisation: the H2D copy, the kernels and the D2H copy
+ * are only enqueued on `stream`; y_host is valid after the caller synchronises that stream (x_host
+ * must stay untouched until then). Pinned host memory makes the copies asynchronous, so plans on
+ * different streams overlap their copies with each other's kernels. */
+WPK_API wpk_status wpk_conv2d_run_host_async(wpk_plan plan, const void *x_host, const void *w, const void *b,
+                                             void *y_host, void *stream);
+
 WPK_API void wpk_conv2d_destroy(wpk_plan plan);
 WPK_API const char *wpk_last_error(void);
 

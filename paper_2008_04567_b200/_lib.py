@@ -93,6 +93,7 @@ def load():
         "wpk_conv2d_tune": (I32, [P, I32, I32, ctypes.POINTER(TuneOptions)]),
         "wpk_conv2d_run": (I32, [P, P, P, P, P, P]),
         "wpk_conv2d_run_host": (I32, [P, P, P, P, P, P]),
+        "wpk_conv2d_run_host_async": (I32, [P, P, P, P, P, P]),
         "wpk_conv2d_destroy": (None, [P]),
         "wpk_last_error": (ctypes.c_char_p, []),
         "wpk_conv2d_workspace_size": (I32, [P, ctypes.POINTER(ctypes.c_size_t)]),

@@ -129,6 +129,17 @@ class Conv2dPlan:
                                              ctypes.c_void_p(y_host.data_ptr()), ctypes.c_void_p(s)))
         return y_host
 
+    def run_host_async(self, x_host: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, y_host: torch.Tensor,
+                       stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """run_host without the final stream sync: y_host is valid after the stream is synchronised."""
+        self._ensure_workspace()
+        s = (stream or torch.cuda.current_stream(w.device)).cuda_stream
+        bp = ctypes.c_void_p(b.data_ptr()) if b is not None else None
+        L.check(self.lib.wpk_conv2d_run_host_async(self.handle, ctypes.c_void_p(x_host.data_ptr()),
+                                                   ctypes.c_void_p(w.data_ptr()), bp,
+                                                   ctypes.c_void_p(y_host.data_ptr()), ctypes.c_void_p(s)))
+        return y_host
+
     def last_launch_count(self) -> int:
         return int(self.lib.wpk_conv2d_last_launch_count(self.handle))
 

@@ -577,8 +577,21 @@ wpk_status wpk_conv2d_run(wpk_plan plan, const void *x, const void *w, const voi
     return WPK_OK;
 }
 
+static wpk_status run_host_impl(wpk_plan plan, const void *x_host, const void *w, const void *b, void *y_host,
+                                void *stream, bool sync);
+
 wpk_status wpk_conv2d_run_host(wpk_plan plan, const void *x_host, const void *w, const void *b, void *y_host,
                                void *stream) {
+    return run_host_impl(plan, x_host, w, b, y_host, stream, true);
+}
+
+wpk_status wpk_conv2d_run_host_async(wpk_plan plan, const void *x_host, const void *w, const void *b, void *y_host,
+                                     void *stream) {
+    return run_host_impl(plan, x_host, w, b, y_host, stream, false);
+}
+
+static wpk_status run_host_impl(wpk_plan plan, const void *x_host, const void *w, const void *b, void *y_host,
+                                void *stream, bool sync) {
     if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
     Plan *p = reinterpret_cast<Plan *>(plan);
     if (!x_host || !y_host || !w) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL pointer");
@@ -598,7 +611,7 @@ wpk_status wpk_conv2d_run_host(wpk_plan plan, const void *x_host, const void *w,
     if (n < 0) return WPK_ERR_CUDA;
     p->last_launches = n;
     if (cudaMemcpyAsync(y_host, ws + L.hy_off, yb, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess) {
+        (sync && cudaStreamSynchronize(s) != cudaSuccess)) {
         cudaError_t e = cudaGetLastError();
         return fail(WPK_ERR_CUDA, std::string("D2H copy / sync failed: ") + cudaGetErrorString(e));
     }

@@ -749,6 +749,10 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 else ptx::umma_commit(&tfull[acc]);                               // accumulator ready
                 if (dbg && w == wstart) dbg[3] = ptx::globaltimer();
                 if (dbg && dit < 8) dbg[16 + dit * 6 + 2] = ptx::globaltimer();
+                if (dbg && dit < 8 && (a.dbg_flags & 4)) {   // experiment: MMA completion seen by a spinning thread
+                    while (!ptx::mbar_test_wait(&tfull[acc], acc_phase)) {}
+                    dbg[16 + dit * 6 + 5] = ptx::globaltimer();
+                }
                 if (++acc == (uint32_t)a.acc_stages) { acc = 0; acc_phase ^= 1; }
             }
         }

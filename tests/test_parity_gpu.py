@@ -199,6 +199,12 @@ def test_run_host_matches_device():
     yd = plan.run(xl.cuda(), wl.cuda(), b.cuda())
     torch.cuda.synchronize()
     assert torch.equal(yh, yd.cpu())
+    # the async variant on a side stream: valid after that stream is synchronised
+    ya = torch.zeros_like(yh).pin_memory()
+    st = torch.cuda.Stream()
+    plan.run_host_async(xl.pin_memory(), wl.cuda(), b.cuda(), ya, stream=st)
+    st.synchronize()
+    assert torch.equal(ya, yh)
 
 
 @pytest.mark.parametrize("layout", ["nchw", "nhwc"])

@@ -20,6 +20,9 @@ y = torch.empty(plan.y_shape(), dtype=xd.dtype, device="cuda")
 fl = 2 * L.n * L.k * plan.p * plan.q * (L.c // L.groups) * L.r * L.s
 if len(sys.argv) > 2 and sys.argv[2] == "grid":
     cfgs = [list(c) for c in itertools.product([64, 128, 256], [3, 4, 6], [1], [0, 1], [0], [1, 2], [128, 256])]
+elif len(sys.argv) > 2 and sys.argv[2] == "grid2":   # wider: pairs, 4 accumulators, split-K
+    cfgs = [list(c) for c in itertools.product([64, 128, 192, 256], [3, 4, 6], [1, 2], [0, 1, 2, 3], [0],
+                                               [1, 2, 4], [128, 256])]
 elif len(sys.argv) > 2:
     vals = [int(v) for v in sys.argv[2:]]
     cfgs = [vals[i:i + 7] for i in range(0, len(vals), 7)]

@@ -17,7 +17,7 @@ if len(sys.argv) > 2:
 x, w, b = workloads.generate(L, "bf16", "uniform", seed=1)
 xd = x.permute(0, 2, 3, 1).contiguous().cuda(); wd = w.permute(0, 2, 3, 1).contiguous().cuda(); bd = b.cuda()
 y = torch.empty(plan.y_shape(), dtype=xd.dtype, device="cuda")
-dbg = torch.zeros(148 * 192, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(148 * 64, dtype=torch.int64, device="cuda")
 lib = _lib.load()
 lib.wpk_debug_set_timeline.argtypes = [ctypes.c_void_p]
 for i in range(3):
@@ -29,8 +29,7 @@ torch.sum(flush.view(torch.int32), dtype=torch.int64)
 plan.run(xd, wd, bd, y)
 torch.cuda.synchronize()
 lib.wpk_debug_set_timeline(None)
-t192 = dbg.view(148, 192).cpu().numpy().astype(np.float64)
-t64 = t192[:, :64]
+t64 = dbg.view(148, 64).cpu().numpy().astype(np.float64)
 t = t64[:, :16]
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
@@ -42,17 +41,11 @@ for i, n in enumerate(names):
     col = col[col > -1e6]
     print(f"  {n:14s} min {col.min():8.2f}  median {np.median(col):8.2f}  max {col.max():8.2f} us")
 ev = t64[t64[:, 0] > 0][:, 16:64].reshape(-1, 8, 6)
-print("  per-tile events of CTA 0 (us): tempty_ok, 1st_full, mma_commit, epi_tfull_ok, epi_done")
+print("  per-tile events of CTA 0 (us): tempty_ok, 1st_full, mma_commit, epi_tfull_ok, epi_done, [mma_seen_done]")
 for it in range(8):
-    row = ev[0, it, :5]
+    row = ev[0, it, :6] if ev[0, it, 5] > 0 else ev[0, it, :5]
     if row[0] > 0:
         print("   tile", it, np.round((row - t0) / 1000.0, 2))
-ce = t192[0]
-print("  CTA 0 clock64 deltas (cycles). MMA: tempty->1st_full, ->mmas_issued, ->commit | EPI: tfull->ld_done, ->sts, ->fence, ->store, ->end")
-for it in range(8):
-    m = ce[128 + it * 4: 132 + it * 4]; e = ce[64 + it * 8: 70 + it * 8]
-    if m[0] > 0:
-        print("   tile", it, np.diff(m).astype(int).tolist(), "|", np.diff(e).astype(int).tolist(), " epi_start - mma_commit:", int(e[0] - m[3]))
 fx = t[:, 8:14]
 if os.environ.get("SPLITK_FIX") and (fx[:, 0] > 0).any():
     sel = fx[:, 0] > 0
