@@ -288,10 +288,14 @@ Config default_config(const ConvDesc &d, int family) {
     c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c <= 4) ? 3 : (d.c < 16) ? 1 : 0;
     c.genes[5] = 2; c.genes[6] = 128;
     if (big) { c.genes[3] = 2; c.genes[6] = 256; }
+    // small-C layers (pixel-segment gather): many short tiles -> 256-row tiles, and few stages
+    // (the gather keeps STAGES-1 of them in flight; more only costs shared memory)
+    const bool seg = d.c <= 4 && c.genes[4] == 3;
+    if (seg && d.M() >= 256LL * 148) c.genes[6] = 256;
     for (int am : {c.genes[4], 2, 0}) {   // small C: explicit im2col, else the gather producer
         c.genes[4] = am;
         bool ok = false;
-        for (int st = 8; st >= 2 && !ok; --st) {
+        for (int st = (seg && am == 3) ? 4 : 8; st >= 2 && !ok; --st) {
             c.genes[1] = st;
             ok = config_valid(d, c, nullptr);
         }
