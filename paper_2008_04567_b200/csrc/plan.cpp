@@ -204,6 +204,23 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     size_t off = (size_t)g->stages * stage;
     g->epi_off = off;
     if (g->epi_tma) off += (size_t)8 * g->epi_bufs * 4096;
+    // Split-K inside a thread-block cluster (DSMEM reduction): the S splits of a tile are the S CTAs
+    // of one cluster, each CTA owns BN/S output columns and receives the others' fp32 partials of
+    // them into its (by then idle) pipeline stages. Needs one tile per CTA (grid = work), whole
+    // 128-byte output chunks per owner, and the receive area within the stage buffers.
+    g->csplit = 0;
+    g->recv_stride = 0;
+    if (g->splits > 1 && g->splits <= 8 && (g->splits & (g->splits - 1)) == 0 && !g->pair && g->a_mode == 0 &&
+        g->epi_tma && !getenv("WPK_NO_CSPLIT")) {
+        const int slice = g->bn / g->splits;
+        const size_t rstride = (size_t)slice * 4 + 16;
+        const size_t recv = (size_t)(g->splits - 1) * g->bm * rstride;
+        // (one wave only: with one tile per CTA, later waves would pay the whole prologue again)
+        if (g->bn % (g->splits * cw) == 0 && recv <= (size_t)g->stages * stage && g->work <= device_sm_count(0)) {
+            g->csplit = 1;
+            g->recv_stride = (int)rstride;
+        }
+    }
     g->bias_off = off;
     off += bias_bytes;
     g->bar_off = off;

@@ -322,7 +322,7 @@ static WsLayout ws_layout(const ConvDesc &d, const Config &cfg, bool host_stagin
             L.x_off = off; L.x_bytes = al256((size_t)d.n * d.h * d.w * g.cpad * e); off += L.x_bytes;
             L.w_off = off; L.w_bytes = al256((size_t)d.k * d.r * d.s * g.cpad * e); off += L.w_bytes;
         }
-        if (g.splits > 1) {
+        if (g.splits > 1 && !g.csplit) {
             L.p_off = off; L.p_bytes = al256((size_t)g.splits * d.M() * d.k * 4); off += L.p_bytes;
             L.c_off = off; L.c_bytes = al256((size_t)g.m_tiles * g.n_tiles * (g.pair ? 2 : 1) * 4); off += L.c_bytes;
         }
@@ -465,8 +465,8 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     if (ce != cudaSuccess) { set_error(std::string("aux kernel launch: ") + cudaGetErrorString(ce)); return -1; }
     UmmaLaunch U{};
     U.dtype = d.dtype; U.x = xk; U.w = wk; U.b = b; U.y = y;
-    U.partial = (g.splits > 1) ? reinterpret_cast<float *>(ws + L.p_off) : nullptr;
-    if (g.splits > 1) {
+    U.partial = (g.splits > 1 && !g.csplit) ? reinterpret_cast<float *>(ws + L.p_off) : nullptr;
+    if (g.splits > 1 && !g.csplit) {
         // counters are self-resetting; zero them once per (workspace, layout) they live at
         char *cptr = ws + L.c_off;
         if (p.counters_at != cptr || p.counters_bytes != L.c_bytes) {

@@ -184,11 +184,13 @@ launch:
     a.C = L.C; a.H = L.H; a.W = L.W; a.R = L.R;
     a.a_mode = g.a_mode; a.seg_sp = g.seg_sp; a.seg_fast = g.seg_fast; a.seg_two = g.seg_two;
     a.kpad_bias = (L.K + 255) / 256 * 256;
+    a.recv_stride = g.recv_stride;
     a.dbg_flags = getenv("WPK_DBG_FLAGS") ? atoi(getenv("WPK_DBG_FLAGS")) : 0;
     cudaStream_t st = (cudaStream_t)L.stream;
     long long grid = (long long)L.sm_count * g.ctas_per_sm;
     if (grid > g.work) grid = g.work;
     if (g.pair) grid = 2 * std::min<long long>(g.work, L.sm_count / 2);
+    if (g.csplit) grid = g.work;   // one (tile, split) per CTA; clusters of SPLIT_K CTAs
     int launches = 0;
     cudaError_t ce = cudaSuccess;
     cudaLaunchConfig_t lc{};
@@ -203,9 +205,9 @@ launch:
         attr[nattr].val.programmaticStreamSerializationAllowed = 1;
         ++nattr;
     }
-    if (g.pair) {   // the two CTAs of a tcgen05 CTA pair form a cluster
+    if (g.pair || g.csplit) {   // the two CTAs of a tcgen05 CTA pair / the splits of a tile form a cluster
         attr[nattr].id = cudaLaunchAttributeClusterDimension;
-        attr[nattr].val.clusterDim.x = 2;
+        attr[nattr].val.clusterDim.x = g.pair ? 2 : g.splits;
         attr[nattr].val.clusterDim.y = 1;
         attr[nattr].val.clusterDim.z = 1;
         ++nattr;
@@ -213,7 +215,7 @@ launch:
     lc.attrs = attr;
     lc.numAttrs = nattr;
     const int ak = g.a_mode == 3 ? AK_SEG : g.a_mode == 2 ? AK_GATHER : g.pair ? AK_PAIR : AK_TMA;
-    const int ek = !g.epi_tma ? EK_DIRECT : g.splits > 1 ? EK_SPLIT : EK_TMA;
+    const int ek = !g.epi_tma ? EK_DIRECT : g.csplit ? EK_CSPLIT : g.splits > 1 ? EK_SPLIT : EK_TMA;
     if (dt == DT_F16) ce = umma_launch_f16(ak, ek, lc, tmA, tmB, tmY, tmP, a);
     else if (dt == DT_BF16) ce = umma_launch_bf16(ak, ek, lc, tmA, tmB, tmY, tmP, a);
     else ce = umma_launch_tf32(ak, ek, lc, tmA, tmB, tmY, tmP, a);

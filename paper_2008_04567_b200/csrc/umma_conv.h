@@ -16,7 +16,7 @@ enum { DT_F16 = 0, DT_BF16 = 1, DT_TF32 = 2 };
 enum { AK_TMA = 0, AK_PAIR = 1, AK_GATHER = 2, AK_SEG = 3 };
 // epilogue kinds: final output via TMA store, split-K partials via TMA store (+ in-kernel fixup),
 // direct global stores (NCHW output or K not a multiple of the 128-byte chunk; final or partial)
-enum { EK_TMA = 0, EK_SPLIT = 1, EK_DIRECT = 2 };
+enum { EK_TMA = 0, EK_SPLIT = 1, EK_DIRECT = 2, EK_CSPLIT = 3 };   // EK_CSPLIT: split-K over a cluster (DSMEM)
 
 struct UmmaArgs {
     const void *bias;
@@ -39,6 +39,7 @@ struct UmmaArgs {
     int a_mode, seg_sp, seg_fast;   // A_MODE 3: pixel-segment gather, filter columns padded to seg_sp
     int seg_two;                    // A_MODE 3: shifted second image copy for odd stride_w
     int kpad_bias;                  // staged bias length (K rounded up to 256, zero-padded)
+    int recv_stride;                // EK_CSPLIT: bytes per received partial row
     int dbg_flags;                  // experiments only (WPK_DBG_FLAGS): 1 = gather zero-fills, 2 = no y stores
 };
 

@@ -210,6 +210,59 @@ __device__ __forceinline__ void epi_chunk_owner(EpiCtx &E, const UmmaArgs &a, co
     stage_and_store<true>(E, a, tmY, pk, k0, mrow, 0);
 }
 
+// Cluster split-K owner chunk: columns [k0, k0 + 128 B) of this CTA's output slice; the other
+// splits' fp32 partials of them were delivered into this CTA's shared memory (recv_row = this
+// lane's row in source slot 0 at the chunk's first column, slot_bytes apart). Summed in split
+// order 0..S-1 (this CTA's own TMEM accumulator at position q) -> deterministic; then bias, ReLU,
+// one rounding, TMA store.
+template <typename T>
+__device__ __forceinline__ void epi_chunk_csplit(EpiCtx &E, const UmmaArgs &a, const CUtensorMap *tmY, uint32_t taddr,
+                                                 int k0, int mrow, uint32_t recv_row, uint32_t slot_bytes, int q,
+                                                 int S) {
+    constexpr int CW = 128 / sizeof(T);
+    uint32_t pk[32];
+#pragma unroll
+    for (int half = 0; half < CW / 32; ++half) {
+        uint32_t raw[32];
+        ptx::tmem_ld32_nowait(taddr + half * 32, raw);
+        ptx::tmem_wait_ld();
+        float acc[32];
+        for (int rk = 0; rk < S; ++rk) {
+            float v[32];
+            if (rk == q) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
+            } else {
+                const uint32_t src = recv_row + (uint32_t)(rk < q ? rk : rk - 1) * slot_bytes + half * 128;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    uint32_t x0, x1, x2, x3;
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                                 : "r"(src + j * 16));
+                    v[4 * j] = __uint_as_float(x0); v[4 * j + 1] = __uint_as_float(x1);
+                    v[4 * j + 2] = __uint_as_float(x2); v[4 * j + 3] = __uint_as_float(x3);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[j] = (rk == 0) ? v[j] : acc[j] + v[j];
+        }
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) {
+            float v[4] = {acc[4 * qq], acc[4 * qq + 1], acc[4 * qq + 2], acc[4 * qq + 3]};
+            bias_relu4(v, E.sBias, k0 + half * 32 + 4 * qq, a.epilogue == 2);
+            if constexpr (sizeof(T) == 2) {
+                pk[half * 16 + 2 * qq] = pack2(v[0], v[1], (T *)nullptr);
+                pk[half * 16 + 2 * qq + 1] = pack2(v[2], v[3], (T *)nullptr);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) pk[4 * qq + j] = __float_as_uint(v[j]);
+            }
+        }
+    }
+    stage_and_store<true>(E, a, tmY, pk, k0, mrow, 0);
+}
+
 // Direct-store epilogue for one 32-row x 16-column chunk (NCHW output, unaligned K, partials).
 template <typename T>
 __device__ __noinline__ void epi_chunk_direct(const UmmaArgs &a, const float *sBias, uint32_t taddr, int k0,
@@ -578,6 +631,8 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
     uint64_t *tempty = bars + 20;     // [4]
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bars + 24);
     volatile int *sFlag = reinterpret_cast<volatile int *>(bars + 25);
+    uint64_t *freeb = bars + 26;      // EK_CSPLIT: every peer's stages are idle (S - 1 remote arrives)
+    uint64_t *datab = bars + 27;      // EK_CSPLIT: every peer delivered its partials (8 (S - 1) arrives)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long *dbg = a.dbg ? a.dbg + blockIdx.x * 64 : nullptr;
@@ -595,6 +650,10 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
         for (int s = 0; s < a.acc_stages; ++s) {
             ptx::mbar_init(&tfull[s], 1);
             ptx::mbar_init(&tempty[s], kPair ? 16 : 8);   // 8 epilogue warps (x2 CTAs for a pair)
+        }
+        if (EK == EK_CSPLIT) {
+            ptx::mbar_init(freeb, a.splits - 1);
+            ptx::mbar_init(datab, 8 * (a.splits - 1));
         }
         ptx::fence_mbar_init();
     }
@@ -620,7 +679,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     ptx::tc_fence_before();
     __syncthreads();
-    if (kPair) ptx::cluster_sync();   // peer barriers initialised before any remote arrive / TMA
+    if (kPair || EK == EK_CSPLIT) ptx::cluster_sync();   // peer barriers initialised before remote arrives / TMA
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     if (dbg && threadIdx.x == 0) dbg[1] = ptx::globaltimer();
@@ -786,6 +845,63 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             }
             const int cw = owner ? cwf : cwp;
             const int nchunks = (a.bn + cw - 1) / cw;
+            if constexpr (EK == EK_CSPLIT) {
+                // ---- split-K over the cluster: the S splits of this tile are the S CTAs; CTA q owns
+                // output columns [q*BN/S, (q+1)*BN/S) and receives the others' partials of them into
+                // its own (idle after the last MMA) pipeline stages.
+                const int S = a.splits;
+                const int q = (int)ptx::cluster_ctarank();
+                const int slice = a.bn / S;
+                const uint32_t slot_bytes = (uint32_t)a.bm * (uint32_t)a.recv_stride;
+                const uint32_t recv0 = ptx::smem_u32(smem);
+                if (warp == 4 && lane == 0)                     // (1) our stages are free
+                    for (int j = 0; j < S; ++j)
+                        if (j != q) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(freeb), (uint32_t)j));
+                ptx::mbar_wait_cluster(freeb, 0);               // (2) every peer's stages are free
+                // (3) send: our accumulator columns of the other slices, 32 at a time, into slot
+                // (q < j ? q : q - 1) of destination j
+                const int sends = (S - 1) * (slice / 32);
+                for (int h = 0; h < nsub; ++h) {
+                    if (nsub == 2 && h != grp) continue;
+                    const int row = h * 128 + quarter * 32 + lane;
+                    const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * acc_cols + h * a.bn;
+                    for (int ci = (nsub == 2 ? 0 : grp); ci < sends; ci += (nsub == 2 ? 1 : 2)) {
+                        const int jd = ci / (slice / 32);
+                        const int j = jd < q ? jd : jd + 1;                   // destination rank
+                        const int cl = (ci - jd * (slice / 32)) * 32;         // column within its slice
+                        uint32_t raw[32];
+                        ptx::tmem_ld32_nowait(tbase + j * slice + cl, raw);
+                        ptx::tmem_wait_ld();
+                        const uint32_t dst = ptx::mapa(recv0 + (uint32_t)(q < j ? q : q - 1) * slot_bytes +
+                                                           (uint32_t)row * a.recv_stride + (uint32_t)cl * 4u,
+                                                       (uint32_t)j);
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            ptx::st_cluster_v4(dst + x * 16, raw[4 * x], raw[4 * x + 1], raw[4 * x + 2], raw[4 * x + 3]);
+                    }
+                }
+                ptx::fence_acq_rel_cluster();
+                __syncwarp();
+                if (lane == 0)
+                    for (int j = 0; j < S; ++j)
+                        if (j != q) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(datab), (uint32_t)j));
+                ptx::mbar_wait_cluster(datab, 0);               // (4) all partials of our slice arrived
+                // (5) reduce our slice in 128-byte output chunks
+                const int own_chunks = slice / cwf;
+                for (int h = 0; h < nsub; ++h) {
+                    if (nsub == 2 && h != grp) continue;
+                    const int row = h * 128 + quarter * 32 + lane;
+                    const int mrow = wp.mt * a.bm + h * 128 + quarter * 32;
+                    const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * acc_cols + h * a.bn;
+                    for (int ci = (nsub == 2 ? 0 : grp); ci < own_chunks; ci += (nsub == 2 ? 1 : 2)) {
+                        const int cl = ci * cwf;
+                        const int k0 = n0 + q * slice + cl;
+                        if (k0 >= a.K) break;
+                        epi_chunk_csplit<T>(E, a, &tmY, tbase + q * slice + cl, k0, mrow,
+                                            recv0 + (uint32_t)row * a.recv_stride + (uint32_t)cl * 4u, slot_bytes, q, S);
+                    }
+                }
+            } else
             // slabs = (h, chunk) pairs; group g takes h == g when nsub == 2, else every other chunk
             for (int h = 0; h < nsub; ++h) {
                 if (nsub == 2 && h != grp) continue;
@@ -864,6 +980,10 @@ static cudaError_t launch_ak(int ek, cudaLaunchConfig_t &lc, const CUtensorMap &
                              const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
     if (ek == EK_TMA) return launch_variant<DT, AK, EK_TMA>(lc, tmA, tmB, tmY, tmP, a);
     if (ek == EK_SPLIT) return launch_variant<DT, AK, EK_SPLIT>(lc, tmA, tmB, tmY, tmP, a);
+    if (ek == EK_CSPLIT) {
+        if constexpr (AK == AK_TMA) return launch_variant<DT, AK, EK_CSPLIT>(lc, tmA, tmB, tmY, tmP, a);
+        else return cudaErrorInvalidConfiguration;   // plan validation never pairs these
+    }
     return launch_variant<DT, AK, EK_DIRECT>(lc, tmA, tmB, tmY, tmP, a);
 }
 

@@ -73,6 +73,8 @@ struct UmmaGeom {
     int a_tiled;        // 1: A fetched by a plain 2-D TMA tile load (1x1, stride 1, pad 0), else im2col
     int epi_bufs;       // staging buffers per epilogue warp (2 = double-buffered TMA stores)
     int epi_tma;        // 1: epilogue stages 32x128-byte tiles in smem and TMA-stores them
+    int csplit;         // 1: split-K reduced inside a cluster of SPLIT_K CTAs through DSMEM
+    int recv_stride;    // csplit: bytes per received partial row (BN/S fp32 + 16 B pad)
     size_t smem_bytes;
     size_t epi_off, bias_off, bar_off;   // byte offsets of the epilogue staging, bias, barriers
     int tmem_cols;
