@@ -159,7 +159,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="wpk", choices=["wpk", "reference"])
     ap.add_argument("--batch", type=int, default=32, help="images per GPU")
-    ap.add_argument("--tune-budget", type=int, default=48, help="distinct configs measured per unique layer")
+    ap.add_argument("--tune-budget", type=int, default=64, help="distinct configs measured per unique layer")
+    ap.add_argument("--ga-pop", type=int, default=12,
+                    help="GA population (profiles/r1c_search_compare.md: with the paper's 48 a budget of 48 is "
+                         "one random generation; 12 gives ~5 generations at budget 64)")
     ap.add_argument("--search", default="ga", choices=["ga", "rl", "random", "none"])
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -207,6 +210,8 @@ def main():
             plan.set_config(fam, genes)
         elif args.search != "none" and args.tune_budget > 0:
             ex = wdist.make_exchange(pg) if world > 1 else {}
+            if args.search == "ga":   # population 12 -> several generations within the budget
+                ex.update(ga_pop=args.ga_pop, ga_pool=args.ga_pop, ga_elites=2)
             res = plan.tune(args.search, args.tune_budget, seed=i, rank=rank, world=world, **ex)
             tune_info.append({"layer": L.name, "best_us": res.best_us, "measured": res.measured,
                               "family": res.family, "genes": res.genes})

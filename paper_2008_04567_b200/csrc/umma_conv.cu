@@ -61,10 +61,13 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
         return -1;
     }
     const UmmaGeom &g = L.g;
+    // two A-issuing threads: measured no faster on the ResNet-50 layers, opt-in only
+    const int a_split = (g.a_mode <= 1 && getenv("WPK_ASPLIT")) ? 1 : 0;
+    const int a_box_rows = (g.pair ? 128 : g.bm) >> a_split;
     CUtensorMap tmA, tmB, tmY, tmP;
     UmmaMapCache *mc = L.cache;
     const bool hit = mc && mc->valid && mc->x == L.x && mc->w == L.w && mc->y == L.y && mc->partial == L.partial &&
-                     mc->cfg == L.cfg;
+                     mc->cfg == L.cfg && mc->a_split == a_split;
     if (hit) {
         tmA = mc->a;
         tmB = mc->b;
@@ -81,7 +84,7 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
     } else if (g.a_tiled) {
         cuuint64_t dims[2] = {(cuuint64_t)g.cpad, (cuuint64_t)L.a_rows};
         cuuint64_t strides[1] = {(cuuint64_t)g.cpad * e};
-        cuuint32_t box[2] = {(cuuint32_t)g.bk, (cuuint32_t)(g.pair ? 128 : g.bm)};
+        cuuint32_t box[2] = {(cuuint32_t)g.bk, (cuuint32_t)a_box_rows};
         cuuint32_t estr[2] = {1, 1};
         CUresult r = encode_tiled()(&tmA, tdt, 2, const_cast<void *>(L.x), dims, strides, box, estr,
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -98,7 +101,7 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
         int upper[2] = {L.pad_w - (L.S - 1) * L.dil_w, L.pad_h - (L.R - 1) * L.dil_h};
         cuuint32_t estr[4] = {1, (cuuint32_t)L.stride_w, (cuuint32_t)L.stride_h, 1};
         CUresult r = encode_im2col()(&tmA, tdt, 4, const_cast<void *>(L.x), dims, strides, lower, upper,
-                                     (cuuint32_t)g.bk, (cuuint32_t)(g.pair ? 128 : g.bm), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                     (cuuint32_t)g.bk, (cuuint32_t)a_box_rows, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
@@ -148,7 +151,7 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
         }
     }
     if (mc) {
-        mc->x = L.x; mc->w = L.w; mc->y = L.y; mc->partial = L.partial; mc->cfg = L.cfg;
+        mc->x = L.x; mc->w = L.w; mc->y = L.y; mc->partial = L.partial; mc->cfg = L.cfg; mc->a_split = a_split;
         mc->a = tmA; mc->b = tmB; mc->yy = tmY; mc->pp = tmP; mc->valid = true;
     }
 launch:
@@ -185,6 +188,7 @@ launch:
     a.a_mode = g.a_mode; a.seg_sp = g.seg_sp; a.seg_fast = g.seg_fast; a.seg_two = g.seg_two;
     a.kpad_bias = (L.K + 255) / 256 * 256;
     a.recv_stride = g.recv_stride;
+    a.a_split = a_split;
     a.dbg_flags = getenv("WPK_DBG_FLAGS") ? atoi(getenv("WPK_DBG_FLAGS")) : 0;
     cudaStream_t st = (cudaStream_t)L.stream;
     long long grid = (long long)L.sm_count * g.ctas_per_sm;

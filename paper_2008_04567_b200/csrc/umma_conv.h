@@ -40,6 +40,7 @@ struct UmmaArgs {
     int seg_two;                    // A_MODE 3: shifted second image copy for odd stride_w
     int kpad_bias;                  // staged bias length (K rounded up to 256, zero-padded)
     int recv_stride;                // EK_CSPLIT: bytes per received partial row
+    int a_split;                    // A stage loaded by two threads (two half-height boxes)
     int dbg_flags;                  // experiments only (WPK_DBG_FLAGS): 1 = gather zero-fills, 2 = no y stores
 };
 
@@ -50,6 +51,7 @@ struct UmmaMapCache {
     const void *x = nullptr, *w = nullptr;
     void *y = nullptr, *partial = nullptr;
     Config cfg;
+    int a_split = 0;
     CUtensorMap a, b, yy, pp;
 };
 

@@ -644,7 +644,8 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
         if (EK != EK_DIRECT) ptx::prefetch_tmap(&tmY);
         if (EK == EK_SPLIT) ptx::prefetch_tmap(&tmP);
         for (int s = 0; s < a.stages; ++s) {
-            ptx::mbar_init(&full[s], kGather ? 5 : 2);   // A (TMA, or 4 gather warps) + B producer
+            // A (TMA: 1 or 2 issuing threads; or 4 gather warps) + B producer
+            ptx::mbar_init(&full[s], kGather ? 5 : (a.a_split ? 3 : 2));
             ptx::mbar_init(&empty[s], 1);      // MMA commit
         }
         for (int s = 0; s < a.acc_stages; ++s) {
@@ -684,17 +685,23 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
     const uint32_t tmem_base = *tmem_holder;
     if (dbg && threadIdx.x == 0) dbg[1] = ptx::globaltimer();
 
-    if (warp == 0 || warp == 2) {
+    if (warp == 0 || warp == 2 || (warp == 3 && !kGather && a.a_split)) {
         // ===================== TMA producers: warp 0 -> A (activations), warp 2 -> B (weights) ====
+        // With a_split, warp 3 loads the second half of each A stage: one thread issues one TMA
+        // instruction per ~430 cycles whatever the box size (tools/tma_bench.cu), so two issuing
+        // threads double the A feed rate up to the SM's ~76 B/clk ingest.
         if (lane == 0 && !(kGather && warp == 0)) {
-            const bool isA = (warp == 0);
+            const bool isA = (warp != 2);
+            const int half = (warp == 3) ? 1 : 0;
             if (isA) asm volatile("griddepcontrol.wait;" ::: "memory");
             uint32_t stage = 0, phase = 0;
-            const uint32_t tx = isA ? a_bytes : b_bytes;
-            uint8_t *dst0 = isA ? smA : smB;
+            const uint32_t a_rows = (kPair ? 128u : (uint32_t)a.bm) >> (a.a_split ? 1 : 0);   // rows per A load
+            const uint32_t tx = isA ? a_rows * 128u : b_bytes;
+            const uint32_t sstride = isA ? a_bytes : b_bytes;
+            uint8_t *dst0 = isA ? smA + (size_t)half * a_rows * 128u : smB;
             for (long long w = wstart; w < a.work; w += wstep) {
                 const WorkPos wp = decode_work(w, a);
-                const long long m0 = (long long)wp.mt * a.bm + crank * 128;
+                const long long m0 = (long long)wp.mt * a.bm + crank * 128 + (long long)half * a_rows;
                 const int n0 = wp.nt * a.bn + (int)crank * (a.bn / 2);
                 int wc = 0, hc = 0, nimg = 0;
                 if (isA && !a.a_tiled) {
@@ -712,7 +719,10 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 int r = rs / a.S, s = rs % a.S;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t *dst = dst0 + stage * tx;
+                    // experiment (dbg_flags & 8): issue times of the first tile's A (B) loads
+                    if (dbg && (a.dbg_flags & 8) && w == wstart && kb - kb0 < 16 && half == 0)
+                        dbg[(isA ? 16 : 32) + (kb - kb0)] = ptx::globaltimer();
+                    uint8_t *dst = dst0 + stage * sstride;
                     if constexpr (kPair) {
                         // both CTAs' bytes land on the leader's barrier; only the leader arms it
                         if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * tx);
@@ -779,13 +789,14 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const long long dit = (w - wstart) / wstep;     // debug: per-tile events of the first 8 tiles
-                if (dbg && dit < 8) dbg[16 + dit * 6 + 0] = ptx::globaltimer();
+                if (dbg && dit < 8 && !(a.dbg_flags & 8)) dbg[16 + dit * 6 + 0] = ptx::globaltimer();
                 const uint32_t d_tmem = tmem_base + acc * acc_cols;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     if (dbg && w == wstart && kb == kb0) dbg[2] = ptx::globaltimer();
-                    if (dbg && dit < 8 && kb == kb0) dbg[16 + dit * 6 + 1] = ptx::globaltimer();
+                    if (dbg && dit < 8 && kb == kb0 && !(a.dbg_flags & 8)) dbg[16 + dit * 6 + 1] = ptx::globaltimer();
+                    if (dbg && (a.dbg_flags & 8) && w == wstart && kb - kb0 < 16) dbg[48 + (kb - kb0)] = ptx::globaltimer();
                     const uint64_t ad = a_desc0 + (uint64_t)((stage * a_bytes) >> 4);
                     const uint64_t bd = b_desc0 + (uint64_t)((stage * b_bytes) >> 4);
                     if constexpr (kPair) {
@@ -807,8 +818,8 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 if constexpr (kPair) ptx::umma_commit2_multicast(&tfull[acc]);   // both CTAs' halves ready
                 else ptx::umma_commit(&tfull[acc]);                               // accumulator ready
                 if (dbg && w == wstart) dbg[3] = ptx::globaltimer();
-                if (dbg && dit < 8) dbg[16 + dit * 6 + 2] = ptx::globaltimer();
-                if (dbg && dit < 8 && (a.dbg_flags & 4)) {   // experiment: MMA completion seen by a spinning thread
+                if (dbg && dit < 8 && !(a.dbg_flags & 8)) dbg[16 + dit * 6 + 2] = ptx::globaltimer();
+                if (dbg && dit < 8 && (a.dbg_flags & 4) && !(a.dbg_flags & 8)) {   // experiment: MMA completion seen by a spinning thread
                     while (!ptx::mbar_test_wait(&tfull[acc], acc_phase)) {}
                     dbg[16 + dit * 6 + 5] = ptx::globaltimer();
                 }
@@ -831,7 +842,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             const long long dit = (w - wstart) / wstep;
-            if (dbg && warp == 4 && lane == 0 && dit < 8) dbg[16 + dit * 6 + 3] = ptx::globaltimer();
+            if (dbg && warp == 4 && lane == 0 && dit < 8 && !(a.dbg_flags & 8)) dbg[16 + dit * 6 + 3] = ptx::globaltimer();
             // split-K (EK_SPLIT): the tile's last split owns the output; it waits until the other
             // splits have published their partials (they precede it in the static schedule, so they
             // are resident or done: no deadlock), then reduces them in split order.
@@ -926,7 +937,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             if (dbg && warp == 4 && lane == 0 && w == wstart) dbg[4] = ptx::globaltimer();
             if (dbg && warp == 4 && lane == 0 && dit < 8) {
                 dbg[8 + dit] = ptx::globaltimer();
-                dbg[16 + dit * 6 + 4] = ptx::globaltimer();
+                if (!(a.dbg_flags & 8)) dbg[16 + dit * 6 + 4] = ptx::globaltimer();
             }
             if (lane == 0) {                                  // TMEM free: the MMA may start the next tile
                 if constexpr (kPair) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));

@@ -40,6 +40,14 @@ for i, n in enumerate(names):
     col = rel[:, i]
     col = col[col > -1e6]
     print(f"  {n:14s} min {col.min():8.2f}  median {np.median(col):8.2f}  max {col.max():8.2f} us")
+if int(os.environ.get("WPK_DBG_FLAGS", "0")) & 8:   # per-K-block stamps of the first tile, CTA 0
+    r0 = t64[0]
+    print("  CTA0 first tile, us:  A issued / B issued / stage full (MMA)")
+    for kb in range(16):
+        a_, b_, f_ = r0[16 + kb], r0[32 + kb], r0[48 + kb]
+        if f_ > 0:
+            print(f"   kb {kb:2d}  {(a_ - t0) / 1e3:7.2f} {(b_ - t0) / 1e3:7.2f} {(f_ - t0) / 1e3:7.2f}")
+    sys.exit(0)
 ev = t64[t64[:, 0] > 0][:, 16:64].reshape(-1, 8, 6)
 print("  per-tile events of CTA 0 (us): tempty_ok, 1st_full, mma_commit, epi_tfull_ok, epi_done, [mma_seen_done]")
 for it in range(8):
