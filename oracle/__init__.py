@@ -47,6 +47,7 @@ def _load():
         i32p = ctypes.POINTER(ctypes.c_int32)
         dp = ctypes.POINTER(ctypes.c_double)
         lib.wpk_oracle_conv2d.argtypes = [i32p, dp, dp, dp, dp, ctypes.c_int]
+        lib.wpk_oracle_conv2d_res.argtypes = [i32p, dp, dp, dp, dp, dp, ctypes.c_int]
         lib.wpk_oracle_conv2d_points.argtypes = [i32p, dp, dp, dp, ctypes.POINTER(ctypes.c_int64),
                                                  ctypes.c_int64, dp, ctypes.c_int]
         lib.wpk_oracle_out_dims.argtypes = [i32p, i32p, i32p]
@@ -54,7 +55,7 @@ def _load():
     return _lib
 
 
-EPI_NONE, EPI_BIAS, EPI_BIAS_RELU = 0, 1, 2
+EPI_NONE, EPI_BIAS, EPI_BIAS_RELU, EPI_BIAS_ADD_RELU = 0, 1, 2, 3
 
 
 def _shape(n, c, h, w, k, r, s, stride, pad, dil, groups, epilogue):
@@ -88,8 +89,11 @@ def out_dims(n, c, h, w, k, r, s, stride=1, pad=0, dil=1, groups=1):
     return p.value, q.value
 
 
-def conv2d(x, w, b=None, stride=1, pad=0, dil=1, groups=1, relu=True, nthreads=1):
-    """y[N,K,P,Q] (float64) for x[N,C,H,W], w[K,C/g,R,S], b[K] (NCHW/KCRS)."""
+def conv2d(x, w, b=None, stride=1, pad=0, dil=1, groups=1, relu=True, nthreads=1, residual=None):
+    """y[N,K,P,Q] (float64) for x[N,C,H,W], w[K,C/g,R,S], b[K] (NCHW/KCRS). With residual
+    z[N,K,P,Q]: y = max(conv + b + z, 0) (epilogue 3, the ResNet block's residual-add fusion)."""
+    if residual is not None:
+        return _conv2d_res(x, w, b, residual, stride, pad, dil, groups, nthreads)
     x, w, b = _as_f64(x), _as_f64(w), _as_f64(b)
     n, c, h, wd = x.shape
     k, cpg, r, s = w.shape
@@ -105,6 +109,24 @@ def conv2d(x, w, b=None, stride=1, pad=0, dil=1, groups=1, relu=True, nthreads=1
     y = np.zeros((n, k, p, q), dtype=np.float64)
     rc = _load().wpk_oracle_conv2d(sh.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                    _ptr(x), _ptr(w), _ptr(b), _ptr(y), int(nthreads))
+    if rc != 0:
+        raise ValueError("invalid shape")
+    return y
+
+
+def _conv2d_res(x, w, b, z, stride, pad, dil, groups, nthreads):
+    x, w, b, z = _as_f64(x), _as_f64(w), _as_f64(b), _as_f64(z)
+    n, c, h, wd = x.shape
+    k, cpg, r, s = w.shape
+    if b is None:
+        b = np.zeros(k)
+    sh = _shape(n, c, h, wd, k, r, s, stride, pad, dil, groups, EPI_BIAS_ADD_RELU)
+    p, q = out_dims(n, c, h, wd, k, r, s, stride, pad, dil, groups)
+    if p < 1 or q < 1 or z.shape != (n, k, p, q):
+        raise ValueError("empty output or residual shape mismatch")
+    y = np.zeros((n, k, p, q), dtype=np.float64)
+    rc = _load().wpk_oracle_conv2d_res(sh.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                       _ptr(x), _ptr(w), _ptr(b), _ptr(z), _ptr(y), int(nthreads))
     if rc != 0:
         raise ValueError("invalid shape")
     return y

@@ -18,6 +18,8 @@
  *                  x[n, grp(k)*Cpg + c, p*stride_h - pad_h + r*dil_h, q*stride_w - pad_w + s*dil_w]
  *                  * w[k, c, r, s]            (x taken as 0 outside [0,H) x [0,W))
  *   y = pre (epilogue 0) | pre + b[k] (1) | max(pre + b[k], 0) (2)
+ *     | max(pre + b[k] + z[n,k,p,q], 0) (3: the residual-add fusion of a ResNet block's last
+ *       conv, SURVEY.md §8(f) NEXT-1 / PAPER.md:15 operator fusion; z has y's shape)
  *
  * Layout: canonical NCHW for x and y, KCRS for w (the test harness transposes with numpy for
  * NHWC cases). Loop order (n, k, p, q, c, r, s), fixed.
@@ -44,7 +46,7 @@ int wpk_oracle_out_dims(const int32_t *shape, int32_t *p_out, int32_t *q_out)
 
 /* One output element, exactly as the definition above. */
 static double one_output(const int32_t *sh, const double *x, const double *w, const double *b,
-                         int n, int k, int p, int q)
+                         const double *z, int n, int k, int p, int q)
 {
     const int C = sh[1], H = sh[2], W = sh[3], K = sh[4], R = sh[5], S = sh[6];
     const int sth = sh[7], stw = sh[8], ph = sh[9], pw = sh[10], dh = sh[11], dw = sh[12];
@@ -62,18 +64,34 @@ static double one_output(const int32_t *sh, const double *x, const double *w, co
                 acc += xv * w[(((size_t)k * Cpg + c) * R + r) * S + s];
             }
     if (epi >= 1) acc += b[k];
-    if (epi == 2 && acc < 0.0) acc = 0.0;
+    if (epi == 3) {
+        int P, Q;
+        wpk_oracle_out_dims(sh, &P, &Q);
+        acc += z[(((size_t)n * K + k) * P + p) * Q + q];
+    }
+    if (epi >= 2 && acc < 0.0) acc = 0.0;
     return acc;
 }
 
 /* Full output tensor y[N][K][P][Q].  nthreads > 1 splits the outermost (n,k) loop with OpenMP;
  * the arithmetic per element is unchanged. Returns 0, or -1 on an invalid shape. */
+int wpk_oracle_conv2d_res(const int32_t *sh, const double *x, const double *w, const double *b,
+                          const double *z, double *y, int nthreads);
 int wpk_oracle_conv2d(const int32_t *sh, const double *x, const double *w, const double *b,
                       double *y, int nthreads)
+{
+    if (sh[14] == 3) return -1;   /* the residual epilogue needs z: wpk_oracle_conv2d_res */
+    return wpk_oracle_conv2d_res(sh, x, w, b, NULL, y, nthreads);
+}
+
+/* Same, with the residual z[N][K][P][Q] (read only when epilogue == 3). */
+int wpk_oracle_conv2d_res(const int32_t *sh, const double *x, const double *w, const double *b,
+                          const double *z, double *y, int nthreads)
 {
     int P, Q;
     if (sh[0] < 1 || sh[1] < 1 || sh[4] < 1 || sh[13] < 1) return -1;
     if (sh[1] % sh[13] != 0 || sh[4] % sh[13] != 0) return -1;
+    if (sh[14] == 3 && z == NULL) return -1;
     if (wpk_oracle_out_dims(sh, &P, &Q) != 0) return -1;
     const int N = sh[0], K = sh[4];
     const long long NK = (long long)N * K;
@@ -83,7 +101,7 @@ int wpk_oracle_conv2d(const int32_t *sh, const double *x, const double *w, const
         int n = (int)(nk / K), k = (int)(nk % K);
         for (int p = 0; p < P; ++p)
             for (int q = 0; q < Q; ++q)
-                y[((size_t)nk * P + p) * Q + q] = one_output(sh, x, w, b, n, k, p, q);
+                y[((size_t)nk * P + p) * Q + q] = one_output(sh, x, w, b, z, n, k, p, q);
     }
     return 0;
 }
@@ -95,6 +113,7 @@ int wpk_oracle_conv2d_points(const int32_t *sh, const double *x, const double *w
 {
     int P, Q;
     if (wpk_oracle_out_dims(sh, &P, &Q) != 0) return -1;
+    if (sh[14] == 3) return -1;   /* sampled outputs: epilogues 0-2 */
     for (int64_t i = 0; i < npts; ++i) {
         const int64_t *t = pts + 4 * i;
         if (t[0] < 0 || t[0] >= sh[0] || t[1] < 0 || t[1] >= sh[4] || t[2] < 0 || t[2] >= P ||
@@ -105,7 +124,7 @@ int wpk_oracle_conv2d_points(const int32_t *sh, const double *x, const double *w
 #pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
     for (int64_t i = 0; i < npts; ++i) {
         const int64_t *t = pts + 4 * i;
-        out[i] = one_output(sh, x, w, b, (int)t[0], (int)t[1], (int)t[2], (int)t[3]);
+        out[i] = one_output(sh, x, w, b, NULL, (int)t[0], (int)t[1], (int)t[2], (int)t[3]);
     }
     return 0;
 }

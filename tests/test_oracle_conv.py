@@ -183,3 +183,42 @@ def test_invalid_shapes_rejected(oracle_lib):
         oracle.conv2d(np.ones((1, 1, 2, 2)), np.ones((1, 1, 3, 3)), None)      # empty output
     with pytest.raises(ValueError):
         oracle.conv2d(np.ones((1, 3, 4, 4)), np.ones((2, 2, 1, 1)), None, groups=2)
+
+
+# ---- residual-add epilogue (epilogue 3: y = max(conv + b + z, 0)) ----------
+def test_residual_closed_forms(oracle_lib):
+    """Pins of the residual epilogue against forms that do not go through it: z = 0 is the
+    bias+ReLU epilogue; a per-channel constant z folds into the bias (so z is indexed by k and added
+    before the ReLU); a 1x1 identity filter gives relu(x + b + z) written out in numpy; z = -(conv+b)
+    gives exactly zero."""
+    rng = np.random.default_rng(5)
+    x = rng.integers(-3, 4, size=(2, 4, 6, 5)).astype(np.float64)
+    w = rng.integers(-2, 3, size=(6, 4, 3, 3)).astype(np.float64)
+    b = rng.integers(-4, 5, size=6).astype(np.float64)
+    base = oracle_lib.conv2d(x, w, b, stride=1, pad=1, relu=True)
+    pre = oracle_lib.conv2d(x, w, b, stride=1, pad=1, relu=False)
+    z0 = np.zeros_like(base)
+    assert np.array_equal(oracle_lib.conv2d(x, w, b, stride=1, pad=1, residual=z0), base)
+    cst = rng.integers(-5, 6, size=6).astype(np.float64)
+    zc = np.broadcast_to(cst[None, :, None, None], base.shape).copy()
+    assert np.array_equal(oracle_lib.conv2d(x, w, b, stride=1, pad=1, residual=zc),
+                          oracle_lib.conv2d(x, w, b + cst, stride=1, pad=1, relu=True))
+    assert np.array_equal(oracle_lib.conv2d(x, w, b, stride=1, pad=1, residual=-pre), np.zeros_like(base))
+    eye = np.zeros((4, 4, 1, 1))
+    eye[np.arange(4), np.arange(4)] = 1.0
+    z = rng.integers(-6, 7, size=x.shape).astype(np.float64)
+    bi = rng.integers(-4, 5, size=4).astype(np.float64)
+    want = np.maximum(x + bi[None, :, None, None] + z, 0.0)
+    assert np.array_equal(oracle_lib.conv2d(x, eye, bi, residual=z), want)
+
+
+def test_residual_vs_torch_float64(oracle_lib):
+    g = torch.Generator().manual_seed(11)
+    x = torch.randn(2, 5, 9, 7, generator=g, dtype=torch.float64)
+    w = torch.randn(8, 5, 3, 3, generator=g, dtype=torch.float64)
+    b = torch.randn(8, generator=g, dtype=torch.float64)
+    ref0 = torch.nn.functional.conv2d(x, w, b, stride=2, padding=1)
+    z = torch.randn(ref0.shape, generator=g, dtype=torch.float64)
+    ref = torch.relu(ref0 + z).numpy()
+    got = oracle_lib.conv2d(x, w, b, stride=2, pad=1, residual=z)
+    assert np.abs(got - ref).max() < 1e-12
