@@ -381,6 +381,41 @@ def main():
                             "pct_peak": fl / (sel.own_us * 1e-6) / 1e12 / peak})
             table.append(row)
 
+    # ---- the same step through the box's cuDNN (rank 0): fused conv+bias+ReLU on channels_last
+    # tensors, all 53 convs captured in ONE CUDA graph like ours, same warm-up / step count ------------
+    cudnn_step = None
+    if rank == 0 and not args.no_cudnn:
+        try:
+            fns = [selector.cudnn_conv_fn(xd, wd, bd, layers[i].stride, layers[i].pad, layers[i].dil, layers[i].groups,
+                                          "nhwc", "bf16", fused=True) for (i, plan, xd, wd, bd, yd) in units]
+            with torch.cuda.stream(stream):
+                for f in fns:
+                    f()
+            torch.cuda.synchronize()
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg, stream=stream):
+                for f in fns:
+                    f()
+            with torch.cuda.stream(stream):
+                for _ in range(args.warmup):
+                    cg.replay()
+            torch.cuda.synchronize()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            with torch.cuda.stream(stream):
+                for _ in range(args.steps):
+                    cg.replay()
+            c1.record(stream)
+            torch.cuda.synchronize()
+            cms = c0.elapsed_time(c1) / args.steps
+            cudnn_step = {"ms_per_step": cms, "value": total_flops / (cms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                          "wpk_speedup": cms / ms_per_step,
+                          "how": "torch.cudnn_convolution_relu on channels_last bf16, the 53 convs in one CUDA graph, "
+                                 "cudnn.benchmark=True, same warm-up and step count"}
+            del cg
+        except Exception as ex:   # the competitor is optional context, never a reason to fail the bench
+            cudnn_step = {"error": str(ex)[:200]}
+
     # ---- CPU oracle baseline (rank 0, N=1 only) -----------------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -415,6 +450,7 @@ def main():
                          "kernel": "umma_conv_kernel (+ split-K fixup where chosen), all 53 launches",
                          "peak_source": peak_src + " bf16 burst"},
             "roofline_step": roof_step,
+            "cudnn_step": cudnn_step,
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "how": "wpk_conv2d_run_host_async per conv on 3 round-robin streams (pinned host x in, host y out)"},
             "gpu_launches": launches,

@@ -21,7 +21,7 @@
  *  - Layouts (dense, row-major in the order given):
  *      WPK_NCHW: x [N][C][H][W],  w [K][C/g][R][S] (KCRS),  y [N][K][P][Q]
  *      WPK_NHWC: x [N][H][W][C],  w [K][R][S][C/g] (KRSC),  y [N][P][Q][K]
- *      b [K] (or NULL iff epilogue == WPK_EPI_NONE).
+ *      b [K] (or NULL iff epilogue == WPK_EPI_NONE); residual z (WPK_EPI_BIAS_ADD_RELU) laid out as y.
  *  - dtypes: x, w, b, y share one element type:
  *      WPK_F32  float32, exact fp32 FMA on CUDA cores (strict-comparison path)
  *      WPK_TF32 float32 in/out, tf32 tensor-core products, fp32 accumulate
@@ -62,7 +62,10 @@ typedef enum {
 
 typedef enum { WPK_F32 = 0, WPK_TF32 = 1, WPK_BF16 = 2, WPK_F16 = 3 } wpk_dtype;
 typedef enum { WPK_NCHW = 0, WPK_NHWC = 1 } wpk_layout;
-typedef enum { WPK_EPI_NONE = 0, WPK_EPI_BIAS = 1, WPK_EPI_BIAS_RELU = 2 } wpk_epilogue;
+/* WPK_EPI_BIAS_ADD_RELU: y = max(conv + b + z, 0) with a residual z of y's shape, layout and dtype
+ * (the last conv of a ResNet block fused with its shortcut add). Run it
+ * with wpk_conv2d_run_residual; the tcgen05 family supports it with SPLIT_K = 1. */
+typedef enum { WPK_EPI_NONE = 0, WPK_EPI_BIAS = 1, WPK_EPI_BIAS_RELU = 2, WPK_EPI_BIAS_ADD_RELU = 3 } wpk_epilogue;
 typedef enum { WPK_SEARCH_GA = 0, WPK_SEARCH_RL = 1, WPK_SEARCH_RANDOM = 2 } wpk_search;
 typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 2 } wpk_eval_mode;
 
@@ -158,6 +161,12 @@ WPK_API wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t bud
  * (weights are inference constants); after mutating w in place call
  * wpk_conv2d_invalidate. One stream at a time per plan. */
 WPK_API wpk_status wpk_conv2d_run(wpk_plan plan, const void *x, const void *w, const void *b, void *y, void *stream);
+
+/* run for WPK_EPI_BIAS_ADD_RELU plans: z is the residual, a device tensor laid out exactly like y
+ * (it may not alias y). WPK_ERR_INVALID_ARGUMENT if the plan's epilogue is not BIAS_ADD_RELU, if z
+ * or b is NULL, or if z is not 16-byte aligned; wpk_conv2d_run on such a plan fails the same way. */
+WPK_API wpk_status wpk_conv2d_run_residual(wpk_plan plan, const void *x, const void *w, const void *b, const void *z,
+                                           void *y, void *stream);
 
 /* Same as run, but x and y are HOST pointers: copies x host->device, runs, copies y back, all on
  * `stream`, then synchronises the stream. Device staging buffers live in the workspace. */

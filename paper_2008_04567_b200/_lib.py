@@ -22,7 +22,7 @@ STATUS_NAMES = ["OK", "INVALID_ARGUMENT", "SHAPE", "UNSUPPORTED", "INVALID_CONFI
                 "OUT_OF_MEMORY", "INTERNAL"]
 DTYPES = {"f32": 0, "tf32": 1, "bf16": 2, "f16": 3}
 LAYOUTS = {"nchw": 0, "nhwc": 1}
-EPILOGUES = {"none": 0, "bias": 1, "bias_relu": 2}
+EPILOGUES = {"none": 0, "bias": 1, "bias_relu": 2, "bias_add_relu": 3}
 SEARCHES = {"ga": 0, "rl": 1, "random": 2}
 EVAL_MODES = {"measured": 0, "replay": 1, "synthetic": 2}
 FAMILIES = {"simt": 0, "umma": 1, "dw": 2, "auto": -1}
@@ -92,6 +92,7 @@ def load():
         "wpk_conv2d_plan": (I32, [ctypes.POINTER(Shape), I32, ctypes.c_int, ctypes.POINTER(P)]),
         "wpk_conv2d_tune": (I32, [P, I32, I32, ctypes.POINTER(TuneOptions)]),
         "wpk_conv2d_run": (I32, [P, P, P, P, P, P]),
+        "wpk_conv2d_run_residual": (I32, [P, P, P, P, P, P, P]),
         "wpk_conv2d_run_host": (I32, [P, P, P, P, P, P]),
         "wpk_conv2d_run_host_async": (I32, [P, P, P, P, P, P]),
         "wpk_conv2d_destroy": (None, [P]),

@@ -104,7 +104,8 @@ class Conv2dPlan:
 
     # -- run -------------------------------------------------------------------------------------
     def run(self, x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, y: torch.Tensor | None = None,
-            stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+            stream: torch.cuda.Stream | None = None, z: torch.Tensor | None = None) -> torch.Tensor:
+        """y = epilogue(conv(x, w)); for epilogue "bias_add_relu" z is the residual (y's shape)."""
         dt = _TORCH_DT[self.dtype]
         for t, nm, shp in ((x, "x", self.x_shape()), (w, "w", self.w_shape())):
             if t.dtype != dt or tuple(t.shape) != shp or not t.is_contiguous() or not t.is_cuda:
@@ -114,6 +115,13 @@ class Conv2dPlan:
         self._ensure_workspace()
         s = (stream or torch.cuda.current_stream(x.device)).cuda_stream
         bp = ctypes.c_void_p(b.data_ptr()) if b is not None else None
+        if self.epilogue == "bias_add_relu":
+            if z is None or z.dtype != dt or tuple(z.shape) != self.y_shape() or not z.is_contiguous() or not z.is_cuda:
+                raise ValueError(f"z: expected contiguous cuda {dt} of shape {self.y_shape()}")
+            L.check(self.lib.wpk_conv2d_run_residual(self.handle, ctypes.c_void_p(x.data_ptr()),
+                                                     ctypes.c_void_p(w.data_ptr()), bp, ctypes.c_void_p(z.data_ptr()),
+                                                     ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(s)))
+            return y
         L.check(self.lib.wpk_conv2d_run(self.handle, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(w.data_ptr()),
                                         bp, ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(s)))
         return y

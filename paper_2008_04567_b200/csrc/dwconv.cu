@@ -83,14 +83,16 @@ __global__ void dw_conv_kernel(const DwArgs a) {
             const int q = qb * PIX + i;
             if (q >= a.Q) continue;
             T out[VEC];
+            const long long yo = (long long)n * a.ys_n + (long long)p * a.ys_p + (long long)q * a.ys_q;
 #pragma unroll
             for (int v = 0; v < VEC; ++v) {
                 float o = acc[i][v];
                 if (a.epilogue >= 1) o += to_f<T>(b[c0 + v]);
-                if (a.epilogue == 2) o = fmaxf(o, 0.f);
+                if (a.epilogue == 3) o += to_f<T>(static_cast<const T *>(a.z)[yo + (long long)(c0 + v) * a.ys_c]);
+                if (a.epilogue >= 2) o = fmaxf(o, 0.f);
                 out[v] = from_f<T>(o);
             }
-            T *yd = y + (long long)n * a.ys_n + (long long)p * a.ys_p + (long long)q * a.ys_q;
+            T *yd = y + yo;
             if (a.ys_c == 1 && VEC * sizeof(T) >= 4) {
                 constexpr int NB = VEC * sizeof(T);
                 if constexpr (NB == 16) *reinterpret_cast<uint4 *>(yd + c0) = *reinterpret_cast<uint4 *>(out);

@@ -9,6 +9,7 @@ namespace wpk {
 struct DwArgs {
     const void *x, *w, *b;   // w packed [R][S][C]
     void *y;
+    const void *z;           // residual (epilogue 3), laid out as y
     int N, C, H, W, R, S, P, Q;
     int sh, sw, ph, pw, dh, dw;
     long long xs_n, xs_c, xs_h, xs_w;

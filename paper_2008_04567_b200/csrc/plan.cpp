@@ -36,7 +36,7 @@ static wpk_status to_desc(const wpk_conv2d_shape *s, int dtype, ConvDesc *d) {
         return fail(WPK_ERR_INVALID_ARGUMENT, "wpk_conv2d_shape.struct_size mismatch (ABI version)");
     if (dtype < WPK_F32 || dtype > WPK_F16) return fail(WPK_ERR_INVALID_ARGUMENT, "bad dtype");
     if (s->layout != WPK_NCHW && s->layout != WPK_NHWC) return fail(WPK_ERR_INVALID_ARGUMENT, "bad layout");
-    if (s->epilogue < WPK_EPI_NONE || s->epilogue > WPK_EPI_BIAS_RELU)
+    if (s->epilogue < WPK_EPI_NONE || s->epilogue > WPK_EPI_BIAS_ADD_RELU)
         return fail(WPK_ERR_INVALID_ARGUMENT, "bad epilogue");
     const int dims[] = {s->n, s->c, s->h, s->w, s->k, s->r, s->s, s->stride_h, s->stride_w,
                         s->dil_h, s->dil_w, s->groups};
@@ -174,6 +174,7 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
         g->num_kb = d.r * d.s * g->c_blocks;
     }
     if (g->splits > g->num_kb) return no("SPLIT_K larger than the number of K blocks");
+    if (g->splits > 1 && d.epilogue == WPK_EPI_BIAS_ADD_RELU) return no("the residual epilogue needs SPLIT_K = 1");
     g->kb_per_split = (g->num_kb + g->splits - 1) / g->splits;
     if ((long long)(g->splits - 1) * g->kb_per_split >= g->num_kb) return no("SPLIT_K leaves an empty split");
     g->m_tiles = (int)((d.M() + g->bm - 1) / g->bm);

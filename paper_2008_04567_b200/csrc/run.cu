@@ -343,7 +343,7 @@ size_t workspace_bytes(const Plan &p, const Config &cfg, bool host_staging) {
 
 // ---- one run ------------------------------------------------------------------------------------------
 int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const void *b, void *y, void *stream,
-                char *ws, size_t ws_bytes) {
+                char *ws, size_t ws_bytes, const void *z) {
     const ConvDesc &d = p.d;
     cudaStream_t st = (cudaStream_t)stream;
     const int sm = device_sm_count(p.device);
@@ -361,7 +361,7 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
                                                  : simt_get_f32(g[3], g[4], g[5], g[6]);
         if (!fn) { set_error("no SIMT instantiation for these tiles"); return -1; }
         SimtArgs a{};
-        a.x = x; a.w = w; a.b = b; a.y = y;
+        a.x = x; a.w = w; a.b = b; a.y = y; a.z = z;
         a.N = d.n; a.C = d.c; a.H = d.h; a.W = d.w; a.K = d.k; a.R = d.r; a.S = d.s; a.P = d.p; a.Q = d.q;
         a.sh = d.sh; a.sw = d.sw; a.ph = d.ph; a.pw = d.pw; a.dh = d.dh; a.dw = d.dw;
         a.Cpg = d.c / d.g; a.Kpg = d.k / d.g; a.groups = d.g;
@@ -395,7 +395,7 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
             p.packed_cfg_family = WPK_FAMILY_DW;
         }
         DwArgs a{};
-        a.x = x; a.w = wp; a.b = b; a.y = y;
+        a.x = x; a.w = wp; a.b = b; a.y = y; a.z = z;
         a.N = d.n; a.C = d.c; a.H = d.h; a.W = d.w; a.R = d.r; a.S = d.s; a.P = d.p; a.Q = d.q;
         a.sh = d.sh; a.sw = d.sw; a.ph = d.ph; a.pw = d.pw; a.dh = d.dh; a.dw = d.dw;
         if (d.layout == WPK_NCHW) {
@@ -464,7 +464,7 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) { set_error(std::string("aux kernel launch: ") + cudaGetErrorString(ce)); return -1; }
     UmmaLaunch U{};
-    U.dtype = d.dtype; U.x = xk; U.w = wk; U.b = b; U.y = y;
+    U.dtype = d.dtype; U.x = xk; U.w = wk; U.b = b; U.y = y; U.z = z;
     U.partial = (g.splits > 1 && !g.csplit) ? reinterpret_cast<float *>(ws + L.p_off) : nullptr;
     if (g.splits > 1 && !g.csplit) {
         // counters are self-resetting; zero them once per (workspace, layout) they live at
@@ -553,7 +553,28 @@ wpk_status wpk_conv2d_set_workspace(wpk_plan plan, void *dev_ptr, size_t bytes) 
     return WPK_OK;
 }
 
+static wpk_status run_impl(wpk_plan plan, const void *x, const void *w, const void *b, const void *z, void *y,
+                           void *stream);
+
 wpk_status wpk_conv2d_run(wpk_plan plan, const void *x, const void *w, const void *b, void *y, void *stream) {
+    if (plan && reinterpret_cast<Plan *>(plan)->d.epilogue == WPK_EPI_BIAS_ADD_RELU)
+        return fail(WPK_ERR_INVALID_ARGUMENT, "the plan's residual epilogue needs wpk_conv2d_run_residual");
+    return run_impl(plan, x, w, b, nullptr, y, stream);
+}
+
+wpk_status wpk_conv2d_run_residual(wpk_plan plan, const void *x, const void *w, const void *b, const void *z, void *y,
+                                   void *stream) {
+    if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
+    if (reinterpret_cast<Plan *>(plan)->d.epilogue != WPK_EPI_BIAS_ADD_RELU)
+        return fail(WPK_ERR_INVALID_ARGUMENT, "wpk_conv2d_run_residual needs a WPK_EPI_BIAS_ADD_RELU plan");
+    if (!z) return fail(WPK_ERR_INVALID_ARGUMENT, "z must be non-NULL");
+    if ((reinterpret_cast<uintptr_t>(z) & 15) != 0) return fail(WPK_ERR_INVALID_ARGUMENT, "z must be 16-byte aligned");
+    if (z == y) return fail(WPK_ERR_INVALID_ARGUMENT, "z may not alias y");
+    return run_impl(plan, x, w, b, z, y, stream);
+}
+
+static wpk_status run_impl(wpk_plan plan, const void *x, const void *w, const void *b, const void *z, void *y,
+                           void *stream) {
     if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
     Plan *p = reinterpret_cast<Plan *>(plan);
     if (!x || !w || !y) return fail(WPK_ERR_INVALID_ARGUMENT, "x, w and y must be non-NULL");
@@ -571,7 +592,7 @@ wpk_status wpk_conv2d_run(wpk_plan plan, const void *x, const void *w, const voi
     size_t bytes;
     wpk_status st = ensure_ws(p, workspace_bytes(*p, p->cfg, false), &ws, &bytes);
     if (st != WPK_OK) return st;
-    int n = launch_conv(*p, p->cfg, x, w, b, y, stream, ws, bytes);
+    int n = launch_conv(*p, p->cfg, x, w, b, y, stream, ws, bytes, z);
     if (n < 0) return WPK_ERR_CUDA;
     p->last_launches = n;
     return WPK_OK;
@@ -595,6 +616,8 @@ static wpk_status run_host_impl(wpk_plan plan, const void *x_host, const void *w
     if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
     Plan *p = reinterpret_cast<Plan *>(plan);
     if (!x_host || !y_host || !w) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL pointer");
+    if (p->d.epilogue == WPK_EPI_BIAS_ADD_RELU)
+        return fail(WPK_ERR_INVALID_ARGUMENT, "the host-buffer calls support epilogues NONE / BIAS / BIAS_RELU");
     const ConvDesc &d = p->d;
     char *ws;
     size_t bytes;

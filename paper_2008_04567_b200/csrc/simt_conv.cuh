@@ -18,6 +18,7 @@ namespace wpk {
 struct SimtArgs {
     const void *x, *w, *b;
     void *y;
+    const void *z;          // residual (epilogue 3), laid out as y
     int N, C, H, W, K, R, S, P, Q;
     int sh, sw, ph, pw, dh, dw, Cpg, Kpg, groups;
     long long xs_n, xs_c, xs_h, xs_w;
@@ -120,8 +121,10 @@ __global__ void simt_conv_kernel(const SimtArgs a) {
                 const int q = q0 + l * bx;
                 if (q >= a.Q) continue;
                 float v = acc[j][i][l] + bias;
-                if (a.epilogue == 2) v = fmaxf(v, 0.f);
-                y[n * a.ys_n + k * a.ys_k + p * a.ys_p + q * a.ys_q] = from_f<T>(v);
+                const long long yi = n * a.ys_n + k * a.ys_k + p * a.ys_p + q * a.ys_q;
+                if (a.epilogue == 3) v += to_f<T>(static_cast<const T *>(a.z)[yi]);
+                if (a.epilogue >= 2) v = fmaxf(v, 0.f);
+                y[yi] = from_f<T>(v);
             }
         }
     }

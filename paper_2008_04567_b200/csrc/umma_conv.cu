@@ -189,6 +189,7 @@ launch:
     a.kpad_bias = (L.K + 255) / 256 * 256;
     a.recv_stride = g.recv_stride;
     a.a_split = a_split;
+    a.z = L.z;
     a.dbg_flags = getenv("WPK_DBG_FLAGS") ? atoi(getenv("WPK_DBG_FLAGS")) : 0;
     cudaStream_t st = (cudaStream_t)L.stream;
     long long grid = (long long)L.sm_count * g.ctas_per_sm;

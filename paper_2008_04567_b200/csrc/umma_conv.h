@@ -41,6 +41,7 @@ struct UmmaArgs {
     int kpad_bias;                  // staged bias length (K rounded up to 256, zero-padded)
     int recv_stride;                // EK_CSPLIT: bytes per received partial row
     int a_split;                    // A stage loaded by two threads (two half-height boxes)
+    const void *z;                  // residual (epilogue 3), laid out as y
     int dbg_flags;                  // experiments only (WPK_DBG_FLAGS): 1 = gather zero-fills, 2 = no y stores
 };
 
@@ -61,6 +62,7 @@ struct UmmaLaunch {
     const void *w;                   // [K][R][S][g.cpad]
     const void *b;
     void *y;
+    const void *z = nullptr;         // residual (epilogue 3), laid out as y
     float *partial;                  // split-K workspace (splits x M x K fp32) or nullptr
     int *counters = nullptr;         // split-K tile counters (zeroed once per workspace)
     int N, H, W, K, R, S, P, Q;

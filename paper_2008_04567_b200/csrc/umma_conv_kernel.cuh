@@ -76,6 +76,18 @@ __device__ __forceinline__ WorkPos decode_work(long long w, const UmmaArgs &a) {
     return r;
 }
 
+// element e (0/1) of a packed pair of 16-bit values, as float
+__device__ __forceinline__ float to_f2(uint32_t u, int e, __half *) {
+    return __half2float(__ushort_as_half((unsigned short)(e ? (u >> 16) : (u & 0xFFFFu))));
+}
+__device__ __forceinline__ float to_f2(uint32_t u, int e, __nv_bfloat16 *) {
+    return __bfloat162float(__ushort_as_bfloat16((unsigned short)(e ? (u >> 16) : (u & 0xFFFFu))));
+}
+__device__ __forceinline__ float to_f2(uint32_t, int, float *) { return 0.f; }
+__device__ __forceinline__ float ld_elem(const __half *p) { return __half2float(*p); }
+__device__ __forceinline__ float ld_elem(const __nv_bfloat16 *p) { return __bfloat162float(*p); }
+__device__ __forceinline__ float ld_elem(const float *p) { return *p; }
+
 // bias + ReLU for 4 consecutive columns (bias staged in smem as fp32, zero-padded past K)
 __device__ __forceinline__ void bias_relu4(float *v, const float *sBias, int k, bool relu) {
     const float4 b = *reinterpret_cast<const float4 *>(sBias + k);
@@ -130,6 +142,16 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx &E, const UmmaArgs &a, cons
     uint32_t raw[k16 ? 64 : 32];
     ptx::tmem_ld32_nowait(taddr, raw);
     if constexpr (k16) ptx::tmem_ld32_nowait(taddr + 32, raw + 32);
+    // residual (epilogue 3): this lane's row, the chunk's 128 bytes, loaded while TMEM drains
+    uint4 zr[8];
+    const bool res = FINAL && a.epilogue == 3;
+    if (res) {
+        const long long m = (long long)mrow + E.lane;
+        const uint4 *zp = reinterpret_cast<const uint4 *>(static_cast<const T *>(a.z) + m * a.K + k0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            zr[j] = (m < a.M && k0 + (j + 1) * (int)(16 / sizeof(T)) <= a.K) ? __ldg(zp + j) : make_uint4(0u, 0u, 0u, 0u);
+    }
     ptx::tmem_wait_ld();
     uint32_t pk[32];
     if constexpr (k16) {
@@ -137,7 +159,16 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx &E, const UmmaArgs &a, cons
         for (int q = 0; q < 16; ++q) {
             float v[4] = {__uint_as_float(raw[4 * q]), __uint_as_float(raw[4 * q + 1]), __uint_as_float(raw[4 * q + 2]),
                           __uint_as_float(raw[4 * q + 3])};
-            bias_relu4(v, E.sBias, k0 + 4 * q, a.epilogue == 2);
+            bias_relu4(v, E.sBias, k0 + 4 * q, false);
+            if (res) {   // 4 16-bit residual values = half of zr[q / 2]
+                const uint32_t lo = (q & 1) ? zr[q >> 1].z : zr[q >> 1].x, hi = (q & 1) ? zr[q >> 1].w : zr[q >> 1].y;
+                v[0] += to_f2(lo, 0, (T *)nullptr); v[1] += to_f2(lo, 1, (T *)nullptr);
+                v[2] += to_f2(hi, 0, (T *)nullptr); v[3] += to_f2(hi, 1, (T *)nullptr);
+            }
+            if (a.epilogue >= 2) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = fmaxf(v[j], 0.f);
+            }
             pk[2 * q] = pack2(v[0], v[1], (T *)nullptr);
             pk[2 * q + 1] = pack2(v[2], v[3], (T *)nullptr);
         }
@@ -146,7 +177,15 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx &E, const UmmaArgs &a, cons
         for (int q = 0; q < 8; ++q) {
             float v[4] = {__uint_as_float(raw[4 * q]), __uint_as_float(raw[4 * q + 1]), __uint_as_float(raw[4 * q + 2]),
                           __uint_as_float(raw[4 * q + 3])};
-            bias_relu4(v, E.sBias, k0 + 4 * q, a.epilogue == 2);
+            bias_relu4(v, E.sBias, k0 + 4 * q, false);
+            if (res) {
+                v[0] += __uint_as_float(zr[q].x); v[1] += __uint_as_float(zr[q].y);
+                v[2] += __uint_as_float(zr[q].z); v[3] += __uint_as_float(zr[q].w);
+            }
+            if (a.epilogue >= 2) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = fmaxf(v[j], 0.f);
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) pk[4 * q + j] = __float_as_uint(v[j]);
         }
@@ -284,14 +323,25 @@ __device__ __noinline__ void epi_chunk_direct(const UmmaArgs &a, const float *sB
         return;
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) bias_relu4(v + 4 * q, sBias, k0 + 4 * q, a.epilogue == 2);
+    for (int q = 0; q < 4; ++q) bias_relu4(v + 4 * q, sBias, k0 + 4 * q, false);
     T *y = static_cast<T *>(a.y);
+    const T *z = static_cast<const T *>(a.z);
     if (a.out_nchw) {
         const long long nimg = m / a.PQ;
         const long long base = nimg * (long long)a.K * a.PQ + (m - nimg * a.PQ);
         for (int j = 0; j < 16; ++j)
-            if (k0 + j < a.K) st_out(y + base + (long long)(k0 + j) * a.PQ, v[j]);
+            if (k0 + j < a.K) {
+                const long long yi = base + (long long)(k0 + j) * a.PQ;
+                float o = v[j];
+                if (a.epilogue == 3) o += ld_elem(z + yi);
+                if (a.epilogue >= 2) o = fmaxf(o, 0.f);
+                st_out(y + yi, o);
+            }
         return;
+    }
+    for (int j = 0; j < 16; ++j) {
+        if (a.epilogue == 3 && k0 + j < a.K) v[j] += ld_elem(z + m * a.K + k0 + j);
+        if (a.epilogue >= 2) v[j] = fmaxf(v[j], 0.f);
     }
     T *dst = y + m * a.K + k0;
     if (full16 && a.vec_ok) {

@@ -91,7 +91,7 @@ struct Plan;
 size_t workspace_bytes(const Plan &p, const Config &cfg, bool host_staging);
 // Launch everything for one run on `stream`; returns number of kernel launches or -1 (error set).
 int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const void *b, void *y,
-                void *stream, char *ws, size_t ws_bytes);
+                void *stream, char *ws, size_t ws_bytes, const void *z = nullptr);
 int device_sm_count(int device);
 int device_l2_bytes(int device);
 

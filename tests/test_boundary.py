@@ -129,3 +129,17 @@ def test_options_defaults():
     assert (o.warmup, o.reps, o.world, o.ga_pop, o.ga_elites) == (3, 11, 1, 48, 4)
     assert (o.rl_c1, o.rl_c2) == (0.15, 20.0)
     assert list(o.rl_hidden) == [512, 1024, 1024, 512]
+
+
+def test_residual_epilogue_host_validation():
+    """WPK_EPI_BIAS_ADD_RELU: split-K configs are invalid; the plain run entry point and the
+    host-buffer call refuse a residual plan before touching the device."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    plan = Conv2dPlan(2, 64, 8, 8, 128, 3, 3, 1, 1, layout="nhwc", epilogue="bias_add_relu", dtype="bf16", device=0)
+    assert plan.config_valid(1, [128, 4, 1, 0, 0, 2, 128])
+    assert not plan.config_valid(1, [128, 4, 2, 0, 0, 2, 128])
+    lib = L.load()
+    fake = ctypes.c_void_p(0x1000)
+    assert lib.wpk_conv2d_run(plan.handle, fake, fake, fake, fake, None) == 1          # WPK_ERR_INVALID_ARGUMENT
+    assert lib.wpk_conv2d_run_residual(plan.handle, fake, fake, fake, None, fake, None) == 1
+    assert lib.wpk_conv2d_run_host(plan.handle, fake, fake, fake, fake, None) == 1

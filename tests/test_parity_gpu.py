@@ -268,3 +268,49 @@ def test_resnet50_n32_sampled_bf16(layer):
     got = y[pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
     want = torch.from_numpy(ref).to(torch.bfloat16)
     assert torch.equal(got.float() + 0, want.float() + 0)
+
+
+def _residual_case(L, dtype, layout, seed):
+    """x, w, b and a residual z (NCHW, y's shape) in exact-integer mode, plus the oracle output."""
+    x, w, b = workloads.generate(L, dtype, "int", seed=seed)
+    p = (L.h + 2 * L.pad - L.dil * (L.r - 1) - 1) // L.stride + 1
+    q = (L.w + 2 * L.pad - L.dil * (L.s - 1) - 1) // L.stride + 1
+    g = torch.Generator().manual_seed(seed + 1)
+    z = torch.randint(-6, 7, (L.n, L.k, p, q), generator=g).to(workloads.torch_dtype(dtype))
+    ref = oracle.conv2d(x, w, b, stride=L.stride, pad=L.pad, dil=L.dil, groups=L.groups, residual=z)
+    return x, w, b, z, ref
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+@pytest.mark.parametrize("dtype", ["f32", "tf32", "bf16", "f16"])
+def test_residual_epilogue(dtype, layout):
+    """Epilogue 3, y = relu(conv + b + z): every family (SIMT for f32, tcgen05 with TMA-store and
+    direct epilogues, pairs, both gathers, depthwise) is bit-exact against the oracle."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import to_layout, from_layout
+    cases = [(ConvLayer("r3", 2, 64, 11, 13, 128, 3, 3, 1, 1), None),
+             (ConvLayer("r1", 1, 96, 9, 7, 200, 1, 1, 1, 0), None),
+             (ConvLayer("rdw", 2, 32, 10, 9, 32, 3, 3, 2, 1, 1, 32), None)]
+    for L, _ in cases:
+        x, w, b, z, ref = _residual_case(L, dtype, layout, seed=41)
+        plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups, layout=layout,
+                          epilogue="bias_add_relu", dtype=dtype)
+        xl, wl = to_layout(x, w, layout)
+        zl = z.permute(0, 2, 3, 1).contiguous() if layout == "nhwc" else z.contiguous()
+        xl, wl, bc, zc = xl.cuda(), wl.cuda(), b.cuda(), zl.cuda()
+        configs = [plan.config]
+        if plan.config[0] == 1:
+            configs += [(1, [128, 4, 1, 0, 0, 2, 128]), (1, [64, 3, 1, 1, 0, 4, 256]), (1, [256, 3, 1, 2, 0, 1, 256])]
+            assert not plan.config_valid(1, [128, 4, 2, 0, 0, 2, 128])   # residual plans: SPLIT_K = 1 only
+        ran = 0
+        for fam, genes in configs:
+            if not plan.config_valid(fam, list(genes)):
+                continue
+            plan.set_config(fam, list(genes))
+            y = plan.run(xl, wl, bc, z=zc)
+            torch.cuda.synchronize()
+            assert_bit_exact(from_layout(y.cpu(), layout), ref)
+            ran += 1
+        assert ran >= 1, L.name
+        with pytest.raises(Exception):   # a residual plan refuses the plain run entry point
+            plan.run(xl, wl, bc)

@@ -1,6 +1,6 @@
 import json, sys
 d = json.load(open(sys.argv[1]))
-for k in ['value','ms_per_step','roofline','roofline_step','e2e','gpu_launches','tuning_seconds','clocks']:
+for k in ['value','ms_per_step','roofline','roofline_step','cudnn_step','e2e','gpu_launches','tuning_seconds','clocks']:
     print(k, d.get(k))
 print(f"{'layer':10s} {'cnt':>3s} {'GF':>6s} {'wpk_us':>8s} {'cudnn':>8s} {'TF':>7s} {'x':>5s} cfg")
 tot_w = tot_c = 0
