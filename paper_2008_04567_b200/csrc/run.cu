@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -480,6 +481,7 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     U.N = d.n; U.H = d.h; U.W = d.w; U.K = d.k; U.R = d.r; U.S = d.s; U.P = d.p; U.Q = d.q;
     U.stride_h = d.sh; U.stride_w = d.sw; U.pad_h = d.ph; U.pad_w = d.pw; U.dil_h = d.dh; U.dil_w = d.dw;
     U.epilogue = d.epilogue; U.out_nchw = d.layout == WPK_NCHW; U.sm_count = sm; U.stream = stream; U.g = g;
+    if (getenv("WPK_GRID_CAP")) U.sm_count = std::min(sm, atoi(getenv("WPK_GRID_CAP")));   // experiments only
     U.a_rows = (g.a_mode == 1) ? d.M() : (long long)d.n * d.h * d.w;
     U.b_rs = (g.a_mode >= 1) ? 1 : d.r * d.s;
     U.C = (g.a_mode == 3) ? 4 : d.c;                          // channels per stored pixel
