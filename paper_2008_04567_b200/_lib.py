@@ -10,7 +10,8 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwpk.so")
+# WPK_LIB: an alternative in-tree build of the same library (A/B experiments on one GPU box)
+LIB_PATH = os.environ.get("WPK_LIB") or os.path.join(_HERE, "libwpk.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "wpk.h")
 
 NUM_GENES = 7

@@ -717,16 +717,10 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             ptx::tmem_relinquish();
         }
     }
-    // Programmatic dependent launch: this prologue overlaps the previous kernel's tail. Weights and
-    // bias are inference constants, so the bias is staged, and the B producer starts
-    // streaming weight tiles into shared memory, before the previous grid has finished; only the
-    // threads that read activations (A producers) or write the output (epilogue) execute
-    // griddepcontrol.wait.
-    if (warp >= 4 && warp < 12) {   // bias -> smem once (fp32, zero past K); zero without bias
-        const T *bias = static_cast<const T *>(a.bias);
-        for (int k = threadIdx.x - 128; k < a.kpad_bias; k += 256)
-            sBias[k] = (a.epilogue >= 1 && k < a.K) ? ld_bias(bias, k) : 0.f;
-    }
+    // Programmatic dependent launch: this prologue overlaps the previous kernel's tail. Weights are
+    // inference constants, so the B producer starts streaming weight tiles into shared
+    // memory before the previous grid has finished; only the threads that read activations (A
+    // producers) or write the output (epilogue) execute griddepcontrol.wait.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     ptx::tc_fence_before();
     __syncthreads();
@@ -878,6 +872,14 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
         }
     } else if (warp >= 4 && warp < 12) {
         // ===================== epilogue warps 4..11 =====================
+        // bias -> smem once (fp32, zero past K; zero without bias), off the prologue's critical
+        // path: the epilogue needs it only after the first tile's K loop
+        {
+            const T *bias = static_cast<const T *>(a.bias);
+            for (int k = threadIdx.x - 128; k < a.kpad_bias; k += 256)
+                sBias[k] = (a.epilogue >= 1 && k < a.K) ? ld_bias(bias, k) : 0.f;
+            ptx::named_bar_sync(1, 256);
+        }
         asm volatile("griddepcontrol.wait;" ::: "memory");   // y may still be in use upstream
         const int quarter = warp & 3;          // TMEM lane quarter this warp may access
         const int grp = (warp - 4) >> 2;       // 0 or 1
