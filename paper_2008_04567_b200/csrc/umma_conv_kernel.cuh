@@ -1010,7 +1010,9 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             }
             if (EK == EK_DIRECT && a.splits > 1) splitk_fixup<T>(a, sBias, sFlag, wp, nsub, warp, lane, crank, kPair ? 1 : 0);
         }
-        if (EK != EK_DIRECT && lane == 0) ptx::bulk_wait_all();
+        // the staging buffers must not be released while TMA stores still read them; the global
+        // writes themselves complete with the grid (a dependent grid's griddepcontrol.wait sees them)
+        if (EK != EK_DIRECT && lane == 0) ptx::bulk_wait_read<0>();
         if (dbg && warp == 4 && lane == 0) dbg[5] = ptx::globaltimer();
     }
 
