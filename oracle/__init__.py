@@ -149,3 +149,13 @@ def conv2d_points(x, w, b, pts, stride=1, pad=0, dil=1, groups=1, relu=True, nth
     if rc != 0:
         raise ValueError("invalid points/shape")
     return out
+
+
+def fold_batchnorm(w, b, gamma, beta, mean, var, eps):
+    """Inference batch-norm folded into (w, b), in float64 (SURVEY.md 8(f) NEXT-1b):
+    s_k = gamma_k / sqrt(var_k + eps); w'[k] = w[k] * s_k; b'_k = (b_k - mean_k) * s_k + beta_k.
+    Test infrastructure only."""
+    w, gamma, beta, mean, var = (_as_f64(t) for t in (w, gamma, beta, mean, var))
+    b = np.zeros(w.shape[0]) if b is None else _as_f64(b)
+    s = gamma / np.sqrt(var + eps)
+    return w * s.reshape((-1,) + (1,) * (w.ndim - 1)), (b - mean) * s + beta

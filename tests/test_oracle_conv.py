@@ -222,3 +222,23 @@ def test_residual_vs_torch_float64(oracle_lib):
     ref = torch.relu(ref0 + z).numpy()
     got = oracle_lib.conv2d(x, w, b, stride=2, pad=1, residual=z)
     assert np.abs(got - ref).max() < 1e-12
+
+
+def test_fold_batchnorm_closed_form(oracle_lib):
+    """conv(x, w') + b' equals batch-norm applied to conv(x, w) + b, written out directly
+    (gamma * (t - mean) / sqrt(var + eps) + beta per output channel)."""
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((2, 3, 7, 6))
+    w = rng.standard_normal((5, 3, 3, 3))
+    b = rng.standard_normal(5)
+    gamma, beta = rng.standard_normal(5), rng.standard_normal(5)
+    mean, var, eps = rng.standard_normal(5), rng.uniform(0.1, 2.0, 5), 1e-3
+    t = oracle_lib.conv2d(x, w, b, stride=1, pad=1, relu=False)
+    bn = gamma[None, :, None, None] * (t - mean[None, :, None, None]) / np.sqrt(var + eps)[None, :, None, None] \
+        + beta[None, :, None, None]
+    wf, bf = oracle.fold_batchnorm(w, b, gamma, beta, mean, var, eps)
+    got = oracle_lib.conv2d(x, wf, bf, stride=1, pad=1, relu=False)
+    assert np.abs(got - bn).max() < 1e-12
+    # gamma = sqrt(var + eps), beta = mean, b = mean: the identity fold
+    wi, bi = oracle.fold_batchnorm(w, mean, np.sqrt(var + eps), mean, mean, var, eps)
+    assert np.allclose(wi, w, rtol=1e-15, atol=0) and np.allclose(bi, mean, rtol=1e-15, atol=1e-15)
