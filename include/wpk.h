@@ -199,6 +199,19 @@ WPK_API int32_t wpk_conv2d_config_valid(wpk_plan plan, int32_t family, const int
 /* Drop the packed-weight / tensor-map caches (call after mutating weights in place). */
 WPK_API wpk_status wpk_conv2d_invalidate(wpk_plan plan);
 
+/* Inference batch-norm folded into the convolution's weights and bias (constant folding; SURVEY.md
+ * 8(f) NEXT-1b): for  y = gamma * (conv(x, w) + b - mean) / sqrt(var + eps) + beta  it writes
+ *   w_out[k, ...] = w[k, ...] * s_k,   b_out[k] = (b[k] - mean[k]) * s_k + beta[k],
+ *   s_k = gamma[k] / sqrt(var[k] + eps),
+ * computed in fp32 and rounded once to the plan's dtype, so that run(x, w_out, b_out) computes the
+ * conv + BN (+ the plan's epilogue). w / w_out: the plan's weight layout and dtype (w_out may alias
+ * w); b: [K] in the plan's dtype or NULL (= 0); b_out [K] in the plan's dtype; gamma, beta, mean,
+ * var: fp32 [K]. All device pointers, enqueued on `stream` (no sync). Call wpk_conv2d_invalidate
+ * if w_out is a weight buffer the plan has already packed. */
+WPK_API wpk_status wpk_conv2d_fold_batchnorm(wpk_plan plan, const void *w, const void *b, const float *gamma,
+                                             const float *beta, const float *mean, const float *var, float eps,
+                                             void *w_out, void *b_out, void *stream);
+
 /* Describe a family's gene domains: for gene g, domain values are written to
  * values[g*32 .. g*32+counts[g]-1] (at most 32 per gene). names may be NULL. */
 WPK_API wpk_status wpk_family_describe(int32_t family, int32_t *counts, int32_t *values, const char **names);

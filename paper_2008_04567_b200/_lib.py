@@ -94,6 +94,7 @@ def load():
         "wpk_conv2d_tune": (I32, [P, I32, I32, ctypes.POINTER(TuneOptions)]),
         "wpk_conv2d_run": (I32, [P, P, P, P, P, P]),
         "wpk_conv2d_run_residual": (I32, [P, P, P, P, P, P, P]),
+        "wpk_conv2d_fold_batchnorm": (I32, [P, P, P, P, P, P, P, ctypes.c_float, P, P, P]),
         "wpk_conv2d_run_host": (I32, [P, P, P, P, P, P]),
         "wpk_conv2d_run_host_async": (I32, [P, P, P, P, P, P]),
         "wpk_conv2d_destroy": (None, [P]),

@@ -148,6 +148,25 @@ class Conv2dPlan:
                                                    ctypes.c_void_p(y_host.data_ptr()), ctypes.c_void_p(s)))
         return y_host
 
+    def fold_batchnorm(self, w: torch.Tensor, b: torch.Tensor | None, gamma: torch.Tensor, beta: torch.Tensor,
+                       mean: torch.Tensor, var: torch.Tensor, eps: float = 1e-5, w_out: torch.Tensor | None = None,
+                       b_out: torch.Tensor | None = None, stream: torch.cuda.Stream | None = None):
+        """(w', b') with conv(x, w') + b' == BN(conv(x, w) + b) (inference BN; fp32 [K] statistics)."""
+        dt = _TORCH_DT[self.dtype]
+        if w_out is None:
+            w_out = torch.empty_like(w)
+        if b_out is None:
+            b_out = torch.empty(self.k, dtype=dt, device=w.device)
+        f32 = [t.float().contiguous() for t in (gamma, beta, mean, var)]
+        s = (stream or torch.cuda.current_stream(w.device)).cuda_stream
+        bp = ctypes.c_void_p(b.data_ptr()) if b is not None else None
+        L.check(self.lib.wpk_conv2d_fold_batchnorm(self.handle, ctypes.c_void_p(w.data_ptr()), bp,
+                                                   *[ctypes.c_void_p(t.data_ptr()) for t in f32], ctypes.c_float(eps),
+                                                   ctypes.c_void_p(w_out.data_ptr()), ctypes.c_void_p(b_out.data_ptr()),
+                                                   ctypes.c_void_p(s)))
+        self._f32_keep = f32   # alive until the stream has consumed them (next call replaces)
+        return w_out, b_out
+
     def last_launch_count(self) -> int:
         return int(self.lib.wpk_conv2d_last_launch_count(self.handle))
 

@@ -165,6 +165,27 @@ __global__ void pack_seg_kernel(const T *__restrict__ w, T *__restrict__ out, in
         out[i] = v;
     }
 }
+// Batch-norm folding (wpk_conv2d_fold_batchnorm): one thread per weight element, then K bias
+// elements; the output channel k is the outermost index in both KCRS and KRSC.
+template <typename T>
+__global__ void fold_bn_kernel(const T *__restrict__ w, const T *__restrict__ b, const float *__restrict__ gamma,
+                               const float *__restrict__ beta, const float *__restrict__ mean,
+                               const float *__restrict__ var, float eps, T *w_out, T *b_out, int K, long long per_k) {
+    const long long total = (long long)K * per_k;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total + K;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (i < total) {
+            const int k = (int)(i / per_k);
+            const float sk = gamma[k] / sqrtf(var[k] + eps);
+            w_out[i] = T(static_cast<float>(w[i]) * sk);
+        } else {
+            const int k = (int)(i - total);
+            const float sk = gamma[k] / sqrtf(var[k] + eps);
+            const float bk = b ? static_cast<float>(b[k]) : 0.f;
+            b_out[k] = T((bk - mean[k]) * sk + beta[k]);
+        }
+    }
+}
 // Depthwise weights [C][R][S] (both layouts, C/g = 1) -> [R][S][C].
 template <typename T>
 __global__ void pack_rsc_kernel(const T *__restrict__ w, T *__restrict__ out, int C, int R, int S) {
@@ -640,6 +661,34 @@ static wpk_status run_host_impl(wpk_plan plan, const void *x_host, const void *w
         cudaError_t e = cudaGetLastError();
         return fail(WPK_ERR_CUDA, std::string("D2H copy / sync failed: ") + cudaGetErrorString(e));
     }
+    return WPK_OK;
+}
+
+wpk_status wpk_conv2d_fold_batchnorm(wpk_plan plan, const void *w, const void *b, const float *gamma, const float *beta,
+                                     const float *mean, const float *var, float eps, void *w_out, void *b_out,
+                                     void *stream) {
+    if (!plan || !w || !gamma || !beta || !mean || !var || !w_out || !b_out)
+        return fail(WPK_ERR_INVALID_ARGUMENT, "fold_batchnorm: NULL argument");
+    if (!(eps >= 0.f)) return fail(WPK_ERR_INVALID_ARGUMENT, "fold_batchnorm: eps must be >= 0");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    const ConvDesc &d = p->d;
+    const long long per_k = (long long)(d.c / d.g) * d.r * d.s;
+    const long long total = (long long)d.k * per_k + d.k;
+    const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 4096);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (d.dtype == WPK_BF16)
+        fold_bn_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16 *)w, (const __nv_bfloat16 *)b, gamma,
+                                                              beta, mean, var, eps, (__nv_bfloat16 *)w_out,
+                                                              (__nv_bfloat16 *)b_out, d.k, per_k);
+    else if (d.dtype == WPK_F16)
+        fold_bn_kernel<__half><<<blocks, 256, 0, st>>>((const __half *)w, (const __half *)b, gamma, beta, mean, var,
+                                                       eps, (__half *)w_out, (__half *)b_out, d.k, per_k);
+    else
+        fold_bn_kernel<float><<<blocks, 256, 0, st>>>((const float *)w, (const float *)b, gamma, beta, mean, var, eps,
+                                                      (float *)w_out, (float *)b_out, d.k, per_k);
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) return fail(WPK_ERR_CUDA, std::string("fold_batchnorm launch: ") + cudaGetErrorString(ce));
+    if (w_out == p->packed_for) p->packed_for = nullptr;   // folded in place: repack on the next run
     return WPK_OK;
 }
 

@@ -314,3 +314,40 @@ def test_residual_epilogue(dtype, layout):
         assert ran >= 1, L.name
         with pytest.raises(Exception):   # a residual plan refuses the plain run entry point
             plan.run(xl, wl, bc)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
+def test_fold_batchnorm(dtype):
+    """wpk_conv2d_fold_batchnorm vs the oracle's float64 fold: folded weights/bias within one
+    rounding of the dtype, and the folded conv within the dtype tolerance of BN(conv) (oracle)."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import to_layout, from_layout, rel_error
+    L = ConvLayer("bn", 2, 32, 9, 9, 48, 3, 3, 1, 1)
+    x, w, b = workloads.generate(L, dtype, "uniform", seed=51)
+    g = torch.Generator().manual_seed(52)
+    gamma = torch.rand(L.k, generator=g) + 0.5
+    beta = torch.rand(L.k, generator=g) - 0.5
+    mean = torch.rand(L.k, generator=g) - 0.5
+    var = torch.rand(L.k, generator=g) + 0.2
+    eps = 1e-5
+    plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype=dtype)
+    xl, wl = to_layout(x, w, "nhwc")
+    wf, bf = plan.fold_batchnorm(wl.cuda(), b.cuda(), gamma.cuda(), beta.cuda(), mean.cuda(), var.cuda(), eps)
+    torch.cuda.synchronize()
+    wo, bo = oracle.fold_batchnorm(w, b, gamma, beta, mean, var, eps)
+    # one rounding of the dtype (bf16/f16), or a few fp32 ulps of the fp32 fold (s_k then w * s_k)
+    ulp = {"f32": 2.0 ** -21, "bf16": 2.0 ** -7, "f16": 2.0 ** -10}[dtype]
+    wf_nchw = wf.permute(0, 3, 1, 2).cpu().double().numpy()
+    tiny = {"f32": 2.0 ** -149, "bf16": 2.0 ** -133, "f16": 2.0 ** -24}[dtype]   # subnormal spacing
+    assert np.all(np.abs(wf_nchw - wo) <= 1.01 * ulp * np.abs(wo) + tiny)
+    # b' = (b - mean) s + beta can cancel: bound by the magnitude of its terms (two fp32 roundings
+    # inside, one rounding of the dtype at the end)
+    sk = gamma.double().numpy() / np.sqrt(var.double().numpy() + eps)
+    mag = np.abs(b.double().numpy() - mean.double().numpy()) * sk + np.abs(beta.double().numpy())
+    assert np.all(np.abs(bf.cpu().double().numpy() - bo) <= 1.01 * ulp * mag + 4 * 2.0 ** -24 * mag + tiny)
+    y = plan.run(xl.cuda(), wf, bf)
+    torch.cuda.synchronize()
+    t = oracle.conv2d(x, w, b, stride=1, pad=1, relu=False)
+    ref = np.maximum(gamma.double().numpy()[None, :, None, None] * (t - mean.double().numpy()[None, :, None, None])
+                     / np.sqrt(var.double().numpy() + eps)[None, :, None, None] + beta.double().numpy()[None, :, None, None], 0)
+    assert rel_error(dtype, from_layout(y.cpu(), "nhwc"), ref) <= TOL[dtype]
