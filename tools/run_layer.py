@@ -14,6 +14,9 @@ L = next(l for l in getattr(workloads, net)(batch) if l.name == name)
 plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype=os.environ.get("DT", "bf16"))
 if len(sys.argv) > 2:
     plan.set_config(1, [int(v) for v in sys.argv[2:9]])
+elif os.environ.get("CFG_JSON"):   # the layer's config from a bench --configs-out file
+    import json
+    plan.set_config(*json.load(open(os.environ["CFG_JSON"]))[name])
 x, w, b = workloads.generate(L, plan.dtype, "uniform", seed=1)
 xd = x.permute(0, 2, 3, 1).contiguous().cuda(); wd = w.permute(0, 2, 3, 1).contiguous().cuda(); bd = b.cuda()
 y = torch.empty(plan.y_shape(), dtype=xd.dtype, device="cuda")

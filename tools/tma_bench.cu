@@ -86,11 +86,11 @@ int main(int argc, char **argv) {
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill))fn;
     cudaFuncSetAttribute(tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     printf("rows stages grid  GB/s   B/clk/SM(at %s)\n", "clock64");
-    for (int wm : {0, 1})
-    for (int P : {1})
+    for (int wm : {0})
+    for (int P : {1, 2, 4})
     for (int nb : {1})
     for (int rows : {64, 128, 256}) {
-        for (int stages : {1, 2, 4, 6}) {
+        for (int stages : {2, 4, 6}) {
             if ((size_t)P * stages * rows * 128 * nb + 4096 > 227 * 1024) continue;
             for (int grid : {sms}) {
                 CUtensorMap tm;
