@@ -4,6 +4,7 @@ Exact-integer mode (x, w in {-1,0,1}, b in {-4..4}) must be bit-exact on every p
 (reading c11); uniform mode must meet BASELINE.json's tolerances: fp32 max-rel 1e-5, TF32
 normwise 5e-3, bf16/fp16 normwise 2e-2."""
 import itertools
+import os
 
 import numpy as np
 import pytest
@@ -268,6 +269,30 @@ def test_resnet50_n32_sampled_bf16(layer):
     got = y[pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
     want = torch.from_numpy(ref).to(torch.bfloat16)
     assert torch.equal(got.float() + 0, want.float() + 0)
+
+
+_TUNED = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r1d_tuned_configs.json")
+
+
+@pytest.mark.parametrize("layer", workloads.resnet50(32), ids=lambda l: l.name)
+def test_resnet50_n32_bench_configs_sampled(layer):
+    """The configs the bench tuned (profiles/r1d_tuned_configs.json, committed): full-size layer,
+    uniform inputs, sampled outputs vs the oracle within the bf16 tolerance; plus exact-integer
+    inputs bit-exact on the same samples."""
+    import json
+    cfgs = json.load(open(_TUNED))
+    fam, genes = cfgs[layer.name]
+    for mode in ("int", "uniform"):
+        x, w, b = workloads.generate(layer, "bf16", mode, seed=workloads.config_seed(1, 1))
+        y, plan = run_product(layer, "bf16", "nhwc", x, w, b, config=(fam, genes))
+        pts = workloads.random_points(layer, plan.p, plan.q, 4096, seed=2).numpy()
+        ref = oracle.conv2d_points(x, w, b, pts, stride=layer.stride, pad=layer.pad, nthreads=8)
+        got = y[pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
+        if mode == "int":
+            assert torch.equal(got.float() + 0, torch.from_numpy(ref).to(torch.bfloat16).float() + 0)
+        else:
+            err = np.linalg.norm(got.double().numpy() - ref) / max(np.linalg.norm(ref), 1e-30)
+            assert err <= TOL["bf16"], err
 
 
 def _residual_case(L, dtype, layout, seed):
