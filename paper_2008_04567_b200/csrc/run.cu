@@ -508,7 +508,7 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     U.C = (g.a_mode == 3) ? 4 : d.c;                          // channels per stored pixel
     if (g.a_mode == 3) { U.H = g.seg_hp; U.W = g.seg_wp; }    // the gather walks the padded image
     U.x_nchw = (g.a_mode == 3) ? 0 : (d.layout == WPK_NCHW);
-    U.dbg = g_debug_timeline;
+    U.dbg = p.dbg ? p.dbg : g_debug_timeline;
     if (!p.map_cache) p.map_cache = new UmmaMapCache();
     U.cache = static_cast<UmmaMapCache *>(p.map_cache);
     U.cfg = cfg;
@@ -554,6 +554,10 @@ extern "C" {
 // Debug hook (not part of include/wpk.h): per-CTA kernel timeline into a device buffer.
 __attribute__((visibility("default"))) void wpk_debug_set_timeline(void *dev_buf) {
     g_debug_timeline = static_cast<unsigned long long *>(dev_buf);
+}
+// Debug hook: timeline buffer of one plan's launches (148 x 64 u64), e.g. all convs of a step graph.
+__attribute__((visibility("default"))) void wpk_debug_set_plan_timeline(wpk_plan plan, void *dev_buf) {
+    if (plan) reinterpret_cast<Plan *>(plan)->dbg = static_cast<unsigned long long *>(dev_buf);
 }
 
 wpk_status wpk_conv2d_workspace_size(wpk_plan plan, size_t *bytes) {

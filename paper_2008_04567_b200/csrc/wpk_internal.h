@@ -109,6 +109,7 @@ struct Plan {
     int packed_cfg_family = -1;
     int last_launches = 0;
     void *map_cache = nullptr;   // UmmaMapCache (umma_conv.h)
+    unsigned long long *dbg = nullptr;   // per-plan kernel timeline (tools only; overrides the global)
     char *counters_at = nullptr; // split-K counters known to be zero at this address
     size_t counters_bytes = 0;
     // tune stats
