@@ -376,3 +376,44 @@ def test_fold_batchnorm(dtype):
     ref = np.maximum(gamma.double().numpy()[None, :, None, None] * (t - mean.double().numpy()[None, :, None, None])
                      / np.sqrt(var.double().numpy() + eps)[None, :, None, None] + beta.double().numpy()[None, :, None, None], 0)
     assert rel_error(dtype, from_layout(y.cpu(), "nhwc"), ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_shapes_random_configs(case):
+    """Seeded random shapes (N, C, H, W, K, R, S, stride, pad, dilation, groups in {1, C}, layout,
+    dtype) x the plan's default config and 3 random valid configs of its family: exact-integer
+    inputs, bit-exact against the oracle."""
+    from paper_2008_04567_b200 import Conv2dPlan, _lib as L
+    from _util import to_layout, from_layout
+    rng = np.random.default_rng(9000 + case)
+    dtype = ["f32", "tf32", "bf16", "f16"][case % 4]
+    layout = ["nhwc", "nchw"][(case // 4) % 2]
+    dw = case % 6 == 5
+    c = int(rng.choice([3, 8, 16, 64, 96, 128]))
+    k = c if dw else int(rng.choice([8, 24, 64, 80, 128, 200]))
+    r, s = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+    st, pd, dl = int(rng.integers(1, 3)), int(rng.integers(0, 3)), int(rng.integers(1, 3))
+    h = dl * (r - 1) + 1 + int(rng.integers(0, 12))
+    w_ = dl * (s - 1) + 1 + int(rng.integers(0, 12))
+    n = int(rng.integers(1, 4))
+    Lc = ConvLayer(f"rand{case}", n, c, h, w_, k, r, s, st, pd, dl, c if dw else 1)
+    x, w, b = workloads.generate(Lc, dtype, "int", seed=case)
+    ref = oracle_full(Lc, x, w, b)
+    plan = Conv2dPlan(Lc.n, Lc.c, Lc.h, Lc.w, Lc.k, Lc.r, Lc.s, Lc.stride, Lc.pad, Lc.dil, Lc.groups,
+                      layout=layout, dtype=dtype)
+    xl, wl = to_layout(x, w, layout)
+    xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
+    fam = plan.config[0]
+    names, doms = L.family_describe(["simt", "umma", "dw"][fam])
+    configs = [plan.config]
+    tries = 0
+    while len(configs) < 4 and tries < 400:
+        tries += 1
+        genes = [int(rng.choice(d)) for d in doms]
+        if plan.config_valid(fam, genes):
+            configs.append((fam, genes))
+    for fam_, genes in configs:
+        plan.set_config(fam_, list(genes))
+        y = plan.run(xl, wl, bc)
+        torch.cuda.synchronize()
+        assert_bit_exact(from_layout(y.cpu(), layout), ref)
