@@ -15,6 +15,7 @@ NCCL all-gather of fitness records (paper_2008_04567_b200/dist.py).
 from __future__ import annotations
 
 import argparse
+import tempfile
 import json
 import os
 import statistics
@@ -152,6 +153,73 @@ def run_reference(args):
 # -------------------------------------------------------------------------------------------------
 # WPK arm
 # -------------------------------------------------------------------------------------------------
+def _step_ms(units, stream, pg, reps=12):
+    """Device time of one whole-step graph replay (max over ranks), for graph refinement."""
+    import torch
+    with torch.cuda.stream(stream):
+        for (i, plan, xd, wd, bd, yd) in units:   # packs weights / sizes workspaces for new configs
+            plan.run(xd, wd, bd, yd, stream=stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for (i, plan, xd, wd, bd, yd) in units:
+            plan.run(xd, wd, bd, yd, stream=stream)
+    with torch.cuda.stream(stream):
+        g.replay()
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    if pg is not None:
+        t = torch.tensor([ms], device=torch.cuda.current_device())
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    del g
+    return ms
+
+
+def graph_refine(args, layers, plans, units, records, stream, pg):
+    """System-level refinement after the per-operator search (implementations are
+    selected per operator, here in the context of the whole graph): the tuner times each candidate
+    alone, but inside the step graph a conv's config also decides how early the next conv's CTAs
+    start on idle SMs (programmatic dependent launch). For each layer, in order, the next-best
+    measured configs (top --graph-refine by the tuner's beta) are tried in the whole-step graph and
+    kept if the step gets >= 0.5% faster (timings max-reduced over ranks, so every rank decides the
+    same)."""
+    base = _step_ms(units, stream, pg)
+    tried, changed = 0, []
+    for i, L in enumerate(layers):
+        path = records.get(i)
+        if not path or not os.path.exists(path):
+            continue
+        recs = [json.loads(l) for l in open(path) if l.strip()]
+        recs = [r for r in recs if r.get("beta_us") is not None and r["beta_us"] < 1e30]
+        recs.sort(key=lambda r: r["beta_us"])
+        cur = (plans[i].config[0], list(plans[i].config[1]))
+        alts, seen = [], {(cur[0], tuple(cur[1]))}
+        for r in recs:
+            key = (r["family"], tuple(r["genes"]))
+            if key not in seen:
+                seen.add(key)
+                alts.append(key)
+            if len(alts) >= args.graph_refine:
+                break
+        for fam, genes in alts:
+            plans[i].set_config(fam, list(genes))
+            t = _step_ms(units, stream, pg)
+            tried += 1
+            if t < base * 0.995:
+                base, cur = t, (fam, list(genes))
+                changed.append(L.name)
+        plans[i].set_config(cur[0], list(cur[1]))
+        os.remove(path)
+    return {"tried": tried, "changed": changed, "step_ms_after": base}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -160,6 +228,8 @@ def main():
     ap.add_argument("--impl", default="wpk", choices=["wpk", "reference"])
     ap.add_argument("--batch", type=int, default=32, help="images per GPU")
     ap.add_argument("--tune-budget", type=int, default=64, help="distinct configs measured per unique layer")
+    ap.add_argument("--graph-refine", type=int, default=3,
+                    help="after the search, try each layer's next-best N measured configs in the whole-step graph")
     ap.add_argument("--ga-pop", type=int, default=12,
                     help="GA population (profiles/r1c_search_compare.md: with the paper's 48 a budget of 48 is "
                          "one random generation; 12 gives ~5 generations at budget 64)")
@@ -202,6 +272,7 @@ def main():
     units = []           # one entry per conv of the network (53), sharing the layer's plan
     plans = []
     tune_info = []
+    records = {}         # layer index -> the tuner's measurement records (graph refinement)
     for i, L in enumerate(layers):
         plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups, layout="nhwc",
                           dtype="bf16", device=local)
@@ -212,6 +283,12 @@ def main():
             ex = wdist.make_exchange(pg) if world > 1 else {}
             if args.search == "ga":   # population 12 -> several generations within the budget
                 ex.update(ga_pop=args.ga_pop, ga_pool=args.ga_pop, ga_elites=2)
+            if args.graph_refine > 0 and world == 1:   # records are written by rank 0 only
+                rec = os.path.join(tempfile.gettempdir(), f"wpk_bench_rec_{os.getpid()}_{i}.jsonl")
+                if os.path.exists(rec):
+                    os.remove(rec)
+                ex["record_path"] = rec
+                records[i] = rec
             res = plan.tune(args.search, args.tune_budget, seed=i, rank=rank, world=world, **ex)
             tune_info.append({"layer": L.name, "best_us": res.best_us, "measured": res.measured,
                               "family": res.family, "genes": res.genes})
@@ -224,6 +301,7 @@ def main():
             yd = torch.empty(plan.y_shape(), dtype=torch.bfloat16, device=dev)
             units.append((i, plan, xd, wd, bd, yd))
     torch.cuda.synchronize()
+    refine_info = graph_refine(args, layers, plans, units, records, stream, pg) if records else None
     tune_seconds = time.perf_counter() - t_tune0
     if args.configs_out and rank == 0:
         json.dump({L.name: list(plans[i].config) for i, L in enumerate(layers)}, open(args.configs_out, "w"))
@@ -465,6 +543,7 @@ def main():
                     "how": "wpk_conv2d_run_host_async per conv on 3 round-robin streams (pinned host x in, host y out)"},
             "gpu_launches": launches,
             "tuning_seconds": tune_seconds,
+            "graph_refine": refine_info,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "layers": table,
