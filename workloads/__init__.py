@@ -85,6 +85,30 @@ def resnet50(n: int = 32) -> list[ConvLayer]:
     return _rn50(n)
 
 
+def resnet18(n: int = 1) -> list[ConvLayer]:
+    """The 11 unique ResNet-18 conv shapes (20 convs with multiplicity) -- the network of the
+    paper's per-convolution comparison (SURVEY.md 8(f) NEXT-3b; the paper labels
+    them C1-C12 as TVM does). torchvision layout: stride on the first 3x3 of a stage, 1x1
+    stride-2 downsample."""
+    L = ConvLayer
+    rows = [
+        # name,      C,   H,   K,  R, stride, pad, count
+        ("conv1",     3, 224,  64, 7, 2, 3, 1),
+        ("s2.c",     64,  56,  64, 3, 1, 1, 4),
+        ("s3b0.c1",  64,  56, 128, 3, 2, 1, 1),
+        ("s3b0.ds",  64,  56, 128, 1, 2, 0, 1),
+        ("s3.c",    128,  28, 128, 3, 1, 1, 3),
+        ("s4b0.c1", 128,  28, 256, 3, 2, 1, 1),
+        ("s4b0.ds", 128,  28, 256, 1, 2, 0, 1),
+        ("s4.c",    256,  14, 256, 3, 1, 1, 3),
+        ("s5b0.c1", 256,  14, 512, 3, 2, 1, 1),
+        ("s5b0.ds", 256,  14, 512, 1, 2, 0, 1),
+        ("s5.c",    512,   7, 512, 3, 1, 1, 3),
+    ]
+    out = [L(nm, n, c, h, h, k, r, r, st, p, 1, 1, cnt) for (nm, c, h, k, r, st, p, cnt) in rows]
+    return out
+
+
 def vgg16(n: int = 64) -> list[ConvLayer]:
     rows = [("conv1_1", 3, 224, 64, 1), ("conv1_2", 64, 224, 64, 1),
             ("conv2_1", 64, 112, 128, 1), ("conv2_2", 128, 112, 128, 1),
