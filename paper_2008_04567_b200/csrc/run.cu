@@ -325,13 +325,32 @@ struct WsLayout {
 
 static size_t al256(size_t v) { return (v + 255) / 256 * 256; }
 
-static WsLayout ws_layout(const ConvDesc &d, const Config &cfg, bool host_staging) {
+int env_knob(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+// The plan's cached UMMA geometry for cfg (derived once per config change).
+static bool plan_geom(Plan &p, const Config &cfg, UmmaGeom *out, std::string *why) {
+    if (!(p.geom_ok && p.geom_cfg == cfg)) {
+        UmmaGeom g;
+        if (!umma_geometry(p.d, cfg, &g, why)) return false;
+        p.geom = g;
+        p.geom_cfg = cfg;
+        p.geom_ok = true;
+    }
+    *out = p.geom;
+    return true;
+}
+
+static WsLayout ws_layout(Plan &p, const Config &cfg, bool host_staging) {
+    const ConvDesc &d = p.d;
     WsLayout L;
     const size_t e = d.elem();
     size_t off = 0;
     if (cfg.family == WPK_FAMILY_UMMA) {
         UmmaGeom g;
-        umma_geometry(d, cfg, &g, nullptr);
+        if (!plan_geom(p, cfg, &g, nullptr)) return L;
         if (g.a_mode == 1) {
             L.x_off = off; L.x_bytes = al256((size_t)d.M() * g.cpad * e); off += L.x_bytes;
             L.w_off = off; L.w_bytes = al256((size_t)d.k * g.cpad * e); off += L.w_bytes;
@@ -359,8 +378,8 @@ static WsLayout ws_layout(const ConvDesc &d, const Config &cfg, bool host_stagin
     return L;
 }
 
-size_t workspace_bytes(const Plan &p, const Config &cfg, bool host_staging) {
-    return ws_layout(p.d, cfg, host_staging).total;
+size_t workspace_bytes(Plan &p, const Config &cfg, bool host_staging) {
+    return ws_layout(p, cfg, host_staging).total;
 }
 
 // ---- one run ------------------------------------------------------------------------------------------
@@ -369,7 +388,7 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     const ConvDesc &d = p.d;
     cudaStream_t st = (cudaStream_t)stream;
     const int sm = device_sm_count(p.device);
-    WsLayout L = ws_layout(d, cfg, false);
+    WsLayout L = ws_layout(p, cfg, false);
     if (L.total > ws_bytes) {
         set_error("workspace too small: need " + std::to_string(L.total) + " bytes");
         return -1;
@@ -435,7 +454,7 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     // ---- UMMA family ----
     UmmaGeom g;
     std::string why;
-    if (!umma_geometry(d, cfg, &g, &why)) { set_error("invalid UMMA config: " + why); return -1; }
+    if (!plan_geom(p, cfg, &g, &why)) { set_error("invalid UMMA config: " + why); return -1; }
     const void *xk = x, *wk = w;
     const int pack_kind = WPK_FAMILY_UMMA * 10 + g.a_mode;
     if (g.a_mode == 3) {
@@ -502,7 +521,8 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     U.N = d.n; U.H = d.h; U.W = d.w; U.K = d.k; U.R = d.r; U.S = d.s; U.P = d.p; U.Q = d.q;
     U.stride_h = d.sh; U.stride_w = d.sw; U.pad_h = d.ph; U.pad_w = d.pw; U.dil_h = d.dh; U.dil_w = d.dw;
     U.epilogue = d.epilogue; U.out_nchw = d.layout == WPK_NCHW; U.sm_count = sm; U.stream = stream; U.g = g;
-    if (getenv("WPK_GRID_CAP")) U.sm_count = std::min(sm, atoi(getenv("WPK_GRID_CAP")));   // experiments only
+    static const int grid_cap = env_knob("WPK_GRID_CAP", 0);   // experiments only
+    if (grid_cap > 0) U.sm_count = std::min(sm, grid_cap);
     U.a_rows = (g.a_mode == 1) ? d.M() : (long long)d.n * d.h * d.w;
     U.b_rs = (g.a_mode >= 1) ? 1 : d.r * d.s;
     U.C = (g.a_mode == 3) ? 4 : d.c;                          // channels per stored pixel
@@ -648,7 +668,7 @@ static wpk_status run_host_impl(wpk_plan plan, const void *x_host, const void *w
     const ConvDesc &d = p->d;
     char *ws;
     size_t bytes;
-    WsLayout L = ws_layout(d, p->cfg, true);
+    WsLayout L = ws_layout(*p, p->cfg, true);
     wpk_status st = ensure_ws(p, L.total, &ws, &bytes);
     if (st != WPK_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;

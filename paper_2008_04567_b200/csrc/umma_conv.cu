@@ -62,7 +62,8 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
     }
     const UmmaGeom &g = L.g;
     // two A-issuing threads: measured no faster on the ResNet-50 layers, opt-in only
-    const int a_split = (g.a_mode <= 1 && getenv("WPK_ASPLIT")) ? 1 : 0;
+    static const int asplit_knob = env_knob("WPK_ASPLIT", 0);
+    const int a_split = (g.a_mode <= 1 && asplit_knob) ? 1 : 0;
     const int a_box_rows = (g.pair ? 128 : g.bm) >> a_split;
     CUtensorMap tmA, tmB, tmY, tmP;
     UmmaMapCache *mc = L.cache;
@@ -190,7 +191,8 @@ launch:
     a.recv_stride = g.recv_stride;
     a.a_split = a_split;
     a.z = L.z;
-    a.dbg_flags = getenv("WPK_DBG_FLAGS") ? atoi(getenv("WPK_DBG_FLAGS")) : 0;
+    static const int dbg_flags = env_knob("WPK_DBG_FLAGS", 0);
+    a.dbg_flags = dbg_flags;
     cudaStream_t st = (cudaStream_t)L.stream;
     long long grid = (long long)L.sm_count * g.ctas_per_sm;
     if (grid > g.work) grid = g.work;
@@ -205,7 +207,8 @@ launch:
     lc.stream = st;
     cudaLaunchAttribute attr[2];
     int nattr = 0;
-    if (!getenv("WPK_NO_PDL")) {
+    static const int no_pdl = env_knob("WPK_NO_PDL", 0) || getenv("WPK_NO_PDL") != nullptr;
+    if (!no_pdl) {
         attr[nattr].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[nattr].val.programmaticStreamSerializationAllowed = 1;
         ++nattr;

@@ -88,11 +88,13 @@ struct Workspace {
 };
 
 struct Plan;
-size_t workspace_bytes(const Plan &p, const Config &cfg, bool host_staging);
+size_t workspace_bytes(Plan &p, const Config &cfg, bool host_staging);
 // Launch everything for one run on `stream`; returns number of kernel launches or -1 (error set).
 int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const void *b, void *y,
                 void *stream, char *ws, size_t ws_bytes, const void *z = nullptr);
 int device_sm_count(int device);
+// environment knob read once per process (experiments and debugging only)
+int env_knob(const char *name, int dflt);
 int device_l2_bytes(int device);
 
 struct Plan {
@@ -110,6 +112,11 @@ struct Plan {
     int last_launches = 0;
     void *map_cache = nullptr;   // UmmaMapCache (umma_conv.h)
     unsigned long long *dbg = nullptr;   // per-plan kernel timeline (tools only; overrides the global)
+    // UMMA geometry of the last config launched (host-side cost of a run: one comparison, not a
+    // re-derivation; WPK_* environment knobs are therefore read when a config is first used)
+    Config geom_cfg;
+    UmmaGeom geom;
+    bool geom_ok = false;
     char *counters_at = nullptr; // split-K counters known to be zero at this address
     size_t counters_bytes = 0;
     // tune stats
