@@ -124,28 +124,31 @@ __global__ void pack_flat_kernel(const T *__restrict__ w, T *__restrict__ out, i
 // (ph, pw) of an Hp x Wp zero canvas, channels >= C zero. Grid (column blocks, N*Hp rows, copies):
 // one thread per padded pixel, no divisions. The second copy (odd stride, 16-bit) is shifted right
 // by one pixel.
-template <typename T>
-__global__ void seg_pad_kernel(const T *__restrict__ x, T *__restrict__ out, int N, int C, int H, int W, int Hp,
-                               int Wp, int ph, int pw, int nchw) {
-    const int wq = blockIdx.x * blockDim.x + threadIdx.x;
-    if (wq >= Wp) return;
+template <typename T, int CC>
+__global__ void seg_pad_kernel(const T *__restrict__ x, T *__restrict__ out, int N, int H, int W, int Hp, int Wp,
+                               int ph, int pw, int nchw) {
     const int nh = blockIdx.y;                      // n * Hp + hq
     const int shift = blockIdx.z;
     const int n = nh / Hp, hq = nh - n * Hp;
-    const int h = hq - ph, w = wq - pw - shift;
-    T v[4] = {T(0.f), T(0.f), T(0.f), T(0.f)};
-    if (h >= 0 && h < H && w >= 0 && w < W) {
-        for (int c = 0; c < C; ++c)
-            v[c] = nchw ? x[(((long long)n * C + c) * H + h) * W + w] : x[(((long long)n * H + h) * W + w) * C + c];
-    }
-    const long long i = ((long long)shift * N * Hp + nh) * Wp + wq;
-    if constexpr (sizeof(T) == 2) {
-        uint2 u;
-        u.x = (uint32_t)(*reinterpret_cast<uint16_t *>(&v[0])) | ((uint32_t)(*reinterpret_cast<uint16_t *>(&v[1])) << 16);
-        u.y = (uint32_t)(*reinterpret_cast<uint16_t *>(&v[2])) | ((uint32_t)(*reinterpret_cast<uint16_t *>(&v[3])) << 16);
-        reinterpret_cast<uint2 *>(out)[i] = u;
-    } else {
-        reinterpret_cast<float4 *>(out)[i] = make_float4(v[0], v[1], v[2], v[3]);
+    const int h = hq - ph;
+    const bool hok = h >= 0 && h < H;
+    const long long orow = ((long long)shift * N * Hp + nh) * Wp;
+    for (int wq = blockIdx.x * blockDim.x + threadIdx.x; wq < Wp; wq += gridDim.x * blockDim.x) {
+        const int w = wq - pw - shift;
+        T v[4] = {T(0.f), T(0.f), T(0.f), T(0.f)};
+        if (hok && w >= 0 && w < W) {
+#pragma unroll
+            for (int c = 0; c < CC; ++c)
+                v[c] = nchw ? x[(((long long)n * CC + c) * H + h) * W + w] : x[(((long long)n * H + h) * W + w) * CC + c];
+        }
+        if constexpr (sizeof(T) == 2) {
+            uint2 u;
+            u.x = (uint32_t)(*reinterpret_cast<uint16_t *>(&v[0])) | ((uint32_t)(*reinterpret_cast<uint16_t *>(&v[1])) << 16);
+            u.y = (uint32_t)(*reinterpret_cast<uint16_t *>(&v[2])) | ((uint32_t)(*reinterpret_cast<uint16_t *>(&v[3])) << 16);
+            reinterpret_cast<uint2 *>(out)[orow + wq] = u;
+        } else {
+            reinterpret_cast<float4 *>(out)[orow + wq] = make_float4(v[0], v[1], v[2], v[3]);
+        }
     }
 }
 // Weights for the pixel-segment gather (A_MODE 3): out[k][(r*Sp + s)*4 + c], zero for s >= S, c >= C
@@ -210,8 +213,17 @@ template <typename T>
 static void launch_aux_t(int which, const void *src, void *dst, const ConvDesc &d, int cp, int sm, cudaStream_t st,
                          int sp) {
     if (which == 7 || which == 8)   // 8: two copies; cp = padded height, sp = padded width
-        seg_pad_kernel<T><<<dim3((sp + 127) / 128, d.n * cp, which - 6), 128, 0, st>>>(
-            (const T *)src, (T *)dst, d.n, d.c, d.h, d.w, cp, sp, d.ph, d.pw, d.layout == WPK_NCHW);
+    {   // one block per padded row (cp = padded height, sp = padded width), channels unrolled
+        const dim3 grid(1, d.n * cp, which - 6);
+        const int thr = std::min(256, (sp + 31) / 32 * 32);
+        const T *xs = (const T *)src;
+        T *o = (T *)dst;
+        const int nchw = d.layout == WPK_NCHW;
+        if (d.c == 1) seg_pad_kernel<T, 1><<<grid, thr, 0, st>>>(xs, o, d.n, d.h, d.w, cp, sp, d.ph, d.pw, nchw);
+        else if (d.c == 2) seg_pad_kernel<T, 2><<<grid, thr, 0, st>>>(xs, o, d.n, d.h, d.w, cp, sp, d.ph, d.pw, nchw);
+        else if (d.c == 3) seg_pad_kernel<T, 3><<<grid, thr, 0, st>>>(xs, o, d.n, d.h, d.w, cp, sp, d.ph, d.pw, nchw);
+        else seg_pad_kernel<T, 4><<<grid, thr, 0, st>>>(xs, o, d.n, d.h, d.w, cp, sp, d.ph, d.pw, nchw);
+    }
     else if (which == 6)
         pack_seg_kernel<T><<<grid_for((long long)d.k * cp, sm), 256, 0, st>>>((const T *)src, (T *)dst, d.k, d.c, d.r,
                                                                               d.s, sp, cp, d.layout == WPK_NCHW);
