@@ -79,8 +79,13 @@ typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 
  *                     tiles for 1x1/s1/p0), 1 = explicit im2col matrix in the workspace,
  *                     2 = fused gather producer (im2col built in shared memory; small-C layers)
  *   WPK_FAMILY_DW   : depthwise (groups == C == K), genes = (VEC_C, PIX_PER_THREAD, THREADS,
- *                     -, -, -, -)                                                      */
-typedef enum { WPK_FAMILY_SIMT = 0, WPK_FAMILY_UMMA = 1, WPK_FAMILY_DW = 2, WPK_FAMILY_AUTO = -1 } wpk_family;
+ *                     -, -, -, -)
+ *   WPK_FAMILY_GEMM32 : exact-fp32 implicit GEMM on CUDA cores (WPK_F32, groups == 1), genes =
+ *                     (BLOCK_M, BLOCK_N, BLOCK_K, THREAD_TILE, SPLIT_K, -, -); the F32 default;
+ *                     SPLIT_K > 1 sums per-split fp32 partials in split order (deterministic) */
+typedef enum {
+    WPK_FAMILY_SIMT = 0, WPK_FAMILY_UMMA = 1, WPK_FAMILY_DW = 2, WPK_FAMILY_GEMM32 = 3, WPK_FAMILY_AUTO = -1
+} wpk_family;
 
 /* Operator shape: the first 9 entries of the paper's O_conv generalised with
  * explicit symmetric padding, dilation and groups (reading c2, c4). */

@@ -26,7 +26,7 @@ LAYOUTS = {"nchw": 0, "nhwc": 1}
 EPILOGUES = {"none": 0, "bias": 1, "bias_relu": 2, "bias_add_relu": 3}
 SEARCHES = {"ga": 0, "rl": 1, "random": 2}
 EVAL_MODES = {"measured": 0, "replay": 1, "synthetic": 2}
-FAMILIES = {"simt": 0, "umma": 1, "dw": 2, "auto": -1}
+FAMILIES = {"simt": 0, "umma": 1, "dw": 2, "gemm32": 3, "auto": -1}
 
 
 class WpkError(RuntimeError):

@@ -73,6 +73,9 @@ static Space make_space(int family) {
         sp.dom = {{16, 32, 64, 96, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8}, {1, 2, 4, 8, 16},
                   {0, 1, 2, 3}, {0, 1, 2, 3}, {1, 2, 4}, {128, 256}};
         sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "MODE", "A_MODE", "ACC_STAGES", "BLOCK_M"};
+    } else if (family == WPK_FAMILY_GEMM32) {
+        sp.dom = {{64, 128}, {64, 128}, {8, 16}, {4, 8}, {1, 2, 4, 8}, {0}, {0}};
+        sp.names = {"BLOCK_M", "BLOCK_N", "BLOCK_K", "THREAD_TILE", "SPLIT_K", "-", "-"};
     } else {
         sp.dom = {{1, 2, 4, 8}, {1, 2, 4}, {64, 128, 256, 512}, {1}, {0}, {0}, {0}};
         sp.names = {"VEC_C", "PIX_PER_THREAD", "THREADS", "-", "-", "-", "-"};
@@ -81,8 +84,8 @@ static Space make_space(int family) {
 }
 
 const Space &family_space(int family) {
-    static const Space spaces[3] = {make_space(0), make_space(1), make_space(2)};
-    return spaces[family < 0 || family > 2 ? 0 : family];
+    static const Space spaces[4] = {make_space(0), make_space(1), make_space(2), make_space(3)};
+    return spaces[family < 0 || family > 3 ? 0 : family];
 }
 
 static bool in_domain(const Space &sp, const Config &cfg, std::string *why) {
@@ -101,6 +104,11 @@ bool family_applicable(const ConvDesc &d, int family, std::string *why) {
     if (family == WPK_FAMILY_SIMT) return true;   // the SIMT kernel handles every valid shape, layout and dtype
     if (family == WPK_FAMILY_DW) {
         if (!(d.g == d.c && d.g == d.k && d.g > 1)) return no("DW family needs groups == C == K");
+        return true;
+    }
+    if (family == WPK_FAMILY_GEMM32) {
+        if (d.dtype != WPK_F32) return no("GEMM32 family is the exact-fp32 path (dtype F32)");
+        if (d.g != 1) return no("GEMM32 family needs groups == 1");
         return true;
     }
     if (family == WPK_FAMILY_UMMA) {
@@ -238,7 +246,7 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
 }
 
 bool config_valid(const ConvDesc &d, const Config &cfg, std::string *why) {
-    if (cfg.family < 0 || cfg.family > 2) { if (why) *why = "bad family"; return false; }
+    if (cfg.family < 0 || cfg.family > 3) { if (why) *why = "bad family"; return false; }
     if (!family_applicable(d, cfg.family, why)) return false;
     if (!in_domain(family_space(cfg.family), cfg, why)) return false;
     const int *gn = cfg.genes;
@@ -261,6 +269,16 @@ bool config_valid(const ConvDesc &d, const Config &cfg, std::string *why) {
         UmmaGeom g;
         return umma_geometry(d, cfg, &g, why);
     }
+    if (cfg.family == WPK_FAMILY_GEMM32) {
+        if ((d.k + gn[1] - 1) / gn[1] > 65535) { if (why) *why = "grid y exceeds 65535"; return false; }
+        const int nk = (d.r * d.s * round_up(d.c, 4) + gn[2] - 1) / gn[2];
+        if (gn[4] > 1 && (gn[4] > nk || (long long)(gn[4] - 1) * ((nk + gn[4] - 1) / gn[4]) >= nk)) {
+            if (why) *why = "SPLIT_K leaves an empty split";
+            return false;
+        }
+        if (gn[4] > 1 && (double)gn[4] * d.M() * d.k * 4 > 8.0e9) { if (why) *why = "split-K partials exceed 8 GB"; return false; }
+        return true;
+    }
     // DW
     int vec = gn[0];
     if (d.c % vec) { if (why) *why = "VEC_C must divide C"; return false; }
@@ -272,6 +290,7 @@ bool config_valid(const ConvDesc &d, const Config &cfg, std::string *why) {
 int default_family(const ConvDesc &d) {
     if (d.g > 1 && d.g == d.c && d.g == d.k) return WPK_FAMILY_DW;
     if (family_applicable(d, WPK_FAMILY_UMMA, nullptr)) return WPK_FAMILY_UMMA;
+    if (family_applicable(d, WPK_FAMILY_GEMM32, nullptr)) return WPK_FAMILY_GEMM32;
     return WPK_FAMILY_SIMT;
 }
 
@@ -280,6 +299,12 @@ Config default_config(const ConvDesc &d, int family) {
     c.family = family;
     if (family == WPK_FAMILY_SIMT) {
         int g[7] = {16, 4, 4, 1, 1, 1, 1};
+        std::memcpy(c.genes, g, sizeof g);
+        return c;
+    }
+    if (family == WPK_FAMILY_GEMM32) {
+        // 128 x 128 CTA tiles of 8 x 8 outputs per thread; 64-wide for narrow layers
+        int g[7] = {64, 64, 16, 4, 1, 0, 0};   // the measured best on most ResNet-50 layers (profiles/r1e)
         std::memcpy(c.genes, g, sizeof g);
         return c;
     }
@@ -431,7 +456,7 @@ wpk_status wpk_conv2d_invalidate(wpk_plan plan) {
 }
 
 wpk_status wpk_family_describe(int32_t family, int32_t *counts, int32_t *values, const char **names) {
-    if (family < 0 || family > 2 || !counts || !values) return fail(WPK_ERR_INVALID_ARGUMENT, "bad argument");
+    if (family < 0 || family > 3 || !counts || !values) return fail(WPK_ERR_INVALID_ARGUMENT, "bad argument");
     const Space &sp = family_space(family);
     for (int g = 0; g < WPK_NUM_GENES; ++g) {
         counts[g] = (int)sp.dom[g].size();

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "dwconv.h"
+#include "gemm32.h"
 #include "simt_conv.cuh"
 #include "umma_conv.h"
 #include "wpk_internal.h"
@@ -381,6 +382,13 @@ static WsLayout ws_layout(Plan &p, const Config &cfg, bool host_staging) {
         }
     } else if (cfg.family == WPK_FAMILY_DW) {
         L.w_off = off; L.w_bytes = al256((size_t)d.c * d.r * d.s * e); off += L.w_bytes;
+    } else if (cfg.family == WPK_FAMILY_GEMM32) {
+        const int cp = (d.c + 3) / 4 * 4;   // channels padded to whole 16-byte vectors
+        if (d.layout == WPK_NCHW || cp != d.c) {
+            L.x_off = off; L.x_bytes = al256((size_t)d.n * d.h * d.w * cp * e); off += L.x_bytes;
+            L.w_off = off; L.w_bytes = al256((size_t)d.k * d.r * d.s * cp * e); off += L.w_bytes;
+        }
+        if (cfg.genes[4] > 1) { L.p_off = off; L.p_bytes = al256((size_t)cfg.genes[4] * d.M() * d.k * 4); off += L.p_bytes; }
     }
     if (host_staging) {
         L.hx_off = off; L.hx_bytes = al256((size_t)d.n * d.c * d.h * d.w * e); off += L.hx_bytes;
@@ -460,6 +468,40 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
         }
         a.epilogue = d.epilogue;
         int rc = dw_launch(a, d.dtype, cfg.genes[0], cfg.genes[1], cfg.genes[2], sm, stream, &err);
+        if (rc < 0) { set_error(err); return -1; }
+        return launches + rc;
+    }
+    if (cfg.family == WPK_FAMILY_GEMM32) {
+        // NHWC activations and KRSC weights as given; NCHW inputs, or C not a multiple of 4, are
+        // re-laid first as NHWC / KRSC with C zero-padded to whole 16-byte vectors (weights once)
+        const void *xk = x, *wk = w;
+        const int cp = (d.c + 3) / 4 * 4;
+        if (d.layout == WPK_NCHW || cp != d.c) {
+            launch_aux(d.layout == WPK_NCHW ? 0 : 1, x, ws + L.x_off, d, cp, sm, st);
+            ++launches;
+            xk = ws + L.x_off;
+            if (p.packed_for != w || p.packed_cfg_family != WPK_FAMILY_GEMM32) {
+                launch_aux(2, w, ws + L.w_off, d, cp, sm, st);
+                ++launches;
+                p.packed_for = w;
+                p.packed_cfg_family = WPK_FAMILY_GEMM32;
+            }
+            wk = ws + L.w_off;
+        }
+        Gemm32Args a{};
+        a.x = (const float *)xk; a.w = (const float *)wk; a.b = (const float *)b; a.y = (float *)y;
+        a.z = (const float *)z;
+        a.M = d.M(); a.PQ = d.p * d.q; a.Q = d.q; a.K = d.k; a.C = cp; a.H = d.h; a.W = d.w; a.R = d.r; a.S = d.s;
+        a.sh = d.sh; a.sw = d.sw; a.ph = d.ph; a.pw = d.pw; a.dh = d.dh; a.dw = d.dw;
+        if (d.layout == WPK_NCHW) {
+            a.ys_n = (long long)d.k * d.p * d.q; a.ys_k = (long long)d.p * d.q; a.ys_p = d.q; a.ys_q = 1;
+        } else {
+            a.ys_n = (long long)d.p * d.q * d.k; a.ys_k = 1; a.ys_p = (long long)d.q * d.k; a.ys_q = d.k;
+        }
+        a.epilogue = d.epilogue;
+        const int *gn = cfg.genes;
+        int rc = gemm32_launch(a, gn[0], gn[1], gn[2], gn[3], gn[4],
+                               gn[4] > 1 ? reinterpret_cast<float *>(ws + L.p_off) : nullptr, sm, stream, &err);
         if (rc < 0) { set_error(err); return -1; }
         return launches + rc;
     }

@@ -87,7 +87,7 @@ def test_output_dims_and_default_plan(oracle_lib, layer):
         if layer.groups > 1:
             assert fam.value == L.FAMILIES["dw"]
         elif dtype == "f32":
-            assert fam.value == L.FAMILIES["simt"]
+            assert fam.value == L.FAMILIES["gemm32"]
         else:
             assert fam.value == L.FAMILIES["umma"]
         assert lib.wpk_conv2d_config_valid(h, fam, genes) == 1
@@ -109,8 +109,13 @@ def test_set_config_validation():
     # f32 cannot use the tensor-core family
     umma = (ctypes.c_int32 * 7)(64, 4, 1, 0, 0, 2, 128)
     assert lib.wpk_conv2d_set_config(h, 1, umma) == L.ERR_INVALID_CONFIG
+    g32 = (ctypes.c_int32 * 7)(128, 64, 16, 4, 2, 0, 0)
+    assert lib.wpk_conv2d_set_config(h, 3, g32) == L.OK
+    g32_bad = (ctypes.c_int32 * 7)(128, 64, 16, 2, 1, 0, 0)   # THREAD_TILE 2 not in {4, 8}
+    assert lib.wpk_conv2d_set_config(h, 3, g32_bad) == L.ERR_INVALID_CONFIG
     lib.wpk_conv2d_destroy(h)
     st, h = _plan(shp, "bf16")
+    assert lib.wpk_conv2d_set_config(h, 3, g32) == L.ERR_INVALID_CONFIG   # GEMM32 is f32-only
     too_deep = (ctypes.c_int32 * 7)(256, 8, 1, 0, 0, 2, 128)   # 8 x 48 KB stages > 227 KB
     assert lib.wpk_conv2d_set_config(h, 1, too_deep) == L.ERR_INVALID_CONFIG
     assert lib.wpk_conv2d_set_config(h, 1, umma) == L.OK
@@ -122,6 +127,8 @@ def test_family_describe_matches_paper_genes():
     assert names == ["T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"]
     names, doms = L.family_describe("umma")
     assert names[0] == "BLOCK_N" and 128 in doms[0]
+    names, doms = L.family_describe("gemm32")
+    assert names[:5] == ["BLOCK_M", "BLOCK_N", "BLOCK_K", "THREAD_TILE", "SPLIT_K"] and doms[3] == [4, 8]
 
 
 def test_options_defaults():

@@ -170,6 +170,42 @@ def test_simt_every_tile_template():
 
 
 @pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+def test_gemm32_every_template(layout):
+    """Exact-fp32 implicit GEMM (WPK_FAMILY_GEMM32): every (BLOCK_M, BLOCK_N, BLOCK_K, THREAD_TILE)
+    instantiation with and without split-K, vector (C % 4 == 0) and scalar operand loads, ragged M/K/R*S*C tails, all
+    epilogues: bit-exact in integer mode, within 1e-5 max-rel in uniform mode."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import to_layout, from_layout
+    layers = [ConvLayer("g3", 2, 20, 13, 11, 72, 3, 3, 1, 1), ConvLayer("g3s2", 1, 7, 17, 15, 130, 3, 3, 2, 1),
+              ConvLayer("g1", 3, 36, 9, 7, 40, 1, 1, 1, 0), ConvLayer("gdil", 1, 12, 14, 16, 24, 3, 5, 1, 2, 2)]
+    for li, L in enumerate(layers):
+        epi = ["none", "bias", "bias_relu", "bias_relu"][li]
+        plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, layout=layout, epilogue=epi,
+                          dtype="f32")
+        assert plan.config[0] == 3
+        ran = 0
+        for mode in ("int", "uniform"):
+            x, w, b = workloads.generate(L, "f32", mode, seed=60 + li)
+            ref = oracle.conv2d(x, w, b if epi != "none" else None, stride=L.stride, pad=L.pad, dil=L.dil,
+                                relu=(epi == "bias_relu"))
+            xl, wl = to_layout(x, w, layout)
+            xl, wl, bc = xl.cuda(), wl.cuda(), (b.cuda() if epi != "none" else None)
+            for bm, bn, bk, tt, sk in itertools.product([64, 128], [64, 128], [8, 16], [4, 8], [1, 2, 8]):
+                if not plan.config_valid(3, [bm, bn, bk, tt, sk, 0, 0]):
+                    assert sk == 8, (L.name, bm, bn, bk, tt, sk)   # only an empty split is invalid
+                    continue
+                ran += 1
+                plan.set_config(3, [bm, bn, bk, tt, sk, 0, 0])
+                y = from_layout(plan.run(xl, wl, bc).cpu(), layout)
+                torch.cuda.synchronize()
+                if mode == "int":
+                    assert_bit_exact(y, ref)
+                else:
+                    assert rel_error("f32", y, ref) <= TOL["f32"], (L.name, bm, bn, bk, tt)
+        assert ran >= 2 * 32, L.name
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
 def test_depthwise(dtype, layout):
     for L in [ConvLayer("dw", 2, 96, 15, 15, 96, 3, 3, 2, 1, 1, 96), ConvLayer("dw1", 1, 32, 12, 12, 32, 3, 3, 1, 1, 1, 32)]:
@@ -324,6 +360,8 @@ def test_residual_epilogue(dtype, layout):
         zl = z.permute(0, 2, 3, 1).contiguous() if layout == "nhwc" else z.contiguous()
         xl, wl, bc, zc = xl.cuda(), wl.cuda(), b.cuda(), zl.cuda()
         configs = [plan.config]
+        if dtype == "f32" and L.groups == 1:   # the paper's SIMT template as well as the GEMM32 default
+            configs += [(0, [16, 4, 4, 1, 1, 1, 1]), (0, [8, 8, 4, 2, 1, 2, 4])]
         if plan.config[0] == 1:
             configs += [(1, [128, 4, 1, 0, 0, 2, 128]), (1, [64, 3, 1, 1, 0, 4, 256]), (1, [256, 3, 1, 2, 0, 1, 256])]
             assert not plan.config_valid(1, [128, 4, 2, 0, 0, 2, 128])   # residual plans: SPLIT_K = 1 only
@@ -404,7 +442,7 @@ def test_random_shapes_random_configs(case):
     xl, wl = to_layout(x, w, layout)
     xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
     fam = plan.config[0]
-    names, doms = L.family_describe(["simt", "umma", "dw"][fam])
+    names, doms = L.family_describe(["simt", "umma", "dw", "gemm32"][fam])
     configs = [plan.config]
     tries = 0
     while len(configs) < 4 and tries < 400:

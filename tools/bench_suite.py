@@ -29,6 +29,7 @@ NETS = {
     "resnet18_n1": (lambda: workloads.resnet18(1), "bf16", "ga"),
     "table1_n1": (lambda: workloads.table1(1), "bf16", "rl"),
     "resnet50_tf32": (lambda: workloads.resnet50(32), "tf32", "ga"),
+    "resnet50_f32_n8": (lambda: workloads.resnet50(8), "f32", "ga"),   # exact-fp32 CUDA-core path
 }
 
 
@@ -56,7 +57,9 @@ def run_net(name, budget):
         fl = 2 * L.n * L.k * plan.p * plan.q * (L.c // L.groups) * L.r * L.s
         e = xd.element_size()
         by = e * (xd.numel() + wd.numel() + bd.numel() + yd.numel())
-        peak_tf = PEAKS["bf16_tflops"] * (0.5 if dtype == "tf32" else 1.0)
+        # f32 runs on the CUDA cores: 148 SMs x 128 FP32 lanes x 2 flop/FMA x max SM clock (74.4 TF/s)
+        peak_tf = (148 * 128 * 2 * PEAKS["sm_max_mhz"] / 1e6 if dtype == "f32"
+                   else PEAKS["bf16_tflops"] * (0.5 if dtype == "tf32" else 1.0))
         rows.append({"layer": L.name, "count": L.count, "n": L.n, "dtype": dtype, "family": res.family,
                      "config": res.genes, "wpk_us": sel.own_us, "cudnn_us": sel.cudnn_us,
                      "cudnn_variant": sel.cudnn_variant, "speedup_vs_cudnn": sel.cudnn_us / sel.own_us,
@@ -72,7 +75,7 @@ def run_net(name, budget):
             "sum_wpk_us": sum(r["wpk_us"] * r["count"] for r in rows),
             "sum_cudnn_us": sum(r["cudnn_us"] * r["count"] for r in rows),
             "sum_selector_us": sum(min(r["wpk_us"], r["cudnn_us"]) * r["count"] for r in rows),
-            "peak_source": "MEASURED_PEAKS.json (tf32 = half the bf16 figure)"}
+            "peak_source": "MEASURED_PEAKS.json (tf32 = half the bf16 figure; f32 = FP32 FMA peak at sm_max_mhz)"}
 
 
 def main():
@@ -87,7 +90,7 @@ def main():
         for r in res:
             f.write(f"\n### {r['net']} ({r['dtype']}, {r['search']}-tuned, budget {r['budget']}/layer; "
                     f"tuning {r['tuning_seconds_1gpu']:.1f} s on 1 GPU)\n\n")
-            f.write("| layer | x | GFLOP | MB | wpk us | cuDNN us | speedup | TF/s | % tensor peak | GB/s | % HBM | config |\n")
+            f.write("| layer | x | GFLOP | MB | wpk us | cuDNN us | speedup | TF/s | % peak (f32: FMA) | GB/s | % HBM | config |\n")
             f.write("|---|---|---|---|---|---|---|---|---|---|---|---|\n")
             for L in r["layers"]:
                 f.write(f"| {L['layer']} | {L['count']} | {L['gflop']:.3f} | {L['mbytes']:.2f} | {L['wpk_us']:.1f} | "
