@@ -738,6 +738,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             const bool isA = (warp != 2);
             const int half = (warp == 3) ? 1 : 0;
             if (isA) asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (dbg && isA && half == 0) dbg[7] = ptx::globaltimer();   // previous grid complete
             uint32_t stage = 0, phase = 0;
             const uint32_t a_rows = (kPair ? 128u : (uint32_t)a.bm) >> (a.a_split ? 1 : 0);   // rows per A load
             const uint32_t tx = isA ? a_rows * 128u : b_bytes;
@@ -1035,6 +1036,14 @@ static cudaError_t launch_variant(cudaLaunchConfig_t &lc, const CUtensorMap &tmA
         cudaError_t e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return e;
+        // one shared-memory carveout for every variant and config: consecutive convs whose dynamic
+        // smem differs would otherwise get different L1/smem splits, and an SM can only switch
+        // carveout once drained -- no overlap of one conv's tail with the next conv's CTAs
+        if (!getenv("WPK_NO_CARVEOUT")) {
+            e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared);
+            if (e != cudaSuccess) return e;
+        }
         attr_done = true;
     }
     return cudaLaunchKernelEx(&lc, umma_conv_kernel<DT, AK, EK>, tmA, tmB, tmY, tmP, a);

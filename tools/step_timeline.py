@@ -46,13 +46,17 @@ for u in units:
     t = u[6].view(148, 64).cpu().numpy().astype(np.float64)
     t = t[t[:, 0] > 0]
     rows.append((u[0], t[:, 0].min(), np.median(t[:, 1]), t[:, 2][t[:, 2] > 0].min() if (t[:, 2] > 0).any() else 0,
-                 t[:, 6].max(), len(t)))
+                 t[:, 6].max(), len(t), t[:, 7][t[:, 7] > 0].min() if (t[:, 7] > 0).any() else 0))
 t0 = rows[0][1]
-print(f"{'conv':10s} {'start':>8s} {'setup':>8s} {'1stfull':>8s} {'end':>8s} {'dur':>7s} {'gap':>7s} CTAs  (us from step start)")
+print(f"{'conv':10s} {'start':>8s} {'setup':>8s} {'1stfull':>8s} {'end':>8s} {'dur':>7s} {'gap':>7s} CTAs "
+      f"{'wait':>7s} {'load':>7s}  (us from step start; wait = previous end -> first griddepcontrol.wait return, "
+      f"load = that -> first full stage)")
 prev_end = None
-for (nm, s0, su, ff, e, n) in rows:
+for (nm, s0, su, ff, e, n, wr) in rows:
     gap = (s0 - prev_end) / 1e3 if prev_end is not None else 0.0
+    wt = (wr - prev_end) / 1e3 if (prev_end is not None and wr > 0) else float("nan")
+    ld = (ff - wr) / 1e3 if (wr > 0 and ff > 0) else float("nan")
     print(f"{nm:10s} {(s0 - t0) / 1e3:8.2f} {(su - t0) / 1e3:8.2f} {(ff - t0) / 1e3:8.2f} {(e - t0) / 1e3:8.2f} "
-          f"{(e - s0) / 1e3:7.2f} {gap:7.2f} {n}")
+          f"{(e - s0) / 1e3:7.2f} {gap:7.2f} {n} {wt:7.2f} {ld:7.2f}")
     prev_end = e
 print(f"step span {(rows[-1][4] - t0) / 1e3:.1f} us")
