@@ -20,8 +20,14 @@
 
 namespace wpk {
 
+// 8x8 thread tiles: at most 128 registers per thread (512 / threads CTAs per SM), except the
+// 64-thread BLOCK_K 16 tile, whose 4 staged A vectors per thread would then spill
+constexpr int gemm32_min_blocks(int bm, int bn, int bk, int tt) {
+    return tt != 8 ? 1 : ((bm / tt) * (bn / tt) == 64 && bk == 16) ? 4 : 512 / ((bm / tt) * (bn / tt));
+}
+
 template <int BM, int BN, int BK, int TT>
-__global__ void __launch_bounds__((BM / TT) * (BN / TT), TT == 8 ? 2 : 1)
+__global__ void __launch_bounds__((BM / TT) * (BN / TT), gemm32_min_blocks(BM, BN, BK, TT))
     gemm32_conv_kernel(const Gemm32Args a) {
     constexpr int TX = BN / TT, TY = BM / TT, NT = TX * TY;
     constexpr int A4 = BM * BK / 4, B4 = BN * BK / 4;                 // float4 slots per tile
@@ -143,23 +149,29 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT), TT == 8 ? 2 : 1)
     for (int t = 0; t < nk; ++t) {
         const int buf = t & 1;
         if (t + 1 < nk) { load_a(kbase + (t + 1) * BK); load_b(kbase + (t + 1) * BK); }
-#pragma unroll
-        for (int kk = 0; kk < BK; ++kk) {
-            float av[TT], bv[TT];
+        // operand fragments double-buffered in registers: row kk+1 is read from shared memory
+        // while row kk's outer product issues (hides the LDS latency at low occupancy)
+        float av[2][TT], bv[2][TT];
+        auto frag = [&](int f, int kk) {
 #pragma unroll
             for (int i = 0; i < TT; i += 4) {
                 const float4 t4 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * TT + i]);
-                av[i] = t4.x; av[i + 1] = t4.y; av[i + 2] = t4.z; av[i + 3] = t4.w;
+                av[f][i] = t4.x; av[f][i + 1] = t4.y; av[f][i + 2] = t4.z; av[f][i + 3] = t4.w;
             }
 #pragma unroll
             for (int j = 0; j < TT; j += 4) {
                 const float4 t4 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][tx * TT + j]);
-                bv[j] = t4.x; bv[j + 1] = t4.y; bv[j + 2] = t4.z; bv[j + 3] = t4.w;
+                bv[f][j] = t4.x; bv[f][j + 1] = t4.y; bv[f][j + 2] = t4.z; bv[f][j + 3] = t4.w;
             }
+        };
+        frag(0, 0);
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            if (kk + 1 < BK) frag((kk + 1) & 1, kk + 1);
 #pragma unroll
             for (int i = 0; i < TT; ++i)
 #pragma unroll
-                for (int j = 0; j < TT; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+                for (int j = 0; j < TT; ++j) acc[i][j] = fmaf(av[kk & 1][i], bv[kk & 1][j], acc[i][j]);
         }
         if (t + 1 < nk) {
             store(buf ^ 1);
