@@ -331,6 +331,27 @@ def test_resnet50_n32_bench_configs_sampled(layer):
             assert err <= TOL["bf16"], err
 
 
+_TUNED_F32 = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r1e_suite_f32.json")
+
+
+@pytest.mark.parametrize("layer", workloads.resnet50(8), ids=lambda l: l.name)
+def test_resnet50_n8_f32_tuned_configs_sampled(layer):
+    """Exact fp32 at full size in the GA-tuned GEMM32 configs of profiles/r1e_suite_f32.json (split-K
+    up to 8): sampled outputs bit-exact in integer mode, within fp32 max-rel 1e-5 in uniform mode."""
+    import json
+    r = {row["layer"]: row for row in json.load(open(_TUNED_F32))[0]["layers"]}[layer.name]
+    for mode in ("int", "uniform"):
+        x, w, b = workloads.generate(layer, "f32", mode, seed=workloads.config_seed(2, 3))
+        y, plan = run_product(layer, "f32", "nhwc", x, w, b, config=(r["family"], r["config"]))
+        pts = workloads.random_points(layer, plan.p, plan.q, 2048, seed=3).numpy()
+        ref = oracle.conv2d_points(x, w, b, pts, stride=layer.stride, pad=layer.pad, nthreads=8)
+        got = y[pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]].double().numpy()
+        if mode == "int":
+            assert np.array_equal(got, ref)
+        else:
+            assert np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30) <= TOL["f32"]
+
+
 def _residual_case(L, dtype, layout, seed):
     """x, w, b and a residual z (NCHW, y's shape) in exact-integer mode, plus the oracle output."""
     x, w, b = workloads.generate(L, dtype, "int", seed=seed)
