@@ -52,7 +52,7 @@ typedef enum {
     WPK_OK = 0,
     WPK_ERR_INVALID_ARGUMENT = 1, /* NULL / misaligned pointer, bad enum, bad option value     */
     WPK_ERR_SHAPE = 2,            /* any dim < 1, P or Q < 1, C % g != 0, K % g != 0            */
-    WPK_ERR_UNSUPPORTED = 3,      /* groups not in {1, C==K}; device not sm_100                 */
+    WPK_ERR_UNSUPPORTED = 3,      /* device not sm_100                                          */
     WPK_ERR_INVALID_CONFIG = 4,   /* genes outside the family's space or violating a constraint */
     WPK_ERR_EXHAUSTED = 5,        /* no valid config could be sampled / every candidate failed  */
     WPK_ERR_CUDA = 6,             /* CUDA runtime/driver error (message in wpk_last_error)      */
@@ -72,7 +72,9 @@ typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 
 /* Kernel families ("schedule templates"). Each has 7 genes (PAPER.md:65 chromosome
  * s = {c_0..c_6}); their meaning per family is listed by wpk_family_describe().
  *   WPK_FAMILY_SIMT : direct conv on CUDA cores, genes = the paper's
- *                     (T_x, T_y, T_z, Tile_x, Tile_y, Tile_z, Tile_rz), T_x*T_y*T_z<=1024
+ *                     (T_x, T_y, T_z, Tile_x, Tile_y, Tile_z, Tile_rz), T_x*T_y*T_z<=1024;
+ *                     every shape, dtype and layout, and the only family for general groups
+ *                     (1 < groups, not depthwise)
  *   WPK_FAMILY_UMMA : tcgen05 implicit GEMM, genes = (BLOCK_N, STAGES, SPLIT_K, MODE,
  *                     A_MODE, ACC_STAGES, BLOCK_M); MODE bit 0 = raster order, bit 1 = CTA pair
  *                     (cta_group::2, 256-row tiles across two SMs, BLOCK_M must be 256); A_MODE 0 = TMA im2col producer (plain TMA

@@ -53,8 +53,6 @@ static wpk_status to_desc(const wpk_conv2d_shape *s, int dtype, ConvDesc *d) {
                             (double)s->n * s->k * d->p * d->q};
     for (double e : elems)
         if (e > 4.0e9) return fail(WPK_ERR_UNSUPPORTED, "tensor larger than 2^32 elements");
-    if (s->groups != 1 && !(s->groups == s->c && s->groups == s->k))
-        return fail(WPK_ERR_UNSUPPORTED, "groups must be 1 or C == K (depthwise) in v1");
     return WPK_OK;
 }
 

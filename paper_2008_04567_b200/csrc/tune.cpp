@@ -62,7 +62,7 @@ void log_line(TuneCtx &t, const std::string &s) {
 // ---------------------------------------------------------------------------------------------------
 struct GpuBench {
     cudaStream_t st = nullptr;
-    void *x = nullptr, *w = nullptr, *b = nullptr, *y = nullptr, *ws = nullptr, *flush = nullptr;
+    void *x = nullptr, *w = nullptr, *b = nullptr, *y = nullptr, *z = nullptr, *ws = nullptr, *flush = nullptr;
     unsigned long long *stamps = nullptr;   // [2 * reps] device timestamps
     size_t ws_bytes = 0, flush_bytes = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -81,6 +81,10 @@ struct GpuBench {
         fill_random_device(x, xb / e, d.dtype, 1, st);
         fill_random_device(w, wb / e, d.dtype, 2, st);
         fill_random_device(b, d.k, d.dtype, 3, st);
+        if (d.epilogue == WPK_EPI_BIAS_ADD_RELU) {   // a residual plan reads z of y's shape
+            if (cudaMalloc(&z, yb)) return fail_("cudaMalloc of the residual buffer");
+            fill_random_device(z, yb / e, d.dtype, 4, st);
+        }
         flush_bytes = (size_t)2 * device_l2_bytes(p.device);
         if (cudaMalloc(&flush, flush_bytes + 256)) return fail_("cudaMalloc of the L2 flush buffer");
         cudaMemsetAsync(flush, 1, flush_bytes + 256, st);
@@ -96,7 +100,7 @@ struct GpuBench {
         return false;
     }
     ~GpuBench() {
-        for (void *ptr : {x, w, b, y, ws, flush, (void *)stamps})
+        for (void *ptr : {x, w, b, y, z, ws, flush, (void *)stamps})
             if (ptr) cudaFree(ptr);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
@@ -124,7 +128,7 @@ struct GpuBench {
         }
         p.packed_for = nullptr;
         for (int i = 0; i < warmup; ++i)
-            if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes) < 0) return INFINITY;
+            if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes, z) < 0) return INFINITY;
         if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
         // Each rep is bracketed by two 1-thread kernels that write %globaltimer (256-ns steps; CUDA
         // events on this part advance in ~2-us steps, too coarse for 5-30 us layers). The constant
@@ -134,7 +138,7 @@ struct GpuBench {
         for (int i = 0; i < reps; ++i) {
             if (l2flush) l2_flush_device(flush, flush_bytes, (char *)flush + flush_bytes, st);
             timestamp_device(stamps + 2 * i, st);
-            if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes) < 0) return INFINITY;
+            if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes, z) < 0) return INFINITY;
             timestamp_device(stamps + 2 * i + 1, st);
             if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
         }

@@ -46,7 +46,7 @@ def _plan(shape, dtype="bf16"):
 @pytest.mark.parametrize("kw,status", [
     (dict(n=0), L.ERR_SHAPE), (dict(c=0), L.ERR_SHAPE), (dict(stride=0), L.ERR_SHAPE),
     (dict(h=1, pad=0), L.ERR_SHAPE),                                  # 3x3 on 1x1 -> empty output
-    (dict(groups=2, c=3), L.ERR_SHAPE), (dict(groups=2, c=4, k=6), L.ERR_UNSUPPORTED),
+    (dict(groups=2, c=3), L.ERR_SHAPE), (dict(groups=2, c=4, k=7), L.ERR_SHAPE),
     (dict(pad=-1), L.ERR_SHAPE),
 ])
 def test_shape_validation(kw, status):
@@ -56,6 +56,24 @@ def test_shape_validation(kw, status):
     st, h = _plan(shp)
     assert st == status, L.last_error()
     assert L.last_error()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "tf32", "bf16", "f16"])
+def test_general_groups_plan_simt(dtype):
+    """General grouped conv (1 < groups < C, NEXT-4): planned on the SIMT family (the only one whose
+    kernel indexes groups); config validation keeps the other families out."""
+    lib = L.load()
+    shp = L.make_shape(2, 32, 9, 9, 48, 3, 3, 1, 1, groups=8, layout="nhwc")
+    st, h = _plan(shp, dtype)
+    assert st == L.OK, L.last_error()
+    fam, genes = ctypes.c_int32(), (ctypes.c_int32 * 7)()
+    L.check(lib.wpk_conv2d_get_config(h, ctypes.byref(fam), genes))
+    assert fam.value == L.FAMILIES["simt"]
+    umma = (ctypes.c_int32 * 7)(64, 4, 1, 0, 0, 2, 128)
+    g32 = (ctypes.c_int32 * 7)(64, 64, 8, 4, 1, 0, 0)
+    assert lib.wpk_conv2d_config_valid(h, L.FAMILIES["umma"], umma) == 0
+    assert lib.wpk_conv2d_config_valid(h, L.FAMILIES["gemm32"], g32) == 0
+    lib.wpk_conv2d_destroy(h)
 
 
 def test_bad_struct_size_and_null():

@@ -206,6 +206,36 @@ def test_gemm32_every_template(layout):
 
 
 @pytest.mark.parametrize("layout", ["nchw", "nhwc"])
+@pytest.mark.parametrize("dtype", ["f32", "tf32", "bf16", "f16"])
+def test_general_groups(dtype, layout):
+    """Grouped conv with 1 < groups (ResNeXt-style C/g = 4, g = 2, channel multiplier 2), default
+    (SIMT) config and two other tile templates: bit-exact in integer mode, within tolerance in
+    uniform mode."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import to_layout, from_layout
+    layers = [ConvLayer("g32x4", 2, 128, 9, 11, 128, 3, 3, 1, 1, 1, 32), ConvLayer("g2s2", 1, 24, 13, 12, 40, 3, 3, 2, 1, 1, 2),
+              ConvLayer("gmult", 2, 16, 8, 8, 32, 3, 3, 1, 1, 1, 16)]
+    for L in layers:
+        plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups, layout=layout, dtype=dtype)
+        assert plan.config[0] == 0, L.name
+        tiles = [None, [8, 8, 4, 2, 1, 2, 1], [32, 2, 2, 1, 2, 1, 1]]
+        for mode in ("int", "uniform"):
+            x, w, b = workloads.generate(L, dtype, mode, seed=71)
+            ref = oracle.conv2d(x, w, b, stride=L.stride, pad=L.pad, dil=L.dil, groups=L.groups)
+            xl, wl = to_layout(x, w, layout)
+            xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
+            for genes in tiles:
+                if genes is not None:
+                    plan.set_config(0, genes)
+                y = from_layout(plan.run(xl, wl, bc).cpu(), layout)
+                torch.cuda.synchronize()
+                if mode == "int":
+                    assert_bit_exact(y, ref)
+                else:
+                    assert rel_error(dtype, y, ref) <= TOL[dtype], (L.name, genes)
+
+
+@pytest.mark.parametrize("layout", ["nchw", "nhwc"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])
 def test_depthwise(dtype, layout):
     for L in [ConvLayer("dw", 2, 96, 15, 15, 96, 3, 3, 2, 1, 1, 96), ConvLayer("dw1", 1, 32, 12, 12, 32, 3, 3, 1, 1, 1, 32)]:
@@ -398,6 +428,23 @@ def test_residual_epilogue(dtype, layout):
         assert ran >= 1, L.name
         with pytest.raises(Exception):   # a residual plan refuses the plain run entry point
             plan.run(xl, wl, bc)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_residual_plan_tunes(dtype):
+    """A residual-epilogue plan can be tuned (the tuner supplies a z buffer to every candidate) and
+    its chosen config is bit-exact."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    L = ConvLayer("rt", 2, 64, 14, 14, 128, 1, 1, 1, 0)
+    x, w, b, z, ref = _residual_case(L, dtype, "nhwc", seed=43)
+    plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", epilogue="bias_add_relu",
+                      dtype=dtype)
+    res = plan.tune("ga", 12, seed=1)
+    assert res.measured >= 1 and res.best_us < float("inf")
+    xl, wl = x.permute(0, 2, 3, 1).contiguous().cuda(), w.permute(0, 2, 3, 1).contiguous().cuda()
+    y = plan.run(xl, wl, b.cuda(), z=z.permute(0, 2, 3, 1).contiguous().cuda())
+    torch.cuda.synchronize()
+    assert_bit_exact(y.cpu().permute(0, 3, 1, 2).contiguous(), ref)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f16"])

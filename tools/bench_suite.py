@@ -30,6 +30,8 @@ NETS = {
     "table1_n1": (lambda: workloads.table1(1), "bf16", "rl"),
     "resnet50_tf32": (lambda: workloads.resnet50(32), "tf32", "ga"),
     "resnet50_f32_n8": (lambda: workloads.resnet50(8), "f32", "ga"),   # exact-fp32 CUDA-core path
+    "resnext50_grouped_bf16_n8": (lambda: workloads.resnext50_grouped(8), "bf16", "ga"),   # general groups (SIMT)
+    "resnext50_grouped_f32_n8": (lambda: workloads.resnext50_grouped(8), "f32", "ga"),
 }
 
 

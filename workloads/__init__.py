@@ -109,6 +109,23 @@ def resnet18(n: int = 1) -> list[ConvLayer]:
     return out
 
 
+def resnext50_grouped(n: int = 8) -> list[ConvLayer]:
+    """The grouped 3x3 convs of ResNeXt-50 32x4d (groups 32, 4..32 channels per group; stride 2 on
+    the first block of stages 3-5) -- the general-groups workload of SURVEY.md 8(f) NEXT-4."""
+    L = ConvLayer
+    rows = [
+        # name,      C,   H, stride, count
+        ("s2.g",    128, 56, 1, 3),
+        ("s3b0.g",  256, 56, 2, 1),
+        ("s3.g",    256, 28, 1, 3),
+        ("s4b0.g",  512, 28, 2, 1),
+        ("s4.g",    512, 14, 1, 5),
+        ("s5b0.g", 1024, 14, 2, 1),
+        ("s5.g",   1024,  7, 1, 2),
+    ]
+    return [L(nm, n, c, h, h, c, 3, 3, st, 1, 1, 32, cnt) for (nm, c, h, st, cnt) in rows]
+
+
 def vgg16(n: int = 64) -> list[ConvLayer]:
     rows = [("conv1_1", 3, 224, 64, 1), ("conv1_2", 64, 224, 64, 1),
             ("conv2_1", 64, 112, 128, 1), ("conv2_2", 128, 112, 128, 1),
