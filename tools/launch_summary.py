@@ -1,7 +1,7 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 --csv) of one bench step into profiles/ncu_summary.json: per-kernel launches, time, share of the step,
 DRAM bytes; plus the conv kernel's DRAM bytes per step / per launch (the bench's roofline 'traffic').
-usage: python tools/launch_summary.py launches.csv out.json"""
+usage: python tools/launch_summary.py launches.csv out.json [steps]"""
 import csv, json, sys
 from collections import defaultdict
 
@@ -26,10 +26,13 @@ for e in k.values():
     e["share"] = e["time_us"] / tot
 u = k.get("umma_conv_kernel", {"launches": 0, "dram_read_MB": 0, "dram_write_MB": 0})
 umma_bytes = (u["dram_read_MB"] + u["dram_write_MB"]) * 1e6
+# the list may cover several steps (tools/profile_step.py STEPS=n): 53 conv launches per step
+steps = int(sys.argv[3]) if len(sys.argv) > 3 else max(1, round(u["launches"] / 53))
 out = {"source": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none, "
-                 "one bench step (tools/profile_step.py with the bench's tuned configs); serialised, cold-cache "
+                 f"{steps} bench step(s) (tools/profile_step.py with the bench's tuned configs); serialised, cold-cache "
                  "launches: compare shares, not absolutes",
-       "kernels": dict(k), "umma_dram_bytes_per_step": umma_bytes,
+       "steps": steps,
+       "kernels": dict(k), "umma_dram_bytes_per_step": umma_bytes / steps,
        "umma_dram_bytes_per_launch": umma_bytes / max(1, u["launches"])}
 json.dump(out, open(sys.argv[2], "w"), indent=1)
 print(json.dumps(out, indent=1))
