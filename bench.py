@@ -48,26 +48,50 @@ def layer_bytes(L, p, q, elem):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML every 5 ms (the timed
+    region of a default run is tens of ms), else nvidia-smi every 100 ms."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index, self.rows, self._stop = index, [], threading.Event()
+        self.source = "nvidia-smi"
+        self.nv = self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.source = "nvml"
+        except Exception:
+            self.nv = None
         self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _sample_nvml(self):
+        nv, h = self.nv, self.h
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        return [str(sm), str(mx), "", *("Active" if r & b else "Not Active" for b in bits)]
 
     def _run(self):
         while not self._stop.is_set():
             try:
+                if self.nv is not None:
+                    self.rows.append(self._sample_nvml())
+                    self._stop.wait(0.005)
+                    continue
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
                 if out:
                     self.rows.append([v.strip() for v in out.split(",")])
             except Exception:
-                pass
+                self.nv = None   # fall back to nvidia-smi
             self._stop.wait(0.1)
 
     def __enter__(self):
@@ -83,11 +107,10 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
                           and "Not" not in r[3 + i]})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": self.source}
 
 
 def dist_env():
@@ -223,7 +246,7 @@ def graph_refine(args, layers, plans, units, records, stream, pg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="wpk", choices=["wpk", "reference"])
     ap.add_argument("--batch", type=int, default=32, help="images per GPU")
