@@ -73,15 +73,15 @@ typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 
  * s = {c_0..c_6}); their meaning per family is listed by wpk_family_describe().
  *   WPK_FAMILY_SIMT : direct conv on CUDA cores, genes = the paper's
  *                     (T_x, T_y, T_z, Tile_x, Tile_y, Tile_z, Tile_rz), T_x*T_y*T_z<=1024;
- *                     every shape, dtype and layout, and the only family for general groups
- *                     (1 < groups, not depthwise)
+ *                     every shape, dtype, layout and groups
  *   WPK_FAMILY_UMMA : tcgen05 implicit GEMM, genes = (BLOCK_N, STAGES, SPLIT_K, MODE,
  *                     A_MODE, ACC_STAGES, BLOCK_M); MODE bit 0 = raster order, bit 1 = CTA pair
  *                     (cta_group::2, 256-row tiles across two SMs, BLOCK_M must be 256); A_MODE 0 = TMA im2col producer (plain TMA
  *                     tiles for 1x1/s1/p0), 1 = explicit im2col matrix in the workspace,
  *                     2 = fused gather producer (im2col built in shared memory; small-C layers)
- *   WPK_FAMILY_DW   : depthwise (groups == C == K), genes = (VEC_C, PIX_PER_THREAD, THREADS,
- *                     -, -, -, -)
+ *   WPK_FAMILY_DW   : grouped conv on CUDA cores, groups > 1: depthwise (groups == C == K, vector
+ *                     over channels) or general groups (vector over VEC_C outputs of one group,
+ *                     VEC_C | K/groups), genes = (VEC_C, PIX_PER_THREAD, THREADS, -, -, -, -)
  *   WPK_FAMILY_GEMM32 : exact-fp32 implicit GEMM on CUDA cores (WPK_F32, groups == 1), genes =
  *                     (BLOCK_M, BLOCK_N, BLOCK_K, THREAD_TILE, SPLIT_K, -, -); the F32 default;
  *                     SPLIT_K > 1 sums per-split fp32 partials in split order (deterministic) */

@@ -101,7 +101,7 @@ bool family_applicable(const ConvDesc &d, int family, std::string *why) {
     auto no = [&](const char *m) { if (why) *why = m; return false; };
     if (family == WPK_FAMILY_SIMT) return true;   // the SIMT kernel handles every valid shape, layout and dtype
     if (family == WPK_FAMILY_DW) {
-        if (!(d.g == d.c && d.g == d.k && d.g > 1)) return no("DW family needs groups == C == K");
+        if (d.g < 2) return no("DW family needs groups > 1 (depthwise or grouped)");
         return true;
     }
     if (family == WPK_FAMILY_GEMM32) {
@@ -277,16 +277,21 @@ bool config_valid(const ConvDesc &d, const Config &cfg, std::string *why) {
         if (gn[4] > 1 && (double)gn[4] * d.M() * d.k * 4 > 8.0e9) { if (why) *why = "split-K partials exceed 8 GB"; return false; }
         return true;
     }
-    // DW
+    // DW: depthwise (vector over channels = groups) or grouped (vector over a group's outputs)
     int vec = gn[0];
-    if (d.c % vec) { if (why) *why = "VEC_C must divide C"; return false; }
     if (d.elem() * vec > 16) { if (why) *why = "VEC_C*elem > 16 bytes"; return false; }
-    if (d.layout == WPK_NCHW && vec != 1) { if (why) *why = "NCHW depthwise needs VEC_C = 1"; return false; }
+    if (d.c == d.g && d.k == d.g) {
+        if (d.c % vec) { if (why) *why = "VEC_C must divide C"; return false; }
+        if (d.layout == WPK_NCHW && vec != 1) { if (why) *why = "NCHW depthwise needs VEC_C = 1"; return false; }
+    } else if ((d.k / d.g) % vec) {
+        if (why) *why = "grouped: VEC_C must divide K/groups";
+        return false;
+    }
     return true;
 }
 
 int default_family(const ConvDesc &d) {
-    if (d.g > 1 && d.g == d.c && d.g == d.k) return WPK_FAMILY_DW;
+    if (d.g > 1) return WPK_FAMILY_DW;   // depthwise and grouped kernels
     if (family_applicable(d, WPK_FAMILY_UMMA, nullptr)) return WPK_FAMILY_UMMA;
     if (family_applicable(d, WPK_FAMILY_GEMM32, nullptr)) return WPK_FAMILY_GEMM32;
     return WPK_FAMILY_SIMT;
@@ -301,14 +306,16 @@ Config default_config(const ConvDesc &d, int family) {
         return c;
     }
     if (family == WPK_FAMILY_GEMM32) {
-        // 128 x 128 CTA tiles of 8 x 8 outputs per thread; 64-wide for narrow layers
-        int g[7] = {64, 64, 16, 4, 1, 0, 0};   // the measured best on most ResNet-50 layers (profiles/r1e)
+        // 64 x 64 CTA tiles of 4 x 4 outputs per thread, 16-deep K steps, no split: the most common
+        // tuned choice on ResNet-50 (profiles/r1e_suite_f32.md)
+        int g[7] = {64, 64, 16, 4, 1, 0, 0};
         std::memcpy(c.genes, g, sizeof g);
         return c;
     }
     if (family == WPK_FAMILY_DW) {
-        int vec = (d.layout == WPK_NCHW) ? 1 : 16 / d.elem();
-        while (vec > 1 && d.c % vec) vec >>= 1;
+        const bool depthwise = d.c == d.g && d.k == d.g;
+        int vec = (depthwise && d.layout == WPK_NCHW) ? 1 : 16 / d.elem();
+        while (vec > 1 && (depthwise ? d.c : d.k / d.g) % vec) vec >>= 1;
         int g[7] = {vec, 1, 256, 1, 0, 0, 0};
         std::memcpy(c.genes, g, sizeof g);
         return c;

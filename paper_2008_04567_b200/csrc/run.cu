@@ -190,6 +190,22 @@ __global__ void fold_bn_kernel(const T *__restrict__ w, const T *__restrict__ b,
         }
     }
 }
+// Grouped weights KCRS (src_kcrs) or KRSC, [K][C/g][R][S] -> [R][S][C/g][K].
+template <typename T>
+__global__ void pack_grouped_kernel(const T *__restrict__ w, T *__restrict__ out, int K, int Cpg, int R, int S,
+                                    int src_kcrs) {
+    const long long total = (long long)K * Cpg * R * S;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(i % K);
+        long long t = i / K;
+        const int c = (int)(t % Cpg);
+        t /= Cpg;
+        const int s = (int)(t % S);
+        const int r = (int)(t / S);
+        out[i] = src_kcrs ? w[(((long long)k * Cpg + c) * R + r) * S + s] : w[(((long long)k * R + r) * S + s) * Cpg + c];
+    }
+}
 // Depthwise weights [C][R][S] (both layouts, C/g = 1) -> [R][S][C].
 template <typename T>
 __global__ void pack_rsc_kernel(const T *__restrict__ w, T *__restrict__ out, int C, int R, int S) {
@@ -244,6 +260,9 @@ static void launch_aux_t(int which, const void *src, void *dst, const ConvDesc &
     else if (which == 2)
         pack_krsc_kernel<T><<<grid_for((long long)d.k * d.r * d.s * cp, sm), 256, 0, st>>>(
             (const T *)src, (T *)dst, d.k, d.c, d.r, d.s, cp, d.layout == WPK_NCHW);
+    else if (which == 9)
+        pack_grouped_kernel<T><<<grid_for((long long)d.k * (d.c / d.g) * d.r * d.s, sm), 256, 0, st>>>(
+            (const T *)src, (T *)dst, d.k, d.c / d.g, d.r, d.s, d.layout == WPK_NCHW);
     else
         pack_rsc_kernel<T><<<grid_for((long long)d.c * d.r * d.s, sm), 256, 0, st>>>((const T *)src, (T *)dst, d.c,
                                                                                      d.r, d.s);
@@ -380,8 +399,8 @@ static WsLayout ws_layout(Plan &p, const Config &cfg, bool host_staging) {
             L.p_off = off; L.p_bytes = al256((size_t)g.splits * d.M() * d.k * 4); off += L.p_bytes;
             L.c_off = off; L.c_bytes = al256((size_t)g.m_tiles * g.n_tiles * (g.pair ? 2 : 1) * 4); off += L.c_bytes;
         }
-    } else if (cfg.family == WPK_FAMILY_DW) {
-        L.w_off = off; L.w_bytes = al256((size_t)d.c * d.r * d.s * e); off += L.w_bytes;
+    } else if (cfg.family == WPK_FAMILY_DW) {   // [R][S][C] or, grouped, [R][S][C/g][K]
+        L.w_off = off; L.w_bytes = al256((size_t)d.k * (d.c / d.g) * d.r * d.s * e); off += L.w_bytes;
     } else if (cfg.family == WPK_FAMILY_GEMM32) {
         const int cp = (d.c + 3) / 4 * 4;   // channels padded to whole 16-byte vectors
         if (d.layout == WPK_NCHW || cp != d.c) {
@@ -449,8 +468,9 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     }
     if (cfg.family == WPK_FAMILY_DW) {
         const void *wp = ws + L.w_off;
+        const bool depthwise = d.c == d.g && d.k == d.g;
         if (p.packed_for != w || p.packed_cfg_family != WPK_FAMILY_DW) {
-            launch_aux(3, w, ws + L.w_off, d, 0, sm, st);
+            launch_aux(depthwise ? 3 : 9, w, ws + L.w_off, d, 0, sm, st);
             ++launches;
             p.packed_for = w;
             p.packed_cfg_family = WPK_FAMILY_DW;
@@ -459,12 +479,13 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
         a.x = x; a.w = wp; a.b = b; a.y = y; a.z = z;
         a.N = d.n; a.C = d.c; a.H = d.h; a.W = d.w; a.R = d.r; a.S = d.s; a.P = d.p; a.Q = d.q;
         a.sh = d.sh; a.sw = d.sw; a.ph = d.ph; a.pw = d.pw; a.dh = d.dh; a.dw = d.dw;
+        a.K = d.k; a.Cpg = depthwise ? 0 : d.c / d.g; a.Kpg = d.k / d.g;
         if (d.layout == WPK_NCHW) {
             a.xs_n = (long long)d.c * d.h * d.w; a.xs_c = (long long)d.h * d.w; a.xs_h = d.w; a.xs_w = 1;
-            a.ys_n = (long long)d.c * d.p * d.q; a.ys_c = (long long)d.p * d.q; a.ys_p = d.q; a.ys_q = 1;
+            a.ys_n = (long long)d.k * d.p * d.q; a.ys_c = (long long)d.p * d.q; a.ys_p = d.q; a.ys_q = 1;
         } else {
             a.xs_n = (long long)d.h * d.w * d.c; a.xs_c = 1; a.xs_h = (long long)d.w * d.c; a.xs_w = d.c;
-            a.ys_n = (long long)d.p * d.q * d.c; a.ys_c = 1; a.ys_p = (long long)d.q * d.c; a.ys_q = d.c;
+            a.ys_n = (long long)d.p * d.q * d.k; a.ys_c = 1; a.ys_p = (long long)d.q * d.k; a.ys_q = d.k;
         }
         a.epilogue = d.epilogue;
         int rc = dw_launch(a, d.dtype, cfg.genes[0], cfg.genes[1], cfg.genes[2], sm, stream, &err);

@@ -59,16 +59,18 @@ def test_shape_validation(kw, status):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "tf32", "bf16", "f16"])
-def test_general_groups_plan_simt(dtype):
-    """General grouped conv (1 < groups < C, NEXT-4): planned on the SIMT family (the only one whose
-    kernel indexes groups); config validation keeps the other families out."""
+def test_general_groups_plan(dtype):
+    """General grouped conv (1 < groups < C, NEXT-4): planned on the grouped (DW) family, with the
+    output vector dividing K/groups; SIMT valid too; the GEMM families are kept out."""
     lib = L.load()
-    shp = L.make_shape(2, 32, 9, 9, 48, 3, 3, 1, 1, groups=8, layout="nhwc")
+    shp = L.make_shape(2, 32, 9, 9, 48, 3, 3, 1, 1, groups=8, layout="nhwc")   # C/g = 4, K/g = 6
     st, h = _plan(shp, dtype)
     assert st == L.OK, L.last_error()
     fam, genes = ctypes.c_int32(), (ctypes.c_int32 * 7)()
     L.check(lib.wpk_conv2d_get_config(h, ctypes.byref(fam), genes))
-    assert fam.value == L.FAMILIES["simt"]
+    assert fam.value == L.FAMILIES["dw"] and 6 % genes[0] == 0
+    assert lib.wpk_conv2d_config_valid(h, L.FAMILIES["dw"], (ctypes.c_int32 * 7)(4, 1, 256, 1, 0, 0, 0)) == 0
+    assert lib.wpk_conv2d_config_valid(h, L.FAMILIES["simt"], (ctypes.c_int32 * 7)(16, 4, 4, 1, 1, 1, 1)) == 1
     umma = (ctypes.c_int32 * 7)(64, 4, 1, 0, 0, 2, 128)
     g32 = (ctypes.c_int32 * 7)(64, 64, 8, 4, 1, 0, 0)
     assert lib.wpk_conv2d_config_valid(h, L.FAMILIES["umma"], umma) == 0

@@ -208,31 +208,35 @@ def test_gemm32_every_template(layout):
 @pytest.mark.parametrize("layout", ["nchw", "nhwc"])
 @pytest.mark.parametrize("dtype", ["f32", "tf32", "bf16", "f16"])
 def test_general_groups(dtype, layout):
-    """Grouped conv with 1 < groups (ResNeXt-style C/g = 4, g = 2, channel multiplier 2), default
-    (SIMT) config and two other tile templates: bit-exact in integer mode, within tolerance in
-    uniform mode."""
+    """Grouped conv with 1 < groups (ResNeXt-style C/g = 4, g = 2, channel multiplier 2): the
+    grouped-kernel default and other output vectors / pixels per thread, and two SIMT tile
+    templates: bit-exact in integer mode, within tolerance in uniform mode."""
     from paper_2008_04567_b200 import Conv2dPlan
     from _util import to_layout, from_layout
     layers = [ConvLayer("g32x4", 2, 128, 9, 11, 128, 3, 3, 1, 1, 1, 32), ConvLayer("g2s2", 1, 24, 13, 12, 40, 3, 3, 2, 1, 1, 2),
               ConvLayer("gmult", 2, 16, 8, 8, 32, 3, 3, 1, 1, 1, 16)]
     for L in layers:
         plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups, layout=layout, dtype=dtype)
-        assert plan.config[0] == 0, L.name
-        tiles = [None, [8, 8, 4, 2, 1, 2, 1], [32, 2, 2, 1, 2, 1, 1]]
+        assert plan.config[0] == 2, L.name
+        tiles = [None, (2, [1, 2, 64, 1, 0, 0, 0]), (2, [2, 4, 128, 1, 0, 0, 0]), (2, [4, 1, 512, 1, 0, 0, 0]),
+                 (0, [8, 8, 4, 2, 1, 2, 1]), (0, [32, 2, 2, 1, 2, 1, 1])]
         for mode in ("int", "uniform"):
             x, w, b = workloads.generate(L, dtype, mode, seed=71)
             ref = oracle.conv2d(x, w, b, stride=L.stride, pad=L.pad, dil=L.dil, groups=L.groups)
             xl, wl = to_layout(x, w, layout)
             xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
-            for genes in tiles:
-                if genes is not None:
-                    plan.set_config(0, genes)
+            for cfg in tiles:
+                if cfg is not None:
+                    if not plan.config_valid(*cfg):
+                        assert cfg[0] == 2 and (L.k // L.groups) % cfg[1][0], (L.name, cfg)
+                        continue
+                    plan.set_config(*cfg)
                 y = from_layout(plan.run(xl, wl, bc).cpu(), layout)
                 torch.cuda.synchronize()
                 if mode == "int":
                     assert_bit_exact(y, ref)
                 else:
-                    assert rel_error(dtype, y, ref) <= TOL[dtype], (L.name, genes)
+                    assert rel_error(dtype, y, ref) <= TOL[dtype], (L.name, cfg)
 
 
 @pytest.mark.parametrize("layout", ["nchw", "nhwc"])
