@@ -114,12 +114,25 @@ __global__ void dw_conv_kernel(const DwArgs a) {
 // General groups (1 < g, C/g or K/g > 1), the same thread layout with the
 // vector over VEC consecutive OUTPUT channels of one group (K/g % VEC == 0): every output of the
 // thread reads the same C/g input channels of its group, so each activation is loaded once per
-// (tap, channel) and multiplied into VEC accumulators; weights are pre-packed to [R][S][C/g][K] so
-// the VEC weights of one (r, s, c) are one vector load. Per output: taps in (r, s, c) order, fp32 FMA.
+// (tap, channel) and multiplied into VEC accumulators; weights are pre-packed to fp32 [R][S][C/g][K]
+// so the VEC weights of one (r, s, c) are one or two vector loads with no conversion. Per output: taps in (r, s, c) order, fp32 FMA.
+// VEC consecutive fp32 weights (16-byte vectors where they fit; K/g % VEC == 0 keeps them aligned)
+template <int VEC>
+__device__ __forceinline__ void load_wvec(float *wv, const float *src) {
+    if constexpr (VEC % 4 == 0) {
+#pragma unroll
+        for (int v = 0; v < VEC; v += 4) *reinterpret_cast<float4 *>(wv + v) = *reinterpret_cast<const float4 *>(src + v);
+    } else if constexpr (VEC == 2) {
+        *reinterpret_cast<float2 *>(wv) = *reinterpret_cast<const float2 *>(src);
+    } else {
+        wv[0] = src[0];
+    }
+}
+
 template <typename T, int VEC, int PIX>
 __global__ void grouped_conv_kernel(const DwArgs a) {
     const T *__restrict__ x = static_cast<const T *>(a.x);
-    const T *__restrict__ wp = static_cast<const T *>(a.w);   // [R][S][Cpg][K]
+    const float *__restrict__ wp = static_cast<const float *>(a.w);   // fp32 [R][S][Cpg][K]
     const T *__restrict__ b = static_cast<const T *>(a.b);
     T *__restrict__ y = static_cast<T *>(a.y);
     const int kvecs = a.K / VEC;
@@ -154,7 +167,7 @@ __global__ void grouped_conv_kernel(const DwArgs a) {
                                       (long long)cbase * a.xs_c
                                 : nullptr;
                 }
-                const T *wrs = wp + ((long long)(r * a.S + s) * a.Cpg) * a.K + k0;
+                const float *wrs = wp + ((long long)(r * a.S + s) * a.Cpg) * a.K + k0;
                 int c = 0;
                 if (a.xs_c == 1 && (a.Cpg & 3) == 0) {   // NHWC, C/g % 4 == 0: 4 channels per load
                     for (; c < a.Cpg; c += 4) {
@@ -170,40 +183,26 @@ __global__ void grouped_conv_kernel(const DwArgs a) {
                         }
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
-                            T wv[VEC];
-                            const T *wsrc = wrs + (long long)(c + j) * a.K;
-                            if constexpr (VEC * sizeof(T) == 16) *reinterpret_cast<uint4 *>(wv) = *reinterpret_cast<const uint4 *>(wsrc);
-                            else if constexpr (VEC * sizeof(T) == 8) *reinterpret_cast<uint2 *>(wv) = *reinterpret_cast<const uint2 *>(wsrc);
-                            else if constexpr (VEC * sizeof(T) == 4) *reinterpret_cast<uint32_t *>(wv) = *reinterpret_cast<const uint32_t *>(wsrc);
-                            else {
-#pragma unroll
-                                for (int v = 0; v < VEC; ++v) wv[v] = wsrc[v];
-                            }
+                            float wv[VEC];
+                            load_wvec<VEC>(wv, wrs + (long long)(c + j) * a.K);
 #pragma unroll
                             for (int i = 0; i < PIX; ++i) {
                                 if (!xs[i]) continue;
 #pragma unroll
-                                for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(xv[i][j], to_f<T>(wv[v]), acc[i][v]);
+                                for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(xv[i][j], wv[v], acc[i][v]);
                             }
                         }
                     }
                 }
                 for (; c < a.Cpg; ++c) {
-                    T wv[VEC];
-                    const T *wsrc = wrs + (long long)c * a.K;
-                    if constexpr (VEC * sizeof(T) == 16) *reinterpret_cast<uint4 *>(wv) = *reinterpret_cast<const uint4 *>(wsrc);
-                    else if constexpr (VEC * sizeof(T) == 8) *reinterpret_cast<uint2 *>(wv) = *reinterpret_cast<const uint2 *>(wsrc);
-                    else if constexpr (VEC * sizeof(T) == 4) *reinterpret_cast<uint32_t *>(wv) = *reinterpret_cast<const uint32_t *>(wsrc);
-                    else {
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) wv[v] = wsrc[v];
-                    }
+                    float wv[VEC];
+                    load_wvec<VEC>(wv, wrs + (long long)c * a.K);
 #pragma unroll
                     for (int i = 0; i < PIX; ++i) {
                         if (!xs[i]) continue;
                         const float xv = to_f<T>(xs[i][(long long)c * a.xs_c]);
 #pragma unroll
-                        for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(xv, to_f<T>(wv[v]), acc[i][v]);
+                        for (int v = 0; v < VEC; ++v) acc[i][v] = fmaf(xv, wv[v], acc[i][v]);
                     }
                 }
             }

@@ -190,9 +190,10 @@ __global__ void fold_bn_kernel(const T *__restrict__ w, const T *__restrict__ b,
         }
     }
 }
-// Grouped weights KCRS (src_kcrs) or KRSC, [K][C/g][R][S] -> [R][S][C/g][K].
+// Grouped weights KCRS (src_kcrs) or KRSC, [K][C/g][R][S] -> fp32 [R][S][C/g][K] (converted once
+// here instead of per use in the kernel's inner loop).
 template <typename T>
-__global__ void pack_grouped_kernel(const T *__restrict__ w, T *__restrict__ out, int K, int Cpg, int R, int S,
+__global__ void pack_grouped_kernel(const T *__restrict__ w, float *__restrict__ out, int K, int Cpg, int R, int S,
                                     int src_kcrs) {
     const long long total = (long long)K * Cpg * R * S;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -203,7 +204,8 @@ __global__ void pack_grouped_kernel(const T *__restrict__ w, T *__restrict__ out
         t /= Cpg;
         const int s = (int)(t % S);
         const int r = (int)(t / S);
-        out[i] = src_kcrs ? w[(((long long)k * Cpg + c) * R + r) * S + s] : w[(((long long)k * R + r) * S + s) * Cpg + c];
+        out[i] = static_cast<float>(src_kcrs ? w[(((long long)k * Cpg + c) * R + r) * S + s]
+                                             : w[(((long long)k * R + r) * S + s) * Cpg + c]);
     }
 }
 // Depthwise weights [C][R][S] (both layouts, C/g = 1) -> [R][S][C].
@@ -262,7 +264,7 @@ static void launch_aux_t(int which, const void *src, void *dst, const ConvDesc &
             (const T *)src, (T *)dst, d.k, d.c, d.r, d.s, cp, d.layout == WPK_NCHW);
     else if (which == 9)
         pack_grouped_kernel<T><<<grid_for((long long)d.k * (d.c / d.g) * d.r * d.s, sm), 256, 0, st>>>(
-            (const T *)src, (T *)dst, d.k, d.c / d.g, d.r, d.s, d.layout == WPK_NCHW);
+            (const T *)src, (float *)dst, d.k, d.c / d.g, d.r, d.s, d.layout == WPK_NCHW);
     else
         pack_rsc_kernel<T><<<grid_for((long long)d.c * d.r * d.s, sm), 256, 0, st>>>((const T *)src, (T *)dst, d.c,
                                                                                      d.r, d.s);
@@ -399,8 +401,9 @@ static WsLayout ws_layout(Plan &p, const Config &cfg, bool host_staging) {
             L.p_off = off; L.p_bytes = al256((size_t)g.splits * d.M() * d.k * 4); off += L.p_bytes;
             L.c_off = off; L.c_bytes = al256((size_t)g.m_tiles * g.n_tiles * (g.pair ? 2 : 1) * 4); off += L.c_bytes;
         }
-    } else if (cfg.family == WPK_FAMILY_DW) {   // [R][S][C] or, grouped, [R][S][C/g][K]
-        L.w_off = off; L.w_bytes = al256((size_t)d.k * (d.c / d.g) * d.r * d.s * e); off += L.w_bytes;
+    } else if (cfg.family == WPK_FAMILY_DW) {   // [R][S][C] (T) or, grouped, [R][S][C/g][K] (fp32)
+        const size_t we = (d.c == d.g && d.k == d.g) ? e : 4;
+        L.w_off = off; L.w_bytes = al256((size_t)d.k * (d.c / d.g) * d.r * d.s * we); off += L.w_bytes;
     } else if (cfg.family == WPK_FAMILY_GEMM32) {
         const int cp = (d.c + 3) / 4 * 4;   // channels padded to whole 16-byte vectors
         if (d.layout == WPK_NCHW || cp != d.c) {
