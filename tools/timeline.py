@@ -1,6 +1,9 @@
 """Per-CTA timeline of one tcgen05 conv launch (globaltimer ns, relative to the earliest CTA start):
 start, setup done, first full stage, first tile MMAs issued, first tile epilogue done, all epilogues
-done, CTA end.  usage: python tools/timeline.py LAYER [genes]"""
+done, CTA end.  usage: python tools/timeline.py LAYER [genes]
+Note: the "end" stamp (thread 0 after the final CTA barrier) reads earlier than the epilogue warps'
+"epi_all_done" stamp although a shared-memory flag written by the epilogue before the barrier is
+always visible to thread 0 after it (checked): compare stamps within one warp's role only."""
 import ctypes, sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, numpy as np
