@@ -250,7 +250,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="wpk", choices=["wpk", "reference"])
     ap.add_argument("--batch", type=int, default=32, help="images per GPU")
-    ap.add_argument("--tune-budget", type=int, default=64, help="distinct configs measured per unique layer")
+    ap.add_argument("--tune-budget", type=int, default=128, help="distinct configs measured per unique layer")
     ap.add_argument("--graph-refine", type=int, default=3,
                     help="after the search, try each layer's next-best N measured configs in the whole-step graph")
     ap.add_argument("--ga-pop", type=int, default=12,
