@@ -400,13 +400,15 @@ def _residual_case(L, dtype, layout, seed):
 @pytest.mark.parametrize("layout", ["nchw", "nhwc"])
 @pytest.mark.parametrize("dtype", ["f32", "tf32", "bf16", "f16"])
 def test_residual_epilogue(dtype, layout):
-    """Epilogue 3, y = relu(conv + b + z): every family (SIMT for f32, tcgen05 with TMA-store and
-    direct epilogues, pairs, both gathers, depthwise) is bit-exact against the oracle."""
+    """Epilogue 3, y = relu(conv + b + z): every family (GEMM32 incl. split-K and SIMT for f32, tcgen05
+    with TMA-store and direct epilogues, pairs, both gathers, depthwise and grouped) is bit-exact
+    against the oracle."""
     from paper_2008_04567_b200 import Conv2dPlan
     from _util import to_layout, from_layout
     cases = [(ConvLayer("r3", 2, 64, 11, 13, 128, 3, 3, 1, 1), None),
              (ConvLayer("r1", 1, 96, 9, 7, 200, 1, 1, 1, 0), None),
-             (ConvLayer("rdw", 2, 32, 10, 9, 32, 3, 3, 2, 1, 1, 32), None)]
+             (ConvLayer("rdw", 2, 32, 10, 9, 32, 3, 3, 2, 1, 1, 32), None),
+             (ConvLayer("rgrp", 2, 32, 10, 9, 48, 3, 3, 1, 1, 1, 4), None)]
     for L, _ in cases:
         x, w, b, z, ref = _residual_case(L, dtype, layout, seed=41)
         plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups, layout=layout,
@@ -415,8 +417,9 @@ def test_residual_epilogue(dtype, layout):
         zl = z.permute(0, 2, 3, 1).contiguous() if layout == "nhwc" else z.contiguous()
         xl, wl, bc, zc = xl.cuda(), wl.cuda(), b.cuda(), zl.cuda()
         configs = [plan.config]
-        if dtype == "f32" and L.groups == 1:   # the paper's SIMT template as well as the GEMM32 default
-            configs += [(0, [16, 4, 4, 1, 1, 1, 1]), (0, [8, 8, 4, 2, 1, 2, 4])]
+        if dtype == "f32" and L.groups == 1:   # the paper's SIMT template, GEMM32 default and split-K
+            configs += [(0, [16, 4, 4, 1, 1, 1, 1]), (0, [8, 8, 4, 2, 1, 2, 4]), (3, [64, 64, 8, 4, 2, 0, 0]),
+                        (3, [128, 64, 16, 8, 4, 0, 0])]
         if plan.config[0] == 1:
             configs += [(1, [128, 4, 1, 0, 0, 2, 128]), (1, [64, 3, 1, 1, 0, 4, 256]), (1, [256, 3, 1, 2, 0, 1, 256])]
             assert not plan.config_valid(1, [128, 4, 2, 0, 0, 2, 128])   # residual plans: SPLIT_K = 1 only
