@@ -150,8 +150,10 @@ WPK_API void wpk_tune_options_init(wpk_tune_options *opts);
 WPK_API wpk_status wpk_conv2d_output_dims(const wpk_conv2d_shape *shape, int32_t *p, int32_t *q);
 
 /* Validate the shape, form the implicit-GEMM view, choose the kernel family for (dtype, groups,
- * alignment) and a deterministic valid default config. Host only: no CUDA call is made until the
- * first run/tune. `device` is the CUDA ordinal the plan will run on. *out owns host state only. */
+ * alignment) and a deterministic valid default config: groups > 1 -> WPK_FAMILY_DW (depthwise or
+ * grouped kernel); WPK_F32 -> WPK_FAMILY_GEMM32; tf32/bf16/f16 -> WPK_FAMILY_UMMA when the TMA
+ * im2col limits hold, else WPK_FAMILY_SIMT. Host only: no CUDA call is made until the first
+ * run/tune. `device` is the CUDA ordinal the plan will run on. *out owns host state only. */
 WPK_API wpk_status wpk_conv2d_plan(const wpk_conv2d_shape *shape, wpk_dtype dtype, int device, wpk_plan *out);
 
 /* Search the plan's configuration space with GA / RL / random search, at most `budget` distinct
