@@ -260,3 +260,30 @@ def test_tuning_cache_roundtrip(tmp_path):
     assert r4.measured > 0
     other = Conv2dPlan(1, 4, 9, 9, 8, 3, 3, 1, 1, layout="nchw", dtype="f32", device=0)
     assert other.tune("ga", 50, **kw).measured > 0  # different operator: miss
+
+
+@pytest.mark.parametrize("family,shape,dtype", [
+    ("gemm32", dict(n=2, c=64, h=14, w=14, k=128, r=3, s=3, stride=1, pad=1), "f32"),
+    ("dw", dict(n=2, c=64, h=14, w=14, k=128, r=3, s=3, stride=1, pad=1, groups=16), "bf16"),
+])
+def test_new_family_spaces_search_valid_and_deterministic(family, shape, dtype):
+    """The exact-fp32 GEMM32 space (incl. SPLIT_K) and the grouped-kernel space (VEC_C | K/groups) are
+    searchable: GA and RL on a synthetic surface return a valid config of the family, the same one
+    for the same seed, and GA reaches the surface's optimum when it is valid."""
+    names, doms = L.family_describe(family)
+    star = [d[-1] if len(d) > 1 else d[0] for d in doms]
+    syn = [5.0] + [0.7] * 7 + star
+    for search in ("ga", "rl"):
+        res = []
+        for _ in range(2):
+            plan = Conv2dPlan(**shape, layout="nhwc", dtype=dtype, device=0)
+            kw = dict(rl_hidden=[32, 32, 32, 32], rl_horizon=8) if search == "rl" else {}
+            r = plan.tune(search, 48, eval_mode="synthetic", synthetic=syn, family=family, seed=7, **kw)
+            assert r.family == L.FAMILIES[family]
+            assert plan.config_valid(r.family, list(r.genes)), (search, r.genes)
+            res.append((tuple(r.genes), r.best_us))
+        assert res[0] == res[1], search
+    plan = Conv2dPlan(**shape, layout="nhwc", dtype=dtype, device=0)
+    if plan.config_valid(L.FAMILIES[family], star):
+        r = plan.tune("ga", 400, eval_mode="synthetic", synthetic=syn, family=family, seed=3)
+        assert list(r.genes) == star and abs(r.best_us - 5.0) < 1e-9
