@@ -170,3 +170,16 @@ def test_residual_epilogue_host_validation():
     assert lib.wpk_conv2d_run(plan.handle, fake, fake, fake, fake, None) == 1          # WPK_ERR_INVALID_ARGUMENT
     assert lib.wpk_conv2d_run_residual(plan.handle, fake, fake, fake, None, fake, None) == 1
     assert lib.wpk_conv2d_run_host(plan.handle, fake, fake, fake, fake, None) == 1
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU or eager fallback: with the shared library absent the binding raises on first use
+    (checked in a fresh interpreter pointing WPK_LIB at a path that does not exist)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, WPK_LIB=str(tmp_path / "absent" / "libwpk.so"))
+    code = ("import paper_2008_04567_b200._lib as L\n"
+            "try:\n    L.load()\nexcept RuntimeError as e:\n    print('RAISED', 'no CPU fallback' in str(e))\n")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=120)
+    assert "RAISED True" in out.stdout, out.stdout + out.stderr
