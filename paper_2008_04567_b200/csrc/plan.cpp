@@ -332,7 +332,10 @@ Config default_config(const ConvDesc &d, int family) {
     const long long mt = (d.M() + 127) / 128;
     if (bn == 256 && mt * ((d.k + 255) / 256) < 120) bn = 128;
     // large layers: a tcgen05 CTA pair (256 x BLOCK_N over two SMs) halves B traffic per SM
-    const bool big = ((d.M() + 255) / 256) * ((d.k + bn - 1) / bn) >= 2 * 148 && bn >= 128 && d.c >= 64;
+    // (not for short-K layers: with 1-2 K blocks per tile a pair's accumulators are seen ~3 us
+    // after the commit, DESIGN.md §10 finding 13, while 1-CTA 128 x 256 tiles stream)
+    const int kblocks = d.r * d.s * ((d.c + 63) / 64);
+    const bool big = ((d.M() + 255) / 256) * ((d.k + bn - 1) / bn) >= 2 * 148 && bn >= 128 && d.c >= 64 && kblocks > 2;
     c.genes[0] = bn; c.genes[1] = 4; c.genes[2] = 1; c.genes[3] = 0; c.genes[4] = (d.c <= 4) ? 3 : (d.c < 16) ? 1 : 0;
     c.genes[5] = 2; c.genes[6] = 128;
     if (big) { c.genes[3] = 2; c.genes[6] = 256; }
