@@ -260,7 +260,7 @@ def main():
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-points", type=int, default=1024)
-    ap.add_argument("--cpu-sample-points", type=int, default=12288)
+    ap.add_argument("--cpu-sample-points", type=int, default=512000, help="oracle outputs per unique layer for cpu_baseline (~10 s of host compute)")
     ap.add_argument("--layers-json", default=None, help="also write the per-layer table here")
     ap.add_argument("--configs-out", default=None, help="write the per-layer chosen configs (JSON)")
     ap.add_argument("--configs-in", default=None, help="use these per-layer configs instead of tuning")
