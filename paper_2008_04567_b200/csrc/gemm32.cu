@@ -4,7 +4,8 @@
 // activations, KRSC weights), every product an fp32 FMA accumulated in increasing kg order (the
 // result is a fixed function of the inputs, within the fp32 tolerance of the float64 oracle).
 // CTA tile BLOCK_M x BLOCK_N, K step BLOCK_K; each thread owns THREAD x THREAD outputs. Operand
-// tiles are gathered into registers (16-byte vectors along c when C % 4 == 0), stored transposed
+// tiles are gathered into registers (16-byte vectors along c; the launcher pads C to a multiple of
+// 4), stored transposed
 // into double-buffered shared memory ([k][m] and [k][n]) and consumed as outer products; the next
 // K step's loads are in flight while the current one is computed. SPLIT_K > 1 (deep layers with
 // few tiles) writes per-split fp32 partials that gemm32_reduce_kernel sums in split order.
@@ -20,10 +21,13 @@
 
 namespace wpk {
 
-// 8x8 thread tiles: at most 128 registers per thread (512 / threads CTAs per SM), except the
-// 64-thread BLOCK_K 16 tile, whose 4 staged A vectors per thread would then spill
+// 8x8 thread tiles: at most 128 registers per thread (512 / threads CTAs per SM), except where
+// that spills (ptxas -v): the 64-thread BLOCK_K 16 tile and the 128 x 64 tile get 4 / 3 CTAs
 constexpr int gemm32_min_blocks(int bm, int bn, int bk, int tt) {
-    return tt != 8 ? 1 : ((bm / tt) * (bn / tt) == 64 && bk == 16) ? 4 : 512 / ((bm / tt) * (bn / tt));
+    return tt != 8 ? 1
+           : ((bm / tt) * (bn / tt) == 64 && bk == 16) ? 4
+           : (bm == 128 && bn == 64) ? 3
+                                     : 512 / ((bm / tt) * (bn / tt));
 }
 
 template <int BM, int BN, int BK, int TT>
@@ -38,8 +42,7 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT), gemm32_min_blocks(BM, B
     const long long m0 = (long long)blockIdx.x * BM;
     const int n0 = blockIdx.y * BN;
     const float *x = a.x, *w = a.w;
-    const int Kg = a.R * a.S * a.C;
-    const bool vec = (a.C % 4) == 0;
+    const int Kg = a.R * a.S * a.C;   // a.C % 4 == 0 (the launcher pads C): 16-byte operand vectors
 
     // rows of the A tile this thread loads: image, top-left input coordinate (or invalid)
     int an[AL], ah[AL], aw[AL];
@@ -61,32 +64,14 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT), gemm32_min_blocks(BM, B
         for (int i = 0; i < AL; ++i) {
             const int idx = tid + i * NT;
             const int kg = k0 + (idx % (BK / 4)) * 4;
-            float v[4] = {0.f, 0.f, 0.f, 0.f};
-            if (an[i] >= 0) {
-                if (vec) {
-                    if (kg < Kg) {
-                        const int c = kg % a.C, rs = kg / a.C, s = rs % a.S, r = rs / a.S;
-                        const int h = ah[i] + r * a.dh, ww = aw[i] + s * a.dw;
-                        if (h >= 0 && h < a.H && ww >= 0 && ww < a.W) {
-                            const float4 t = *reinterpret_cast<const float4 *>(
-                                x + (((long long)an[i] * a.H + h) * a.W + ww) * a.C + c);
-                            v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int kk = kg + e;
-                        if (kk < Kg) {
-                            const int c = kk % a.C, rs = kk / a.C, s = rs % a.S, r = rs / a.S;
-                            const int h = ah[i] + r * a.dh, ww = aw[i] + s * a.dw;
-                            if (h >= 0 && h < a.H && ww >= 0 && ww < a.W)
-                                v[e] = x[(((long long)an[i] * a.H + h) * a.W + ww) * a.C + c];
-                        }
-                    }
-                }
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (an[i] >= 0 && kg < Kg) {   // 4 channels of one tap (kg % 4 == 0, C % 4 == 0)
+                const int c = kg % a.C, rs = kg / a.C, s = rs % a.S, r = rs / a.S;
+                const int h = ah[i] + r * a.dh, ww = aw[i] + s * a.dw;
+                if (h >= 0 && h < a.H && ww >= 0 && ww < a.W)
+                    v = *reinterpret_cast<const float4 *>(x + (((long long)an[i] * a.H + h) * a.W + ww) * a.C + c);
             }
-            ra[i] = make_float4(v[0], v[1], v[2], v[3]);
+            ra[i] = v;
         }
     };
     auto load_b = [&](int k0) {
@@ -95,19 +80,9 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT), gemm32_min_blocks(BM, B
             const int idx = tid + i * NT;
             const int col = idx / (BK / 4), kg = k0 + (idx % (BK / 4)) * 4;
             const int n = n0 + col;
-            float v[4] = {0.f, 0.f, 0.f, 0.f};
-            if (idx < B4 && n < a.K) {
-                const float *wr = w + (long long)n * Kg;
-                if (vec && kg + 3 < Kg) {
-                    const float4 t = *reinterpret_cast<const float4 *>(wr + kg);
-                    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (kg + e < Kg) v[e] = wr[kg + e];
-                }
-            }
-            rb[i] = make_float4(v[0], v[1], v[2], v[3]);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (idx < B4 && n < a.K && kg < Kg) v = *reinterpret_cast<const float4 *>(w + (long long)n * Kg + kg);
+            rb[i] = v;
         }
     };
     auto store = [&](int buf) {

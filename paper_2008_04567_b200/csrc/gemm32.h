@@ -5,7 +5,7 @@
 namespace wpk {
 
 struct Gemm32Args {
-    const float *x;   // NHWC [N][H][W][C]
+    const float *x;   // NHWC [N][H][W][C], C % 4 == 0 (zero-padded by the launcher otherwise)
     const float *w;   // KRSC [K][R][S][C]
     const float *b;   // [K] (epilogue >= 1)
     float *y;         // output, element (n, k, p, q) at n*ys_n + k*ys_k + p*ys_p + q*ys_q
