@@ -210,12 +210,19 @@ __global__ void __launch_bounds__((BM / TT) * (BN / TT), gemm32_min_blocks(BM, B
 }
 
 // Split-K reduction: y = epilogue(sum over splits 0..S-1 in increasing order); one thread per output.
+// All splits' loads are issued before the in-order sum (SPLIT_K <= 8), so one L2/HBM latency is
+// paid per output instead of one per split.
 __global__ void gemm32_reduce_kernel(const Gemm32Args a, int splits) {
     const long long total = a.M * a.K;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        float o = a.partial[i];
-        for (int z = 1; z < splits; ++z) o += a.partial[(long long)z * total + i];
+        float v[8];
+#pragma unroll
+        for (int z = 0; z < 8; ++z) v[z] = z < splits ? __ldcs(a.partial + (long long)z * total + i) : 0.f;
+        float o = v[0];
+#pragma unroll
+        for (int z = 1; z < 8; ++z)
+            if (z < splits) o += v[z];
         const long long m = i / a.K;
         const int k = (int)(i - m * a.K);
         const int n = (int)(m / a.PQ);
