@@ -34,6 +34,12 @@
 #include "ptx.cuh"
 #include "umma_conv.h"
 
+#ifdef WPK_TIMELINE
+#define WPK_DBG_FLAGS(a) ((a).dbg_flags)   // experiment switches (tools only)
+#else
+#define WPK_DBG_FLAGS(a) 0
+#endif
+
 namespace wpk {
 
 template <int DT> struct OutT;
@@ -125,7 +131,7 @@ __device__ __forceinline__ void stage_and_store(EpiCtx &E, const UmmaArgs &a, co
         ptx::st_shared_v4(buf + ((uint32_t)(j ^ (E.lane & 7)) << 4), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
     ptx::fence_proxy_async_smem();
     __syncwarp();
-    if (E.lane == 0 && !(a.dbg_flags & 2)) {
+    if (E.lane == 0 && !(WPK_DBG_FLAGS(a) & 2)) {
         if constexpr (FINAL) ptx::tma_store_2d(tmY, bufp, k0, mrow);
         else ptx::tma_store_3d(tmY, bufp, k0, mrow, split);
         ptx::bulk_commit();
@@ -578,7 +584,7 @@ __device__ __forceinline__ void segment_gather(const UmmaArgs &a, uint8_t *smA, 
         for (int hh = 0; hh < 2; ++hh) {
             rptr[hh] = nullptr;
             const long long m = (long long)wp.mt * a.bm + hh * 128 + t;
-            if (hh < nsub && m < a.M && !(a.dbg_flags & 1)) {
+            if (hh < nsub && m < a.M && !(WPK_DBG_FLAGS(a) & 1)) {
                 const int n = (int)(m / a.PQ);
                 const int rem = (int)(m - (long long)n * a.PQ);
                 const int p = rem / a.Q, q = rem - (rem / a.Q) * a.Q;
@@ -685,7 +691,11 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
     uint64_t *datab = bars + 27;      // EK_CSPLIT: every peer delivered its partials (8 (S - 1) arrives)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef WPK_TIMELINE   // per-CTA globaltimer stamps for tools/timeline.py (libwpk_timeline.so only)
     unsigned long long *dbg = a.dbg ? a.dbg + blockIdx.x * 64 : nullptr;
+#else                 // production build: every stamp and experiment switch folds away
+    unsigned long long *const dbg = nullptr;
+#endif
     if (dbg && threadIdx.x == 0) dbg[0] = ptx::globaltimer();
 
     if (warp == 0 && lane == 0) {
@@ -765,7 +775,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     // experiment (dbg_flags & 8): issue times of the first tile's A (B) loads
-                    if (dbg && (a.dbg_flags & 8) && w == wstart && kb - kb0 < 16 && half == 0)
+                    if (dbg && (WPK_DBG_FLAGS(a) & 8) && w == wstart && kb - kb0 < 16 && half == 0)
                         dbg[(isA ? 16 : 32) + (kb - kb0)] = ptx::globaltimer();
                     uint8_t *dst = dst0 + stage * sstride;
                     if constexpr (kPair) {
@@ -834,14 +844,14 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const long long dit = (w - wstart) / wstep;     // debug: per-tile events of the first 8 tiles
-                if (dbg && dit < 8 && !(a.dbg_flags & 8)) dbg[16 + dit * 6 + 0] = ptx::globaltimer();
+                if (dbg && dit < 8 && !(WPK_DBG_FLAGS(a) & 8)) dbg[16 + dit * 6 + 0] = ptx::globaltimer();
                 const uint32_t d_tmem = tmem_base + acc * acc_cols;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     if (dbg && w == wstart && kb == kb0) dbg[2] = ptx::globaltimer();
-                    if (dbg && dit < 8 && kb == kb0 && !(a.dbg_flags & 8)) dbg[16 + dit * 6 + 1] = ptx::globaltimer();
-                    if (dbg && (a.dbg_flags & 8) && w == wstart && kb - kb0 < 16) dbg[48 + (kb - kb0)] = ptx::globaltimer();
+                    if (dbg && dit < 8 && kb == kb0 && !(WPK_DBG_FLAGS(a) & 8)) dbg[16 + dit * 6 + 1] = ptx::globaltimer();
+                    if (dbg && (WPK_DBG_FLAGS(a) & 8) && w == wstart && kb - kb0 < 16) dbg[48 + (kb - kb0)] = ptx::globaltimer();
                     const uint64_t ad = a_desc0 + (uint64_t)((stage * a_bytes) >> 4);
                     const uint64_t bd = b_desc0 + (uint64_t)((stage * b_bytes) >> 4);
                     if constexpr (kPair) {
@@ -863,8 +873,8 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 if constexpr (kPair) ptx::umma_commit2_multicast(&tfull[acc]);   // both CTAs' halves ready
                 else ptx::umma_commit(&tfull[acc]);                               // accumulator ready
                 if (dbg && w == wstart) dbg[3] = ptx::globaltimer();
-                if (dbg && dit < 8 && !(a.dbg_flags & 8)) dbg[16 + dit * 6 + 2] = ptx::globaltimer();
-                if (dbg && dit < 8 && (a.dbg_flags & 4) && !(a.dbg_flags & 8)) {   // experiment: MMA completion seen by a spinning thread
+                if (dbg && dit < 8 && !(WPK_DBG_FLAGS(a) & 8)) dbg[16 + dit * 6 + 2] = ptx::globaltimer();
+                if (dbg && dit < 8 && (WPK_DBG_FLAGS(a) & 4) && !(WPK_DBG_FLAGS(a) & 8)) {   // experiment: MMA completion seen by a spinning thread
                     while (!ptx::mbar_test_wait(&tfull[acc], acc_phase)) {}
                     dbg[16 + dit * 6 + 5] = ptx::globaltimer();
                 }
@@ -895,7 +905,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             const long long dit = (w - wstart) / wstep;
-            if (dbg && warp == 4 && lane == 0 && dit < 8 && !(a.dbg_flags & 8)) dbg[16 + dit * 6 + 3] = ptx::globaltimer();
+            if (dbg && warp == 4 && lane == 0 && dit < 8 && !(WPK_DBG_FLAGS(a) & 8)) dbg[16 + dit * 6 + 3] = ptx::globaltimer();
             // split-K (EK_SPLIT): the tile's last split owns the output; it waits until the other
             // splits have published their partials (they precede it in the static schedule, so they
             // are resident or done: no deadlock), then reduces them in split order.
@@ -990,7 +1000,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             if (dbg && warp == 4 && lane == 0 && w == wstart) dbg[4] = ptx::globaltimer();
             if (dbg && warp == 4 && lane == 0 && dit < 8) {
                 dbg[8 + dit] = ptx::globaltimer();
-                if (!(a.dbg_flags & 8)) dbg[16 + dit * 6 + 4] = ptx::globaltimer();
+                if (!(WPK_DBG_FLAGS(a) & 8)) dbg[16 + dit * 6 + 4] = ptx::globaltimer();
             }
             if (lane == 0) {                                  // TMEM free: the MMA may start the next tile
                 if constexpr (kPair) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));

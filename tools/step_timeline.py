@@ -5,6 +5,14 @@ between consecutive kernels under programmatic dependent launch.
 usage: python tools/step_timeline.py CONFIGS_JSON"""
 import ctypes, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# the production library compiles the stamps out: use the timeline build (make -C
+# paper_2008_04567_b200/csrc timeline)
+_TL = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2008_04567_b200",
+                   "libwpk_timeline.so")
+if not os.environ.get("WPK_LIB"):
+    if not os.path.exists(_TL):
+        sys.exit(f"{_TL} missing: run `make -C paper_2008_04567_b200/csrc -j16 timeline`")
+    os.environ["WPK_LIB"] = _TL
 import numpy as np
 import torch
 import workloads

@@ -6,6 +6,14 @@ Note: the "end" stamp (thread 0 after the final CTA barrier) reads earlier than 
 always visible to thread 0 after it (checked): compare stamps within one warp's role only."""
 import ctypes, sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# the production library compiles the stamps out: use the timeline build (make -C
+# paper_2008_04567_b200/csrc timeline)
+_TL = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2008_04567_b200",
+                   "libwpk_timeline.so")
+if not os.environ.get("WPK_LIB"):
+    if not os.path.exists(_TL):
+        sys.exit(f"{_TL} missing: run `make -C paper_2008_04567_b200/csrc -j16 timeline`")
+    os.environ["WPK_LIB"] = _TL
 import torch, numpy as np
 import workloads
 from paper_2008_04567_b200 import Conv2dPlan, _lib
