@@ -141,7 +141,7 @@ __device__ __forceinline__ void stage_and_store(EpiCtx &E, const UmmaArgs &a, co
 
 // One 32-row x 128-byte chunk through smem + TMA store. FINAL: +bias, ReLU, RN-round to T (64
 // columns for 16-bit T, 32 for fp32); else fp32 split-K partials (32 columns) into [split][M][K].
-template <typename T, bool FINAL>
+template <typename T, bool FINAL, bool RES = false>
 __device__ __forceinline__ void epi_chunk_tma(EpiCtx &E, const UmmaArgs &a, const CUtensorMap *tmY, uint32_t taddr,
                                               int k0, int mrow, int split) {
     constexpr bool k16 = FINAL && sizeof(T) == 2;
@@ -149,9 +149,11 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx &E, const UmmaArgs &a, cons
     ptx::tmem_ld32_nowait(taddr, raw);
     if constexpr (k16) ptx::tmem_ld32_nowait(taddr + 32, raw + 32);
     // residual (epilogue 3): this lane's row, the chunk's 128 bytes, loaded while TMEM drains
-    uint4 zr[8];
-    const bool res = FINAL && a.epilogue == 3;
-    if (res) {
+    // (a compile-time switch: the residual variant is its own kernel instantiation, so the plain
+    // epilogue does not carry the residual's 32 registers)
+    uint4 zr[RES ? 8 : 1];
+    constexpr bool res = FINAL && RES;
+    if constexpr (res) {
         const long long m = (long long)mrow + E.lane;
         const uint4 *zp = reinterpret_cast<const uint4 *>(static_cast<const T *>(a.z) + m * a.K + k0);
 #pragma unroll
@@ -166,7 +168,7 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx &E, const UmmaArgs &a, cons
             float v[4] = {__uint_as_float(raw[4 * q]), __uint_as_float(raw[4 * q + 1]), __uint_as_float(raw[4 * q + 2]),
                           __uint_as_float(raw[4 * q + 3])};
             bias_relu4(v, E.sBias, k0 + 4 * q, false);
-            if (res) {   // 4 16-bit residual values = half of zr[q / 2]
+            if constexpr (res) {   // 4 16-bit residual values = half of zr[q / 2]
                 const uint32_t lo = (q & 1) ? zr[q >> 1].z : zr[q >> 1].x, hi = (q & 1) ? zr[q >> 1].w : zr[q >> 1].y;
                 v[0] += to_f2(lo, 0, (T *)nullptr); v[1] += to_f2(lo, 1, (T *)nullptr);
                 v[2] += to_f2(hi, 0, (T *)nullptr); v[3] += to_f2(hi, 1, (T *)nullptr);
@@ -184,7 +186,7 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx &E, const UmmaArgs &a, cons
             float v[4] = {__uint_as_float(raw[4 * q]), __uint_as_float(raw[4 * q + 1]), __uint_as_float(raw[4 * q + 2]),
                           __uint_as_float(raw[4 * q + 3])};
             bias_relu4(v, E.sBias, k0 + 4 * q, false);
-            if (res) {
+            if constexpr (res) {
                 v[0] += __uint_as_float(zr[q].x); v[1] += __uint_as_float(zr[q].y);
                 v[2] += __uint_as_float(zr[q].z); v[3] += __uint_as_float(zr[q].w);
             }
@@ -655,7 +657,7 @@ __device__ __forceinline__ void segment_gather(const UmmaArgs &a, uint8_t *smA, 
 // 12 warps (16 with gather producers): 0 = A producer, 1 = TMEM allocator + MMA issuer,
 // 2 = B producer, 3 = spare, 4..11 = epilogue (two groups of four; warp w reads TMEM lanes
 // [32*(w%4), +32)), 12..15 = gather producers.
-template <int DT, int AK, int EK>
+template <int DT, int AK, int EK, bool RES = false>
 __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
     umma_conv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmP,
@@ -986,7 +988,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                     const int k0 = n0 + c0;
                     if (k0 >= a.K) break;   // warp-uniform
                     if constexpr (EK == EK_TMA) {
-                        epi_chunk_tma<T, true>(E, a, &tmY, tbase + c0, k0, mrow, 0);
+                        epi_chunk_tma<T, true, RES>(E, a, &tmY, tbase + c0, k0, mrow, 0);
                     } else if constexpr (EK == EK_SPLIT) {
                         if (owner) epi_chunk_owner<T>(E, a, &tmY, tbase + c0, k0, mrow);
                         else epi_chunk_tma<T, false>(E, a, &tmP, tbase + c0, k0, mrow, wp.split);
@@ -1038,31 +1040,33 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
 }
 
 // ---- launch of one (dtype) instantiation family -----------------------------------------------
-template <int DT, int AK, int EK>
+template <int DT, int AK, int EK, bool RES = false>
 static cudaError_t launch_variant(cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                                   const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return e;
         // one shared-memory carveout for every variant and config: consecutive convs whose dynamic
         // smem differs would otherwise get different L1/smem splits, and an SM can only switch
         // carveout once drained -- no overlap of one conv's tail with the next conv's CTAs
         if (!getenv("WPK_NO_CARVEOUT")) {
-            e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK, RES>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      (int)cudaSharedmemCarveoutMaxShared);
             if (e != cudaSuccess) return e;
         }
         attr_done = true;
     }
-    return cudaLaunchKernelEx(&lc, umma_conv_kernel<DT, AK, EK>, tmA, tmB, tmY, tmP, a);
+    return cudaLaunchKernelEx(&lc, umma_conv_kernel<DT, AK, EK, RES>, tmA, tmB, tmY, tmP, a);
 }
 
 template <int DT, int AK>
 static cudaError_t launch_ak(int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                              const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
-    if (ek == EK_TMA) return launch_variant<DT, AK, EK_TMA>(lc, tmA, tmB, tmY, tmP, a);
+    if (ek == EK_TMA)
+        return a.epilogue == 3 ? launch_variant<DT, AK, EK_TMA, true>(lc, tmA, tmB, tmY, tmP, a)
+                               : launch_variant<DT, AK, EK_TMA, false>(lc, tmA, tmB, tmY, tmP, a);
     if (ek == EK_SPLIT) return launch_variant<DT, AK, EK_SPLIT>(lc, tmA, tmB, tmY, tmP, a);
     if (ek == EK_CSPLIT) {
         if constexpr (AK == AK_TMA) return launch_variant<DT, AK, EK_CSPLIT>(lc, tmA, tmB, tmY, tmP, a);
