@@ -576,7 +576,8 @@ __device__ __forceinline__ void segment_gather(const UmmaArgs &a, uint8_t *smA, 
     const char *xb = static_cast<const char *>(a.x);
     const uint32_t swz = (uint32_t)(t & 7) << 4;       // rows t and 128 + t share the swizzle phase
     uint32_t stage = 0, phase = 0;
-    uint32_t pend[LAG];                                // stages issued but not yet signalled (FIFO)
+    // stages issued but not yet signalled: the npend stages before `stage` (in issue order, so no
+    // FIFO array -- a runtime-indexed array would live in local memory on this hot loop)
     int npend = 0;
     for (long long w = wstart; w < a.work; w += wstep) {
         const WorkPos wp = decode_work(w, a);
@@ -638,12 +639,14 @@ __device__ __forceinline__ void segment_gather(const UmmaArgs &a, uint8_t *smA, 
                 ptx::cp_async_wait<LAG>();
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&full[pend[0]]);
-#pragma unroll
-                for (int i = 0; i + 1 < LAG; ++i) pend[i] = pend[i + 1];
+                if (lane == 0) {
+                    uint32_t oldest = stage + (uint32_t)a.stages - LAG;
+                    if (oldest >= (uint32_t)a.stages) oldest -= (uint32_t)a.stages;
+                    ptx::mbar_arrive(&full[oldest]);
+                }
                 --npend;
             }
-            pend[npend++] = stage;
+            ++npend;
             if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
         }
     }
@@ -651,7 +654,11 @@ __device__ __forceinline__ void segment_gather(const UmmaArgs &a, uint8_t *smA, 
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0)
-        for (int i = 0; i < npend; ++i) ptx::mbar_arrive(&full[pend[i]]);
+        for (int i = 0; i < npend; ++i) {
+            uint32_t st = stage + (uint32_t)a.stages - (uint32_t)npend + (uint32_t)i;
+            if (st >= (uint32_t)a.stages) st -= (uint32_t)a.stages;
+            ptx::mbar_arrive(&full[st]);
+        }
 }
 
 // 12 warps (16 with gather producers): 0 = A producer, 1 = TMEM allocator + MMA issuer,
