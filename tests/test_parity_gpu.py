@@ -341,12 +341,12 @@ def test_resnet50_n32_sampled_bf16(layer):
     assert torch.equal(got.float() + 0, want.float() + 0)
 
 
-_TUNED = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r1j_tuned_configs.json")
+_TUNED = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r1k_tuned_configs.json")
 
 
 @pytest.mark.parametrize("layer", workloads.resnet50(32), ids=lambda l: l.name)
 def test_resnet50_n32_bench_configs_sampled(layer):
-    """The configs the bench tuned (profiles/r1j_tuned_configs.json, committed): full-size layer,
+    """The configs the bench tuned (profiles/r1k_tuned_configs.json, committed): full-size layer,
     uniform inputs, sampled outputs vs the oracle within the bf16 tolerance; plus exact-integer
     inputs bit-exact on the same samples."""
     import json
