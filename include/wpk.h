@@ -116,7 +116,8 @@ typedef struct {
     int32_t l2_flush;         /* 1: overwrite a >= 2x L2 buffer before every timed rep (default) */
     int32_t eval_mode;        /* wpk_eval_mode (default MEASURED)                               */
     int32_t family;           /* wpk_family to search; WPK_FAMILY_AUTO = the plan's default      */
-    const char *record_path;  /* if set: append every measured record as JSONL                  */
+    const char *record_path;  /* if set: append every measured record as JSONL (with world > 1
+                               * every rank writes the same gathered table: give each its own path) */
     const char *replay_path;  /* if set with EVAL_REPLAY: read records instead of measuring     */
     const char *log_path;     /* if set: per-generation (GA) / per-step (RL) history JSONL      */
     double synthetic[1 + 2 * WPK_NUM_GENES]; /* EVAL_SYNTHETIC: base, w[7], c*[7] */
@@ -137,13 +138,20 @@ typedef struct {
                                * operator identity (shapes, filter, stride, padding;
                                * plus dilation, groups, dtype, layout, epilogue) + family + device.
                                * A hit whose recorded budget >= the request costs 0 evaluations.
-                               * Writes are atomic (temp file + rename).                        */
+                               * Writes are atomic (temp file + rename). With world > 1 a hit is
+                               * used only if every rank's lookup returns the same record.       */
+    int32_t finalists;        /* EVAL_MEASURED: the top-k configs by measured beta are re-timed on
+                               * EVERY rank after the search and the one with the lowest median
+                               * across ranks is chosen (SURVEY.md 8(d) protocol item 2; the
+                               * single best-ever timing is biased low). 0 = off; default 4.     */
 } wpk_tune_options;
 
 typedef struct wpk_plan_s *wpk_plan;
 
 /* Fill defaults (seed 0, rank 0, world 1, W=3, R=11, L2 flush, measured, GA 48/4/48/50/0.1/0.02,
- * PPO E=1 T=64 epochs 4 minibatch 16 gamma .99 mu .95 clip .2 c1 .15 c2 20 lr 1e-4 keep .85). */
+ * PPO E=1 T=64 epochs 4 minibatch 16 gamma .99 mu .95 clip .2 c1 .15 c2 20 lr 1e-4 keep .85,
+ * 4 finalists). Stop decisions (max_seconds, a fatal CUDA error on any rank) are collective:
+ * every rank leaves the search after the same exchange. */
 WPK_API void wpk_tune_options_init(wpk_tune_options *opts);
 
 /* Output spatial size (host only; no device needed). WPK_ERR_SHAPE if P or Q < 1. */
@@ -205,7 +213,10 @@ WPK_API wpk_status wpk_conv2d_set_config(wpk_plan plan, int32_t family, const in
 /* 1 if (family, genes) is valid for this plan, else 0 (and the reason in wpk_last_error). */
 WPK_API int32_t wpk_conv2d_config_valid(wpk_plan plan, int32_t family, const int32_t *genes);
 
-/* Drop the packed-weight / tensor-map caches (call after mutating weights in place). */
+/* Drop the packed-weight / tensor-map caches (call after mutating weights in place). The
+ * workspace holds persistent per-plan state (packed weights, self-resetting split-K counters):
+ * it belongs to ONE plan and may not be shared by plans whose runs can interleave; the state is
+ * re-derived whenever the workspace or the plan's config changes. */
 WPK_API wpk_status wpk_conv2d_invalidate(wpk_plan plan);
 
 /* Inference batch-norm folded into the convolution's weights and bias (constant folding; SURVEY.md

@@ -69,6 +69,7 @@ class TuneOptions(ctypes.Structure):
         ("max_seconds", ctypes.c_int32),
         ("seed_default", ctypes.c_int32),
         ("cache_dir", ctypes.c_char_p),
+        ("finalists", ctypes.c_int32),
     ]
 
 

@@ -118,6 +118,10 @@ class Conv2dPlan:
                 raise ValueError(f"{nm}: expected contiguous cuda {dt} of shape {tuple(shp)}, got {t.dtype} {tuple(t.shape)}")
         if y is None:
             y = torch.empty(self._ys, dtype=dt, device=x.device)
+        elif y.dtype is not dt or y.shape != self._ys or not y.is_cuda or not y.is_contiguous():
+            raise ValueError(f"y: expected contiguous cuda {dt} of shape {tuple(self._ys)}, got {y.dtype} {tuple(y.shape)}")
+        if b is not None and (b.dtype is not dt or b.shape != (self.k,) or not b.is_cuda or not b.is_contiguous()):
+            raise ValueError(f"b: expected contiguous cuda {dt} of shape ({self.k},), got {b.dtype} {tuple(b.shape)}")
         if self._ws_bytes < 0:
             self._ensure_workspace()
         s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
@@ -139,9 +143,21 @@ class Conv2dPlan:
                                         bp, ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(s)))
         return y
 
+    def _check_host(self, x_host, w, b, y_host):
+        dt = self._tdt
+        for t, nm, shp in ((x_host, "x_host", self._xs), (y_host, "y_host", self._ys)):
+            if t.dtype is not dt or t.shape != shp or t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{nm}: expected contiguous CPU {dt} of shape {tuple(shp)}, got "
+                                 f"{t.dtype} {tuple(t.shape)} on {t.device}")
+        if w.dtype is not dt or w.shape != self._wsh or not w.is_cuda or not w.is_contiguous():
+            raise ValueError(f"w: expected contiguous cuda {dt} of shape {tuple(self._wsh)}")
+        if b is not None and (b.dtype is not dt or b.shape != (self.k,) or not b.is_cuda or not b.is_contiguous()):
+            raise ValueError(f"b: expected contiguous cuda {dt} of shape ({self.k},)")
+
     def run_host(self, x_host: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, y_host: torch.Tensor,
                  stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         """x_host/y_host are (pinned) CPU tensors; H2D + conv + D2H inside, then stream sync."""
+        self._check_host(x_host, w, b, y_host)
         self._ensure_workspace()
         s = (stream or torch.cuda.current_stream(w.device)).cuda_stream
         bp = ctypes.c_void_p(b.data_ptr()) if b is not None else None
@@ -153,6 +169,7 @@ class Conv2dPlan:
     def run_host_async(self, x_host: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, y_host: torch.Tensor,
                        stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         """run_host without the final stream sync: y_host is valid after the stream is synchronised."""
+        self._check_host(x_host, w, b, y_host)
         self._ensure_workspace()
         s = (stream or torch.cuda.current_stream(w.device)).cuda_stream
         bp = ctypes.c_void_p(b.data_ptr()) if b is not None else None

@@ -223,7 +223,7 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
         const size_t rstride = (size_t)slice * 4 + 16;
         const size_t recv = (size_t)(g->splits - 1) * g->bm * rstride;
         // (one wave only: with one tile per CTA, later waves would pay the whole prologue again)
-        if (g->bn % (g->splits * cw) == 0 && recv <= (size_t)g->stages * stage && g->work <= device_sm_count(0)) {
+        if (g->bn % (g->splits * cw) == 0 && recv <= (size_t)g->stages * stage && g->work <= device_sm_count(d.device)) {
             g->csplit = 1;
             g->recv_stride = (int)rstride;
         }
@@ -388,6 +388,7 @@ void wpk_tune_options_init(wpk_tune_options *o) {
     o->rl_adv_norm = 1;
     o->rl_restart_every = 1;
     o->seed_default = 1;
+    o->finalists = 4;
 }
 
 wpk_status wpk_conv2d_output_dims(const wpk_conv2d_shape *shape, int32_t *p, int32_t *q) {
@@ -411,6 +412,7 @@ wpk_status wpk_conv2d_plan(const wpk_conv2d_shape *shape, wpk_dtype dtype, int d
     ConvDesc d;
     wpk_status st = to_desc(shape, (int)dtype, &d);
     if (st != WPK_OK) return st;
+    d.device = device;
     Plan *p = new (std::nothrow) Plan();
     if (!p) return fail(WPK_ERR_OUT_OF_MEMORY, "host allocation failed");
     p->d = d;
@@ -452,14 +454,13 @@ wpk_status wpk_conv2d_set_config(wpk_plan plan, int32_t family, const int32_t *g
     std::memcpy(c.genes, genes, sizeof c.genes);
     std::string why;
     if (!config_valid(p->d, c, &why)) return fail(WPK_ERR_INVALID_CONFIG, why);
-    if (!(c.family == p->cfg.family)) p->packed_for = nullptr;
-    p->cfg = c;
+    p->cfg = c;   // launch_conv re-keys the workspace state on the config
     return WPK_OK;
 }
 
 wpk_status wpk_conv2d_invalidate(wpk_plan plan) {
     if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
-    reinterpret_cast<Plan *>(plan)->packed_for = nullptr;
+    reinterpret_cast<Plan *>(plan)->reset_ws_state();
     return WPK_OK;
 }
 

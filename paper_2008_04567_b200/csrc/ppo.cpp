@@ -248,7 +248,7 @@ wpk_status rl_search(TuneCtx &t) {
     long long steps = 0;
     const double keep = o.rl_keep_prob > 0 ? o.rl_keep_prob : 1.0;
     const double consts[3] = {o.rl_c1, o.rl_c2, o.rl_clip};
-    while (!t.exhausted() && steps < max_steps && !t.time_up()) {
+    while (!t.exhausted() && steps < max_steps && !t.stop()) {
         // ---- rollout of T steps in each of the E environments ----
         std::vector<double> bobs, blogp, br, bv;
         std::vector<int32_t> bact;

@@ -437,6 +437,20 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     }
     int launches = 0;
     std::string err;
+    // the workspace's persistent state (packed weights, zeroed split-K counters) is only trusted
+    // for the workspace and config that produced it: another config (or another workspace) may
+    // have written its own layout over those bytes
+    if (p.state_ws != ws || !(p.packed_cfg == cfg)) {
+        p.packed_for = nullptr;
+        p.packed_cfg_family = -1;
+        p.packed_cfg = cfg;
+    }
+    if (p.state_ws != ws || !(p.counters_cfg == cfg)) {
+        p.counters_at = nullptr;
+        p.counters_bytes = 0;
+        p.counters_cfg = cfg;
+    }
+    p.state_ws = ws;
     if (cfg.family == WPK_FAMILY_SIMT) {
         const int *g = cfg.genes;
         SimtKernelFn fn = (d.dtype == WPK_BF16) ? simt_get_bf16(g[3], g[4], g[5], g[6])
@@ -629,7 +643,7 @@ static wpk_status ensure_ws(Plan *p, size_t need, char **ws, size_t *bytes) {
         if (p->ws_own) cudaFree(p->ws_own);
         p->ws_own = nullptr;
         p->ws_own_bytes = 0;
-        p->packed_for = nullptr;
+        p->reset_ws_state();
         if (need) {
             if (cudaMalloc(&p->ws_own, need) != cudaSuccess) {
                 cudaGetLastError();
@@ -672,7 +686,7 @@ wpk_status wpk_conv2d_set_workspace(wpk_plan plan, void *dev_ptr, size_t bytes) 
     size_t need = workspace_bytes(*p, p->cfg, false);
     if (dev_ptr && bytes < need)
         return fail(WPK_ERR_OUT_OF_MEMORY, "workspace too small: need " + std::to_string(need) + " bytes");
-    if (dev_ptr != p->ws_user) p->packed_for = nullptr;
+    if (dev_ptr != p->ws_user || bytes != p->ws_user_bytes) p->reset_ws_state();
     p->ws_user = static_cast<char *>(dev_ptr);
     p->ws_user_bytes = dev_ptr ? bytes : 0;
     return WPK_OK;

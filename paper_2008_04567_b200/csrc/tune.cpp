@@ -126,7 +126,7 @@ struct GpuBench {
             if (cudaMalloc(&ws, need) != cudaSuccess) { cudaGetLastError(); return INFINITY; }
             ws_bytes = need;
         }
-        p.packed_for = nullptr;
+        p.reset_ws_state();
         for (int i = 0; i < warmup; ++i)
             if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes, z) < 0) return INFINITY;
         if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
@@ -208,6 +208,12 @@ struct Rec {
 };
 static_assert(sizeof(Rec) == 16, "record layout");
 
+static int32_t config_hash(const Config &c) {
+    uint32_t h = 2166136261u ^ (uint32_t)c.family;
+    for (int g = 0; g < WPK_NUM_GENES; ++g) h = (h ^ (uint32_t)c.genes[g]) * 16777619u;
+    return (int32_t)(h & 0x7fffffff);
+}
+
 static double evaluate_one(TuneCtx &t, const Config &c, int32_t *status) {
     *status = 0;
     if (!t.valid(c)) { *status = 1; return INFINITY; }
@@ -245,36 +251,49 @@ std::vector<Config> TuneCtx::measure_batch(const std::vector<Config> &cfgs) {
     }
     int room = budget - (int)order.size();
     if ((int)fresh.size() > room) fresh.resize(std::max(room, 0));
+    // every rank computes the same `fresh` (replicated state), so all ranks exchange or none do
     if (fresh.empty() || err != WPK_OK) return {};
     const int n = (int)fresh.size(), world = std::max(1, o.world), rank = o.rank;
     const int per = (n + world - 1) / world;
-    std::vector<Rec> send(per), recv((size_t)per * world);
+    // per rank: `per` fitness records + one flags record {idx -2, status = bit0 time-up | bit1 fatal}
+    std::vector<Rec> send(per + 1), recv((size_t)(per + 1) * world);
     for (int i = 0; i < per; ++i) {
         int j = rank + i * world;
-        if (j < n) {
+        if (j < n && err == WPK_OK) {
             int32_t st;
             double b = evaluate_one(*this, fresh[j], &st);
             send[i] = Rec{j, st, b};
         } else {
-            send[i] = Rec{-1, 0, 0.0};
+            send[i] = Rec{j < n ? j : -1, j < n ? 3 : 0, INFINITY};   // after a fatal error: not measured
         }
     }
+    send[per] = Rec{-2, (time_up() ? 1 : 0) | (err != WPK_OK ? 2 : 0), 0.0};
     std::vector<double> beta(n, INFINITY);
     if (world > 1) {
-        if (!o.exchange || o.exchange(o.exchange_ctx, send.data(), per * sizeof(Rec), recv.data()) != 0) {
+        if (!o.exchange || o.exchange(o.exchange_ctx, send.data(), (per + 1) * sizeof(Rec), recv.data()) != 0) {
             err = WPK_ERR_INTERNAL;
             set_error("tune: exchange (all-gather of fitness records) failed");
             return {};
         }
+        int32_t flags = 0;
+        for (const Rec &r : recv)
+            if (r.idx == -2) flags |= r.status;
+        if (flags & 1) stop_all = true;
+        if ((flags & 2) && err == WPK_OK) {
+            err = WPK_ERR_CUDA;
+            set_error("tune: another rank hit a fatal CUDA error; all ranks stop");
+        }
+        if (err != WPK_OK) return {};
     } else {
         recv = send;
+        if (err != WPK_OK) return {};
     }
     for (const Rec &r : recv)
         if (r.idx >= 0 && r.idx < n) beta[r.idx] = r.beta;
     for (int j = 0; j < n; ++j) {
         memo[fresh[j]] = beta[j];
         order.push_back(fresh[j]);
-        if (rec && rank == 0 && o.eval_mode == WPK_EVAL_MEASURED) {
+        if (rec && o.eval_mode == WPK_EVAL_MEASURED) {   // the gathered table: identical on every rank
             fprintf(rec, "{\"family\": %d, \"genes\": %s, \"beta_us\": %s}\n", fresh[j].family,
                     genes_json(fresh[j]).c_str(), dbl(beta[j]).c_str());
         }
@@ -354,7 +373,7 @@ static wpk_status ga_search(TuneCtx &t) {
             log_line(t, s);
         }
         // Step4: runtimes close enough, budget, generation cap
-        if (spread < o.ga_eps || t.exhausted() || gen + 1 >= o.ga_max_gen || pop.empty() || nf == 0 || t.time_up())
+        if (spread < o.ga_eps || t.exhausted() || gen + 1 >= o.ga_max_gen || pop.empty() || nf == 0 || t.stop())
             break;
         // Step3
         Rng r(o.seed, (uint64_t)gen + 1);
@@ -407,7 +426,7 @@ static wpk_status random_search(TuneCtx &t) {
     if (t.o.seed_default && t.has_default) t.measure_batch({t.default_cfg});
     const long long limit = 100LL * std::max(t.budget, 1);
     const int batch = std::max(1, t.o.ga_pop);
-    while (!t.exhausted() && draws < limit && !t.time_up()) {
+    while (!t.exhausted() && draws < limit && !t.stop()) {
         std::vector<Config> b;
         const int room = t.budget - (int)t.order.size();
         while ((int)b.size() < std::min(batch, room) && draws < limit) {
@@ -507,10 +526,19 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
     if (t.o.cache_dir && t.o.cache_dir[0]) {
         cpath = std::string(t.o.cache_dir) + "/" + cache_key(*p, t.family, t.o.eval_mode == WPK_EVAL_MEASURED) + ".json";
         Config hit;
-        double hb;
-        if (cache_lookup(cpath, budget, &hit, &hb) && config_valid(p->d, hit, nullptr)) {
+        double hb = 0;
+        bool use = cache_lookup(cpath, budget, &hit, &hb) && config_valid(p->d, hit, nullptr);
+        if (t.o.world > 1) {   // collective: a hit counts only if every rank read the same record
+            Rec mine{use ? 1 : 0, use ? config_hash(hit) : 0, use ? hb : 0.0};
+            std::vector<Rec> all(t.o.world);
+            if (t.o.exchange(t.o.exchange_ctx, &mine, sizeof(Rec), all.data()) != 0)
+                return fail(WPK_ERR_INTERNAL, "tune: cache-decision exchange failed");
+            for (const Rec &r : all)
+                if (r.idx != 1 || r.status != mine.status || r.beta != mine.beta) use = false;
+        }
+        if (use) {
             p->cfg = hit;
-            p->packed_for = nullptr;
+            p->reset_ws_state();
             p->best_us = hb;
             p->measured = 0;
             p->rounds = 0;
@@ -527,16 +555,63 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
         if (!gb.init(*p)) return fail(WPK_ERR_CUDA, "tune: " + gb.err);
         t.gb = &gb;
     }
-    if (t.o.record_path && t.o.rank == 0) t.rec = fopen(t.o.record_path, "a");
+    if (t.o.record_path) t.rec = fopen(t.o.record_path, "a");   // per-rank path (caller's choice)
     if (t.o.log_path && t.o.rank == 0) t.log = fopen(t.o.log_path, "w");
     wpk_status st;
     if (search == WPK_SEARCH_GA) st = ga_search(t);
     else if (search == WPK_SEARCH_RANDOM) st = random_search(t);
     else st = rl_search(t);
-    if (t.rec) fclose(t.rec);
-    if (t.log) fclose(t.log);
+    struct Closer {   // history files stay open through the finalist re-timing
+        TuneCtx &t;
+        ~Closer() {
+            if (t.rec) fclose(t.rec);
+            if (t.log) fclose(t.log);
+        }
+    } closer{t};
     if (st != WPK_OK) return st;
     if (!t.have_best || !std::isfinite(t.best_beta)) return fail(WPK_ERR_EXHAUSTED, "every candidate failed");
+    // Finalists (SURVEY.md 8(d) protocol item 2): the top-k measured configs are re-timed on every
+    // rank and the lowest median across ranks wins. Deterministic given the gathered table: every
+    // rank holds the same memo, ranks the same finalists and sees the same all-gathered timings.
+    if (t.o.eval_mode == WPK_EVAL_MEASURED && t.o.finalists > 0 && t.order.size() > 1) {
+        std::vector<int> idx(t.order.size());
+        std::iota(idx.begin(), idx.end(), 0);
+        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return t.memo[t.order[a]] < t.memo[t.order[b]]; });
+        std::vector<Config> fin;
+        for (int i : idx)
+            if ((int)fin.size() < t.o.finalists && std::isfinite(t.memo[t.order[i]])) fin.push_back(t.order[i]);
+        const int k = (int)fin.size(), world = std::max(1, t.o.world);
+        std::vector<Rec> mine(k), all((size_t)k * world);
+        for (int i = 0; i < k; ++i) {
+            bool fatal = false;
+            double b = (t.err == WPK_OK) ? gb.measure(*p, fin[i], t.o.warmup, t.o.reps, t.o.l2_flush != 0, &fatal) : INFINITY;
+            if (fatal && t.err == WPK_OK) { t.err = WPK_ERR_CUDA; set_error("tune: " + gb.err); }
+            mine[i] = Rec{i, (fatal || t.err != WPK_OK) ? 3 : 0, b};
+        }
+        if (world > 1) {
+            if (t.o.exchange(t.o.exchange_ctx, mine.data(), k * sizeof(Rec), all.data()) != 0)
+                return fail(WPK_ERR_INTERNAL, "tune: finalist exchange failed");
+        } else {
+            all = mine;
+        }
+        for (const Rec &r : all)
+            if (r.status == 3) return fail(WPK_ERR_CUDA, "tune: a rank failed while re-timing the finalists");
+        int besti = -1;
+        double bestm = INFINITY;
+        for (int i = 0; i < k; ++i) {
+            std::vector<double> v;
+            for (int r = 0; r < world; ++r) v.push_back(all[(size_t)r * k + i].beta);
+            std::sort(v.begin(), v.end());
+            const double med = (v.size() & 1) ? v[v.size() / 2] : 0.5 * (v[v.size() / 2 - 1] + v[v.size() / 2]);
+            log_line(t, "{\"finalist\": " + std::to_string(i) + ", \"genes\": " + genes_json(fin[i]) +
+                            ", \"search_beta\": " + dbl(t.memo[fin[i]]) + ", \"median_beta\": " + dbl(med) + "}");
+            if (med < bestm) { bestm = med; besti = i; }   // ties keep the better search-time rank
+        }
+        if (besti >= 0) {
+            t.best = fin[besti];
+            t.best_beta = bestm;
+        }
+    }
     // every rank must have chosen the same config (replicated deterministic searcher state)
     if (t.o.world > 1) {
         Rec mine{t.best.family, 0, t.best_beta};
@@ -551,7 +626,7 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
                 return fail(WPK_ERR_INTERNAL, "tune: ranks disagree on the chosen config");
     }
     p->cfg = t.best;
-    p->packed_for = nullptr;
+    p->reset_ws_state();   // the tuning workspace is gone; the plan's own starts from scratch
     p->best_us = t.best_beta;
     if (!cpath.empty() && t.o.rank == 0) cache_store(cpath, t.best, t.best_beta, budget, (int)search);
     p->measured = (int)t.order.size();

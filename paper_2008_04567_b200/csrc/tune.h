@@ -38,6 +38,11 @@ struct TuneCtx {
     bool exhausted() const { return (int)order.size() >= budget; }
     bool valid(const Config &c) const { return config_valid(plan->d, c, nullptr); }
     bool time_up() const;
+    // Stop decisions are collective: with world > 1 every exchange also carries each rank's
+    // (time-up, fatal-error) flags, OR-reduced, so all ranks leave the search at the same step and
+    // never enter an all-gather that another rank skips. stop() is the searchers' check.
+    bool stop_all = false;
+    bool stop() const { return o.world > 1 ? stop_all : time_up(); }
     // Measure the new distinct configs of `cfgs` (first-occurrence order, truncated to the
     // remaining budget), sharded over ranks; returns the configs measured. Updates memo/best.
     std::vector<Config> measure_batch(const std::vector<Config> &cfgs);

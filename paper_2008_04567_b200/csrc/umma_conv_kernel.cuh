@@ -28,6 +28,8 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
+
+#include <atomic>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -1050,8 +1052,13 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
 template <int DT, int AK, int EK, bool RES = false>
 static cudaError_t launch_variant(cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                                   const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
-    static bool attr_done = false;
-    if (!attr_done) {
+    // the shared-memory opt-in is per device context: remember it per device (bit d), so a plan
+    // on a second device of the same process sets it again; racing host threads at worst set it twice
+    static std::atomic<unsigned long long> attr_done{0ull};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
         cudaError_t e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return e;
@@ -1063,7 +1070,7 @@ static cudaError_t launch_variant(cudaLaunchConfig_t &lc, const CUtensorMap &tmA
                                      (int)cudaSharedmemCarveoutMaxShared);
             if (e != cudaSuccess) return e;
         }
-        attr_done = true;
+        attr_done.fetch_or(bit, std::memory_order_acq_rel);
     }
     return cudaLaunchKernelEx(&lc, umma_conv_kernel<DT, AK, EK, RES>, tmA, tmB, tmY, tmP, a);
 }

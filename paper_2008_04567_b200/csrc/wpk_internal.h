@@ -22,6 +22,7 @@ struct ConvDesc {
     int layout, epilogue;
     int p, q;          // output spatial size
     int dtype;         // wpk_dtype
+    int device = 0;    // CUDA device of the plan (SM count for one-wave checks)
     long long M() const { return (long long)n * p * q; }
     long long flops() const { return 2LL * n * k * p * q * (c / g) * r * s; }
     int elem() const { return (dtype == WPK_BF16 || dtype == WPK_F16) ? 2 : 4; }
@@ -106,9 +107,14 @@ struct Plan {
     size_t ws_user_bytes = 0;
     char *ws_own = nullptr;
     size_t ws_own_bytes = 0;
-    // packed weights cache
+    // Persistent per-plan state in the workspace (the workspace belongs to ONE plan): the packed
+    // weights and the zeroed split-K counters. Both are keyed by (workspace base, config) as well
+    // as by the weight pointer / counter address; reset_ws_state() forgets them whenever the
+    // workspace changes or another config has run over it.
     const void *packed_for = nullptr;
     int packed_cfg_family = -1;
+    Config packed_cfg;
+    const char *state_ws = nullptr;   // workspace base the state below refers to
     int last_launches = 0;
     void *map_cache = nullptr;   // UmmaMapCache (umma_conv.h)
     unsigned long long *dbg = nullptr;   // per-plan kernel timeline (tools only; overrides the global)
@@ -119,6 +125,14 @@ struct Plan {
     bool geom_ok = false;
     char *counters_at = nullptr; // split-K counters known to be zero at this address
     size_t counters_bytes = 0;
+    Config counters_cfg;
+    void reset_ws_state() {
+        packed_for = nullptr;
+        packed_cfg_family = -1;
+        counters_at = nullptr;
+        counters_bytes = 0;
+        state_ws = nullptr;
+    }
     // tune stats
     double best_us = 0, tune_seconds = 0;
     int measured = 0, rounds = 0;

@@ -3,11 +3,13 @@ kernel and a third-party implementation -- here the same box's cuDNN reached thr
 (BASELINE.json north_star). Ties go to the own kernel (reading c25).
 
 The timing protocol is the one the tuner uses: W warm-ups, then R CUDA-event-timed
-reps with an L2 flush before each, median. The C library never sees torch; this module only
-records which implementation a layer should dispatch to.
+reps with an L2 flush before each, median. The C library never sees torch: the choice lives here,
+in SelectedConv2d, which persists it next to the tuning cache and dispatches each call to it.
 """
 from __future__ import annotations
 
+import json
+import os
 import statistics
 from dataclasses import dataclass
 
@@ -51,22 +53,44 @@ def time_fn(fn, warmup: int = 3, reps: int = 11, flush: bool = True, stream=None
     return statistics.median(ts)
 
 
-def cudnn_conv_fn(x, w, b, stride, pad, dil, groups, layout, dtype, fused: bool):
-    """cuDNN competitor: NHWC tensors are passed as channels_last views (no copies)."""
+def cudnn_conv_fn(x, w, b, stride, pad, dil, groups, layout, dtype, fused: bool, z=None, epilogue="bias_relu"):
+    """cuDNN competitor: NHWC tensors are passed as channels_last views (no copies). The returned
+    callable gives the output in the caller's layout (an NHWC view of cuDNN's channels_last result).
+    epilogue: "bias_relu" (default), "bias", "none", or "bias_add_relu" with the residual z."""
     torch.backends.cudnn.benchmark = True
     torch.backends.cudnn.allow_tf32 = (dtype == "tf32")
     torch.backends.cuda.matmul.allow_tf32 = (dtype == "tf32")
-    if layout == "nhwc":
+    nhwc = layout == "nhwc"
+    if nhwc:
         xt = x.permute(0, 3, 1, 2)             # logical NCHW view of channels_last memory
         wt = w.permute(0, 3, 1, 2)
+        zt = z.permute(0, 3, 1, 2) if z is not None else None
     else:
-        xt, wt = x, w
-    if fused and b is not None and hasattr(torch, "cudnn_convolution_relu"):
-        def f():
-            return torch.cudnn_convolution_relu(xt, wt, b, (stride, stride), (pad, pad), (dil, dil), groups)
+        xt, wt, zt = x, w, z
+    st, pd, dl = (stride, stride), (pad, pad), (dil, dil)
+    if epilogue == "bias_add_relu":
+        if fused and hasattr(torch, "cudnn_convolution_add_relu"):
+            def g():
+                return torch.cudnn_convolution_add_relu(xt, wt, zt, 1.0, b, st, pd, dl, groups)
+        else:
+            def g():
+                return F.relu_(F.conv2d(xt, wt, b, stride, pad, dil, groups).add_(zt))
+    elif epilogue in ("bias", "none"):
+        bb = b if epilogue == "bias" else None
+
+        def g():
+            return F.conv2d(xt, wt, bb, stride, pad, dil, groups)
+    elif fused and b is not None and hasattr(torch, "cudnn_convolution_relu"):
+        def g():
+            return torch.cudnn_convolution_relu(xt, wt, b, st, pd, dl, groups)
     else:
-        def f():
+        def g():
             return F.relu_(F.conv2d(xt, wt, b, stride, pad, dil, groups))
+    if not nhwc:
+        return g
+
+    def f():
+        return g().permute(0, 2, 3, 1)           # NHWC view (channels_last memory: no copy)
     return f
 
 
@@ -78,18 +102,109 @@ class Selection:
     choice: str          # "wpk" or "cudnn"
 
 
-def select(plan, x, w, b, y, stride, pad, dil, groups, warmup=3, reps=11) -> Selection:
+_VARIANT_NAMES = {("bias_relu", True): "cudnn_convolution_relu", ("bias_relu", False): "conv2d+relu_",
+                  ("bias_add_relu", True): "cudnn_convolution_add_relu", ("bias_add_relu", False): "conv2d+add_+relu_",
+                  ("bias", True): "conv2d", ("bias", False): "conv2d", ("none", True): "conv2d",
+                  ("none", False): "conv2d"}
+
+
+def select(plan, x, w, b, y, stride, pad, dil, groups, warmup=3, reps=11, z=None) -> Selection:
     """Time the plan's current config and both cuDNN variants; pick the argmin (ties -> wpk)."""
-    own = time_fn(lambda: plan.run(x, w, b, y), warmup, reps)
+    own = time_fn(lambda: plan.run(x, w, b, y, z=z), warmup, reps)
     best, variant = float("inf"), "none"
     for fused in (False, True):
         try:
-            f = cudnn_conv_fn(x, w, b, stride, pad, dil, groups, plan.layout, plan.dtype, fused)
+            f = cudnn_conv_fn(x, w, b, stride, pad, dil, groups, plan.layout, plan.dtype, fused, z=z,
+                              epilogue=plan.epilogue)
             f()
             t = time_fn(f, warmup, reps)
         except (RuntimeError, TypeError):
             continue
         if t < best:
-            best, variant = t, ("cudnn_convolution_relu" if fused else "conv2d+relu_")
+            best, variant = t, _VARIANT_NAMES[(plan.epilogue, fused)]
     choice = "wpk" if own <= best else "cudnn"
     return Selection(own, best, variant, choice)
+
+
+def _device_tag(device) -> str:
+    p = torch.cuda.get_device_properties(device)
+    return "".join(ch if ch.isalnum() else "_" for ch in f"{p.name}_sm{p.multi_processor_count}")
+
+
+class SelectedConv2d:
+    """One convolution of the optimized inference plan (§2.5: "If the third-party
+    implementation is superior, we will use this ... implementation in our optimized inference
+    plan"): a tuned WPK plan plus the system-level choice between it and the box's cuDNN, made by
+    `select` (same protocol as the tuner, ties -> WPK) and persisted next to the tuning cache.
+
+    __call__ dispatches: "wpk" runs the plan (libwpk.so kernels, into y if given); "cudnn" runs the
+    chosen cuDNN variant through torch and returns its own output tensor in the plan's layout (an
+    NHWC view of channels_last memory for NHWC plans; y is not written)."""
+
+    def __init__(self, plan, stride=1, pad=0, dil=1, cache_dir: str | None = None):
+        self.plan, self.stride, self.pad, self.dil = plan, stride, pad, dil
+        self.groups = plan.groups
+        self.cache_dir = cache_dir
+        self.choice = "wpk"          # until a selection is made or loaded
+        self.variant = None
+        self.selection: Selection | None = None
+        self._fns = {}
+
+    # -- persistence -----------------------------------------------------------------------------
+    def key(self) -> str:
+        pl = self.plan
+        return (f"sel_n{pl.n}_c{pl.c}_h{pl.h}_w{pl.w}_k{pl.k}_r{pl.r}_s{pl.s}_st{self.stride}_p{self.pad}"
+                f"_d{self.dil}_g{pl.groups}_{pl.layout}_{pl.epilogue}_{pl.dtype}_{_device_tag(pl.device)}")
+
+    def _path(self):
+        return os.path.join(self.cache_dir, self.key() + ".json") if self.cache_dir else None
+
+    def save(self):
+        path = self._path()
+        if path is None or self.selection is None:
+            return
+        os.makedirs(self.cache_dir, exist_ok=True)
+        fam, genes = self.plan.config
+        rec = {"choice": self.choice, "cudnn_variant": self.variant, "own_us": self.selection.own_us,
+               "cudnn_us": self.selection.cudnn_us, "family": fam, "genes": genes}
+        tmp = f"{path}.tmp{os.getpid()}"
+        with open(tmp, "w") as f:
+            json.dump(rec, f)
+        os.replace(tmp, path)
+
+    def load(self) -> bool:
+        """Adopt a persisted choice if it was made for the plan's current config."""
+        path = self._path()
+        if path is None or not os.path.exists(path):
+            return False
+        rec = json.load(open(path))
+        fam, genes = self.plan.config
+        if rec.get("family") != fam or list(rec.get("genes", [])) != list(genes):
+            return False
+        self.choice, self.variant = rec["choice"], rec.get("cudnn_variant")
+        self.selection = Selection(rec["own_us"], rec["cudnn_us"], self.variant or "none", self.choice)
+        return True
+
+    # -- selection and dispatch ------------------------------------------------------------------
+    def select(self, x, w, b, y=None, z=None, warmup=3, reps=11) -> Selection:
+        if y is None:
+            y = torch.empty(self.plan.y_shape(), dtype=x.dtype, device=x.device)
+        sel = select(self.plan, x, w, b, y, self.stride, self.pad, self.dil, self.groups, warmup, reps, z=z)
+        self.selection, self.choice, self.variant = sel, sel.choice, sel.cudnn_variant
+        self.save()
+        return sel
+
+    def __call__(self, x, w, b, y=None, z=None, stream=None):
+        if self.choice == "wpk":
+            return self.plan.run(x, w, b, y, stream=stream, z=z)
+        key = (x.data_ptr(), w.data_ptr(), None if b is None else b.data_ptr(), None if z is None else z.data_ptr())
+        f = self._fns.get(key)
+        if f is None:
+            fused = self.variant in ("cudnn_convolution_relu", "cudnn_convolution_add_relu")
+            f = cudnn_conv_fn(x, w, b, self.stride, self.pad, self.dil, self.groups, self.plan.layout,
+                              self.plan.dtype, fused, z=z, epilogue=self.plan.epilogue)
+            self._fns[key] = f
+        if stream is not None:
+            with torch.cuda.stream(stream):
+                return f()
+        return f()

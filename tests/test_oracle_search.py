@@ -230,3 +230,123 @@ def test_ga_beats_random():
         rnd = S.random_run(DOMAINS, valid, f, seed=seed, budget=512)
         wins += ga.best_beta <= rnd.best_beta
     assert wins >= 18
+
+
+# --- pins added in round 2 for the functions that had only self-consistency checks ----------------
+def test_observation_hand_vector():
+    """O_conv entry order of PAPER.md:89-93: (N, C_in, C_out, K_h, K_w, H, W, Stride, Padding,
+    T_x, T_y, T_z, Tile_x, Tile_y, Tile_z, Tile_rz, alpha_t), with the log2(1+v) feature scaling of
+    DESIGN.md reading c24b. Every size entry is 2^j - 1 with a different j, so log2(1+v) = j is
+    exact and a swapped pair (C_in/C_out, H/W, K_h/K_w, a gene pair) changes the vector."""
+    shape9 = (1, 3, 7, 15, 31, 63, 127, 255, 1)          # padding 1 = SAME
+    genes = (0, 1, 3, 7, 15, 31, 63)
+    o = S.observation(shape9, genes, 511.0)
+    want = [1, 2, 3, 4, 5, 6, 7, 8, 1, 0, 1, 2, 3, 4, 5, 6, 9]   # written out by hand
+    assert o.shape == (17,)
+    assert o.tolist() == [float(v) for v in want]
+    assert S.observation(shape9[:8] + (0,), genes, 0.0)[8] == 0.0 and S.observation(shape9, genes, 0.0)[16] == 0.0
+
+
+# SELU constants (Klambauer et al. 2017), written out: lambda, alpha and lambda*alpha
+SELU_LAMBDA = 1.0507009873554804934
+SELU_ALPHA = 1.6732632423543772848
+SELU_LAMBDA_ALPHA = 1.7580993408473768599
+
+
+def test_selu_constants():
+    assert float(S.selu(np.array(1.0))) == pytest.approx(SELU_LAMBDA, rel=1e-15)
+    assert float(S.selu(np.array(-50.0))) == pytest.approx(-SELU_LAMBDA_ALPHA, rel=1e-15)
+    assert float(S.selu(np.array(math.log(0.5)))) == pytest.approx(-SELU_LAMBDA_ALPHA / 2, rel=1e-14)
+    assert SELU_LAMBDA * SELU_ALPHA == pytest.approx(SELU_LAMBDA_ALPHA, rel=1e-15)
+
+
+def test_mlp_forward_hand_network():
+    """A 1-unit-per-layer network whose pre-activations are chosen so each activation has a closed
+    form: tanh(atanh 0.5) = 0.5, tanh(atanh 0.6) = 0.6, selu(1) = lambda, selu(ln 0.5) = -lambda*alpha/2,
+    then the linear head. The order tanh, tanh, selu, selu of PAPER.md:99 is what produces these
+    numbers (any other order gives e.g. selu(atanh 0.5) = 0.577 in layer 1)."""
+    z1 = 0.54930614433405484570        # atanh(0.5)
+    z2 = 0.69314718055994530942        # atanh(0.6) = ln 2
+    params = [
+        (np.array([[2 * z1]]), np.array([0.0])),                    # obs 0.5 -> z1
+        (np.array([[2 * z2]]), np.array([0.0])),                    # h1 0.5  -> z2
+        (np.array([[0.0]]), np.array([1.0])),                       # -> z3 = 1
+        (np.array([[0.0]]), np.array([math.log(0.5)])),            # -> z4 = ln 0.5
+        (np.array([[2.0], [-1.0]]), np.array([0.25, 0.0])),        # linear head, A = 1 logit + value
+    ]
+    out, cache = S.mlp_forward(params, np.array([[0.5]]))
+    h = [float(v[0, 0]) for v in cache["h"][1:]]
+    assert h[0] == pytest.approx(0.5, abs=1e-15)
+    assert h[1] == pytest.approx(0.6, abs=1e-15)
+    assert h[2] == pytest.approx(SELU_LAMBDA, abs=1e-15)
+    assert h[3] == pytest.approx(-SELU_LAMBDA_ALPHA / 2, abs=1e-15)
+    np.testing.assert_allclose(out[0], [0.25 - SELU_LAMBDA_ALPHA, SELU_LAMBDA_ALPHA / 2], rtol=0, atol=1e-15)
+    # inverted dropout after the 4th hidden layer: a dropped unit zeroes the head's input
+    out0, _ = S.mlp_forward(params, np.array([[0.5]]), mask=np.array([[0.0]]), keep=0.85)
+    np.testing.assert_allclose(out0[0], [0.25, 0.0], atol=0)
+    out1, _ = S.mlp_forward(params, np.array([[0.5]]), mask=np.array([[1.0]]), keep=0.5)
+    np.testing.assert_allclose(out1[0], [0.25 - 2 * SELU_LAMBDA_ALPHA, SELU_LAMBDA_ALPHA], atol=1e-14)
+
+
+def _const_head(A, V):
+    """A network whose output ignores the input: logits all 0 (uniform policy), value V."""
+    dims = [1, 1, 1, 1, 1]
+    ps = [(np.zeros((dims[i + 1], dims[i])), np.zeros(dims[i + 1])) for i in range(4)]
+    ps.append((np.zeros((A + 1, 1)), np.array([0.0] * A + [V])))
+    return ps
+
+
+def test_ppo_objective_hand_values():
+    """L = mean[L^clip - c1 L^VF + c2 S] with the paper's c1 = 0.15, c2 = 20,
+    L^VF = (V - (A + V_old))^2 (reading c20), on a uniform 2-action policy (S = ln 2) and value 1.
+    Values worked by hand:
+      ratio 1 (old logp = ln 1/2): L^clip = adv = (0.5, -0.5); V^target = (0.5, 0.5) -> L^VF = 0.25
+        L = 0 - 0.15*0.25 + 20 ln 2 = 13.825443611198906
+      ratio 2 (old logp = ln 1/4), clip 0.2: L^clip = (min(1.0, 0.6), min(-1.0, -0.6)) = (0.6, -1.0)
+        L = -0.2 - 0.0375 + 20 ln 2 = 13.625443611198906"""
+    params = _const_head(2, 1.0)
+    obs = np.zeros((2, 1))
+    acts = np.array([0, 1])
+    adv = np.array([0.5, -0.5])
+    v_old = np.array([0.0, 1.0])
+    c = S.PPOConsts()
+    assert (c.c1, c.c2) == (0.15, 20.0)
+    L, parts = S.ppo_objective(params, obs, acts, np.log([0.5, 0.5]), adv, v_old, c)
+    np.testing.assert_allclose(parts["ent"], [math.log(2)] * 2, rtol=1e-15)
+    np.testing.assert_allclose(parts["lvf"], [0.25, 0.25], rtol=1e-15)
+    assert L == pytest.approx(13.825443611198906, abs=1e-12)
+    L2, parts2 = S.ppo_objective(params, obs, acts, np.log([0.25, 0.25]), adv, v_old, c)
+    np.testing.assert_allclose(parts2["lclip"], [0.6, -1.0], rtol=1e-14)
+    assert L2 == pytest.approx(13.625443611198906, abs=1e-12)
+    # the value term alone: c2 = 0, V = 3, targets 0.5 -> L = mean(adv) - c1 * 6.25
+    L3, _ = S.ppo_objective(_const_head(2, 3.0), obs, acts, np.log([0.5, 0.5]), adv, v_old,
+                            S.PPOConsts(c1=0.15, c2=0.0))
+    assert L3 == pytest.approx(-0.15 * 6.25, abs=1e-14)
+
+
+def test_random_run_hand_enumerated_space():
+    """Random search: uniform valid samples, best-ever. On a 3-gene space with one
+    invalid corner, enumerated by hand: {1,2}^3 minus (2,2,2) = 7 valid configs."""
+    doms = [[1, 2], [1, 2], [1, 2]]
+    ok = lambda c: c[0] * c[1] * c[2] <= 4
+    space = [(1, 1, 1), (1, 1, 2), (1, 2, 1), (1, 2, 2), (2, 1, 1), (2, 1, 2), (2, 2, 1)]
+    assert sorted(S.enumerate_space(doms, ok)) == space
+    cost = {c: 10.0 + i for i, c in enumerate([(2, 1, 2), (1, 1, 1), (2, 2, 1), (1, 2, 2),
+                                                 (1, 1, 2), (2, 1, 1), (1, 2, 1)])}
+    f = lambda c: cost[c]
+    # budget >= |space|: every valid config measured once, never the invalid one, exact optimum
+    for seed in range(5):
+        res = S.random_run(doms, ok, f, seed=seed, budget=10)
+        assert sorted(res.measured) == space
+        assert res.best == (2, 1, 2) and res.best_beta == 10.0
+    # budget 3: three distinct valid configs, best = min of those measured
+    for seed in range(20):
+        res = S.random_run(doms, ok, f, seed=seed, budget=3)
+        assert len(res.measured) == 3 == len(set(res.measured))
+        assert all(c in space for c in res.measured)
+        assert res.best_beta == min(cost[c] for c in res.measured)
+    # uniform over the valid configs: the first measured config of 7000 seeds, 3-sigma per cell
+    first = [S.random_run(doms, ok, f, seed=s, budget=1).measured[0] for s in range(7000)]
+    cnt = [first.count(c) for c in space]
+    sig = math.sqrt(7000 * (1 / 7) * (6 / 7))
+    assert all(abs(n - 1000) < 3.5 * sig for n in cnt), cnt

@@ -331,38 +331,13 @@ def test_segment_gather_small_c(dtype, layout):
 @pytest.mark.parametrize("layer", workloads.resnet50(32), ids=lambda l: l.name)
 def test_resnet50_n32_sampled_bf16(layer):
     """Full-size bench layers (BASELINE.json configs[1], N=32 bf16 NHWC, default config): sampled
-    outputs (all borders of image 0 / first channels + 4096 random points) vs the oracle."""
+    outputs (every border pixel of every image x all channels + 65,536 interior points) vs the oracle."""
     x, w, b = workloads.generate(layer, "bf16", "int", seed=workloads.config_seed(1, 0))
     y, plan = run_product(layer, "bf16", "nhwc", x, w, b)
-    pts = workloads.random_points(layer, plan.p, plan.q, 4096, seed=1).numpy()
-    ref = oracle.conv2d_points(x, w, b, pts, stride=layer.stride, pad=layer.pad, nthreads=8)
+    pts = workloads.parity_points(layer, plan.p, plan.q, 65536, seed=1).numpy()
+    ref = oracle.conv2d_points(x, w, b, pts, stride=layer.stride, pad=layer.pad, nthreads=os.cpu_count() or 8)
     got = y[pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
-    want = torch.from_numpy(ref).to(torch.bfloat16)
-    assert torch.equal(got.float() + 0, want.float() + 0)
-
-
-_TUNED = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r1k_tuned_configs.json")
-
-
-@pytest.mark.parametrize("layer", workloads.resnet50(32), ids=lambda l: l.name)
-def test_resnet50_n32_bench_configs_sampled(layer):
-    """The configs the bench tuned (profiles/r1k_tuned_configs.json, committed): full-size layer,
-    uniform inputs, sampled outputs vs the oracle within the bf16 tolerance; plus exact-integer
-    inputs bit-exact on the same samples."""
-    import json
-    cfgs = json.load(open(_TUNED))
-    fam, genes = cfgs[layer.name]
-    for mode in ("int", "uniform"):
-        x, w, b = workloads.generate(layer, "bf16", mode, seed=workloads.config_seed(1, 1))
-        y, plan = run_product(layer, "bf16", "nhwc", x, w, b, config=(fam, genes))
-        pts = workloads.random_points(layer, plan.p, plan.q, 4096, seed=2).numpy()
-        ref = oracle.conv2d_points(x, w, b, pts, stride=layer.stride, pad=layer.pad, nthreads=8)
-        got = y[pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]]
-        if mode == "int":
-            assert torch.equal(got.float() + 0, torch.from_numpy(ref).to(torch.bfloat16).float() + 0)
-        else:
-            err = np.linalg.norm(got.double().numpy() - ref) / max(np.linalg.norm(ref), 1e-30)
-            assert err <= TOL["bf16"], err
+    assert_bit_exact(got, ref)
 
 
 _TUNED_F32 = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r1e_suite_f32.json")

@@ -232,3 +232,38 @@ def random_points(layer: ConvLayer, p: int, q: int, count: int, seed: int):
     qq = torch.randint(0, q, (count,), generator=g)
     pts += list(zip(n.tolist(), k.tolist(), pp.tolist(), qq.tolist()))
     return torch.tensor(pts, dtype=torch.int64)
+
+
+def parity_points(layer: ConvLayer, p: int, q: int, interior: int = 65536, seed: int = 0,
+                  border_channels: int | None = None):
+    """Seeded full-size parity sample of output coordinates (n, k, p, q) ("all
+    border rows/columns + >= 65,536 random interior outputs per layer"): every border pixel
+    (p in {0, P-1} or q in {0, Q-1}) of EVERY image, for every output channel (or, with
+    border_channels=c, for c channels per pixel rotating through all K), plus `interior` uniform
+    draws from the non-border pixels (all pixels when P or Q <= 2). Returns an int64 [count, 4]."""
+    g = torch.Generator().manual_seed(int(seed) + 4567)
+    pp, qq = torch.meshgrid(torch.arange(p), torch.arange(q), indexing="ij")
+    border = (pp == 0) | (pp == p - 1) | (qq == 0) | (qq == q - 1)
+    bp, bq = pp[border], qq[border]                       # [nb]
+    nb = bp.numel()
+    if border_channels is None or border_channels >= layer.k:
+        ks = torch.arange(layer.k)
+        n_idx = torch.arange(layer.n).view(-1, 1, 1).expand(layer.n, nb, layer.k)
+        k_idx = ks.view(1, 1, -1).expand(layer.n, nb, layer.k)
+        p_idx = bp.view(1, -1, 1).expand(layer.n, nb, layer.k)
+        q_idx = bq.view(1, -1, 1).expand(layer.n, nb, layer.k)
+    else:
+        c = border_channels
+        n_idx = torch.arange(layer.n).view(-1, 1, 1).expand(layer.n, nb, c)
+        off = (torch.arange(layer.n).view(-1, 1, 1) * nb + torch.arange(nb).view(1, -1, 1)) * c
+        k_idx = (off + torch.arange(c).view(1, 1, -1)) % layer.k
+        p_idx = bp.view(1, -1, 1).expand(layer.n, nb, c)
+        q_idx = bq.view(1, -1, 1).expand(layer.n, nb, c)
+    bpts = torch.stack([n_idx.reshape(-1), k_idx.reshape(-1), p_idx.reshape(-1), q_idx.reshape(-1)], 1)
+    inner = ~border if (p > 2 and q > 2) else torch.ones_like(border)
+    ip, iq = pp[inner], qq[inner]
+    sel = torch.randint(0, ip.numel(), (interior,), generator=g)
+    n = torch.randint(0, layer.n, (interior,), generator=g)
+    k = torch.randint(0, layer.k, (interior,), generator=g)
+    ipts = torch.stack([n, k, ip[sel], iq[sel]], 1)
+    return torch.cat([bpts, ipts]).to(torch.int64)
