@@ -442,9 +442,9 @@ def main():
     ap.add_argument("--no-cudnn", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-points", type=int, default=1024)
-    ap.add_argument("--cpu-interior-points", type=int, default=65536,
+    ap.add_argument("--cpu-interior-points", type=int, default=262144,
                     help="interior oracle outputs per unique layer for cpu_baseline / parity")
-    ap.add_argument("--cpu-border-channels", type=int, default=2,
+    ap.add_argument("--cpu-border-channels", type=int, default=8,
                     help="channels per border pixel (rotating over K) in the cpu_baseline / parity sample")
     ap.add_argument("--layers-json", default=None, help="also write the full line + per-layer table here")
     ap.add_argument("--trace-out", default=None, help="write the per-launch CUPTI trace of the step graph here")
@@ -452,6 +452,9 @@ def main():
     ap.add_argument("--configs-in", default=None, help="use these per-layer configs instead of tuning")
     ap.add_argument("--cache-dir", default=None, help="tuning + selection cache directory (PAPER.md:179)")
     args = ap.parse_args()
+    if os.environ.get("WPK_BENCH_WATCHDOG"):   # tests: dump every thread's stack and exit instead of hanging
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["WPK_BENCH_WATCHDOG"]), exit=True)
     if args.impl == "reference":
         return run_reference(args)
 

@@ -172,6 +172,12 @@ WPK_API wpk_status wpk_conv2d_plan(const wpk_conv2d_shape *shape, wpk_dtype dtyp
  * identical for every world size. opts may be NULL (defaults). */
 WPK_API wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t budget, const wpk_tune_options *opts);
 
+/* Time the plan's current config with the tuner's protocol (the fitness measurement of a candidate,
+ * PAPER.md:68): `warmup` untimed runs, then `reps` runs each bracketed by device %globaltimer
+ * stamps (L2 evicted before each when l2_flush != 0), interquartile mean in microseconds -> *us.
+ * Uses its own synthetic buffers and stream, synchronises; WPK_ERR_CUDA if the launch fails. */
+WPK_API wpk_status wpk_conv2d_measure(wpk_plan plan, int32_t warmup, int32_t reps, int32_t l2_flush, double *us);
+
 /* Run the convolution on `stream` (a cudaStream_t; NULL = legacy default stream). Asynchronous:
  * no host synchronisation, no allocation once a workspace is set. Pointers must be 16-byte
  * aligned device pointers laid out as described above. Packed weights are cached per w pointer

@@ -93,6 +93,7 @@ def load():
         "wpk_conv2d_output_dims": (I32, [ctypes.POINTER(Shape), I32P, I32P]),
         "wpk_conv2d_plan": (I32, [ctypes.POINTER(Shape), I32, ctypes.c_int, ctypes.POINTER(P)]),
         "wpk_conv2d_tune": (I32, [P, I32, I32, ctypes.POINTER(TuneOptions)]),
+        "wpk_conv2d_measure": (I32, [P, I32, I32, I32, DP]),
         "wpk_conv2d_run": (I32, [P, P, P, P, P, P]),
         "wpk_conv2d_run_residual": (I32, [P, P, P, P, P, P, P]),
         "wpk_conv2d_fold_batchnorm": (I32, [P, P, P, P, P, P, P, ctypes.c_float, P, P, P]),

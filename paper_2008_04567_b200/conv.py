@@ -210,6 +210,12 @@ class Conv2dPlan:
         self._ws_bytes = -1
         return self.tune_stats()
 
+    def measure(self, warmup: int = 3, reps: int = 11, l2_flush: bool = True) -> float:
+        """Microseconds of the current config under the tuner's timing protocol (wpk_conv2d_measure)."""
+        us = ctypes.c_double()
+        L.check(self.lib.wpk_conv2d_measure(self.handle, int(warmup), int(reps), int(bool(l2_flush)), ctypes.byref(us)))
+        return us.value
+
     def tune_stats(self) -> TuneResult:
         best, secs = ctypes.c_double(), ctypes.c_double()
         meas, rounds = ctypes.c_int32(), ctypes.c_int32()

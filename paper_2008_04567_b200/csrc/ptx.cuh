@@ -95,6 +95,18 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *m, int c0, in
                  "r"(c0), "r"(c1), "r"(c2)
                  : "memory");
 }
+// Non-tensor bulk prefetch of [p, p + bytes) into L2 (p 16-byte aligned, bytes a multiple of 16);
+// issued in <= 64 KB pieces.
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, unsigned long long bytes) {
+    const char *c = static_cast<const char *>(p);
+    while (bytes >= 16) {
+        const uint32_t n = (uint32_t)(bytes > 65536ull ? 65536ull : (bytes & ~15ull));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(c)), "r"(n)
+                     : "memory");
+        c += n;
+        bytes -= n;
+    }
+}
 __device__ __forceinline__ void tma_load_im2col_4d(void *smem, const CUtensorMap *m, uint64_t *bar, int c,
                                                    int w, int h, int n, uint16_t off_w, uint16_t off_h) {
     asm volatile(

@@ -494,6 +494,21 @@ static void cache_store(const std::string &path, const Config &cfg, double beta,
 
 using namespace wpk;
 
+extern "C" wpk_status wpk_conv2d_measure(wpk_plan plan, int32_t warmup, int32_t reps, int32_t l2_flush, double *us) {
+    if (!plan || !us) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (reps < 1 || reps > 1024 || warmup < 0) return fail(WPK_ERR_INVALID_ARGUMENT, "bad timing protocol");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    GpuBench gb;
+    if (!gb.init(*p)) return fail(WPK_ERR_CUDA, "measure: " + gb.err);
+    bool fatal = false;
+    const Config cfg = p->cfg;
+    *us = gb.measure(*p, cfg, warmup, reps, l2_flush != 0, &fatal);
+    p->reset_ws_state();   // the measurement ran on its own workspace
+    if (fatal) return fail(WPK_ERR_CUDA, "measure: " + gb.err);
+    if (!std::isfinite(*us)) return fail(WPK_ERR_CUDA, "measure: the launch failed: " + std::string(wpk_last_error()));
+    return WPK_OK;
+}
+
 extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t budget, const wpk_tune_options *opts) {
     if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
     if (budget < 1) return fail(WPK_ERR_INVALID_ARGUMENT, "budget must be >= 1");

@@ -193,6 +193,11 @@ launch:
     a.z = L.z;
     static const int dbg_flags = env_knob("WPK_DBG_FLAGS", 0);
     a.dbg_flags = dbg_flags;
+    static const int l2pf = env_knob("WPK_L2PF", 0);   // measured: neutral (weights) to -8% (activations), off
+    a.l2pf = (g.a_mode <= 1) ? l2pf : (l2pf & 1);
+    a.wgt = L.w;
+    a.w_bytes = (long long)L.K * L.b_rs * g.cpad * e;
+    a.e_size = e;
     cudaStream_t st = (cudaStream_t)L.stream;
     long long grid = (long long)L.sm_count * g.ctas_per_sm;
     if (grid > g.work) grid = g.work;

@@ -43,6 +43,12 @@ struct UmmaArgs {
     int a_split;                    // A stage loaded by two threads (two half-height boxes)
     const void *z;                  // residual (epilogue 3), laid out as y
     int dbg_flags;                  // experiments only (WPK_DBG_FLAGS): 1 = gather zero-fills, 2 = no y stores
+    // L2 prefetch (bit 0: weights, this CTA's 1/grid slice of the packed tensor, before the PDL wait;
+    // bit 1: activations, the input rows of this CTA's next work item, TMA producers only)
+    int l2pf;
+    const void *wgt;                // packed weights [K][R*S][C] as the B tensor map sees them
+    long long w_bytes;
+    int e_size;                     // bytes per element of x / w
 };
 
 // Tensor maps of the last launch, reused while pointers and config are unchanged (host-side

@@ -663,6 +663,27 @@ __device__ __forceinline__ void segment_gather(const UmmaArgs &a, uint8_t *smA, 
         }
 }
 
+// L2 prefetch of the activation rows one work item's A loads will read: NHWC rows [h_lo, h_hi]
+// of the images its output pixels m0 .. m0 + rows - 1 belong to (whole rows: contiguous bytes);
+// for the plain 2-D A view (1x1/s1/p0) the pixel rows themselves.
+__device__ __forceinline__ void prefetch_a_rows(const UmmaArgs &a, long long m0, int rows) {
+    if (m0 >= a.M) return;
+    const long long m1 = min(a.M, m0 + rows) - 1;
+    const long long rowb = (long long)a.C * a.e_size;             // bytes per input pixel
+    const char *x = static_cast<const char *>(a.x);
+    if (a.a_tiled) {
+        ptx::bulk_prefetch_l2(x + m0 * rowb, (unsigned long long)((m1 - m0 + 1) * rowb));
+        return;
+    }
+    const long long n0 = m0 / a.PQ, n1 = m1 / a.PQ;
+    const int p0 = (int)((m0 - n0 * a.PQ) / a.Q), p1 = (int)((m1 - n1 * a.PQ) / a.Q);
+    const int hlo = max(0, p0 * a.stride_h - a.pad_h);
+    const int hhi = min(a.H - 1, p1 * a.stride_h - a.pad_h + (a.R - 1) * a.dil_h);
+    const long long b0 = ((n0 * a.H + hlo) * a.W) * rowb;
+    const long long b1 = ((n1 * a.H + hhi + 1) * a.W) * rowb;
+    if (b1 > b0) ptx::bulk_prefetch_l2(x + b0, (unsigned long long)(b1 - b0));
+}
+
 // 12 warps (16 with gather producers): 0 = A producer, 1 = TMEM allocator + MMA issuer,
 // 2 = B producer, 3 = spare, 4..11 = epilogue (two groups of four; warp w reads TMEM lanes
 // [32*(w%4), +32)), 12..15 = gather producers.
@@ -758,7 +779,21 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
         if (lane == 0 && !(kGather && warp == 0)) {
             const bool isA = (warp != 2);
             const int half = (warp == 3) ? 1 : 0;
+            // weights are inference constants: this CTA's 1/grid slice of them goes to L2 while the
+            // previous grid (PDL) is still running, so no K block waits on DRAM for its B tile
+            if (!isA && (a.l2pf & 1)) {
+                const long long chunk = ((a.w_bytes + gridDim.x - 1) / gridDim.x + 255) / 256 * 256;
+                const long long off = (long long)blockIdx.x * chunk;
+                if (off < a.w_bytes)
+                    ptx::bulk_prefetch_l2(static_cast<const char *>(a.wgt) + off,
+                                          (unsigned long long)min(chunk, a.w_bytes - off));
+            }
             if (isA) asm volatile("griddepcontrol.wait;" ::: "memory");
+            const int pf_rows = (int)((kPair ? 128u : (uint32_t)a.bm) >> (a.a_split ? 1 : 0));
+            if (isA && half == 0 && (a.l2pf & 2) && wstart < a.work) {   // the first work item's input rows
+                const WorkPos wp0 = decode_work(wstart, a);
+                prefetch_a_rows(a, (long long)wp0.mt * a.bm + crank * 128, pf_rows << (a.a_split ? 1 : 0));
+            }
             if (dbg && isA && half == 0) dbg[7] = ptx::globaltimer();   // previous grid complete
             uint32_t stage = 0, phase = 0;
             const uint32_t a_rows = (kPair ? 128u : (uint32_t)a.bm) >> (a.a_split ? 1 : 0);   // rows per A load
@@ -768,6 +803,10 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             for (long long w = wstart; w < a.work; w += wstep) {
                 const WorkPos wp = decode_work(w, a);
                 const long long m0 = (long long)wp.mt * a.bm + crank * 128 + (long long)half * a_rows;
+                if (isA && half == 0 && (a.l2pf & 2) && w + wstep < a.work) {   // one work item ahead
+                    const WorkPos wn = decode_work(w + wstep, a);
+                    if (wn.mt != wp.mt) prefetch_a_rows(a, (long long)wn.mt * a.bm + crank * 128, pf_rows << (a.a_split ? 1 : 0));
+                }
                 const int n0 = wp.nt * a.bn + (int)crank * (a.bn / 2);
                 int wc = 0, hc = 0, nimg = 0;
                 if (isA && !a.a_tiled) {

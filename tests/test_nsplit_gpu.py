@@ -70,16 +70,21 @@ def test_nsplit_shards_equal_single_process(tmp_path):
         assert parts[-1][0] + parts[-1][1] == parts[0][2]
 
 
-def test_bench_two_ranks_gloo_one_device():
-    env = dict(os.environ, WPK_BENCH_BACKEND="gloo", OMP_NUM_THREADS="4")
+def test_bench_two_ranks_gloo_one_device(tmp_path):
+    env = dict(os.environ, WPK_BENCH_BACKEND="gloo", OMP_NUM_THREADS="4", WPK_BENCH_WATCHDOG="420")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2",
            "--steps", "3", "--warmup", "3", "--tune-budget", "6", "--ga-pop", "4", "--no-cudnn",
            "--no-cpu-baseline", "--graph-refine", "1"]
-    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500, cwd=ROOT)
-    assert out.returncode == 0, out.stderr[-3000:]
-    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
-    assert len(lines) == 1, out.stdout[-2000:]
+    with open(tmp_path / "out.txt", "w") as fo, open(tmp_path / "err.txt", "w") as fe:
+        try:
+            rc = subprocess.run(cmd, env=env, stdout=fo, stderr=fe, timeout=600, cwd=ROOT).returncode
+        except subprocess.TimeoutExpired:
+            rc = "timeout"
+    out, err = open(tmp_path / "out.txt").read(), open(tmp_path / "err.txt").read()
+    assert rc == 0, (rc, err[-6000:])
+    lines = [l for l in out.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out[-2000:]
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
     assert line["config"]["global_batch"] == 64

@@ -18,7 +18,7 @@ def test_measured_tune_bf16(search, tmp_path):
     default = plan.config
     rec = str(tmp_path / "rec.jsonl")
     kw = dict(rl_hidden=[64, 64, 64, 64], rl_horizon=8, rl_envs=4) if search == "rl" else {}
-    res = plan.tune(search, 24, seed=1, record_path=rec, warmup=2, reps=5, **kw)
+    res = plan.tune(search, 24, seed=1, record_path=rec, warmup=2, reps=5, finalists=0, **kw)
     assert res.measured <= 24 and res.best_us > 0
     assert len(open(rec).read().splitlines()) == res.measured
     x, w, b = workloads.generate(L, "bf16", "int", seed=3)
@@ -30,3 +30,21 @@ def test_measured_tune_bf16(search, tmp_path):
     plan2 = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype="bf16")
     res2 = plan2.tune(search, 24, seed=1, eval_mode="replay", replay_path=rec, **kw)
     assert res2.genes == res.genes and res2.best_us == res.best_us
+
+
+def test_measured_tune_finalists(tmp_path):
+    """Finalist re-timing (SURVEY.md 8(d) protocol item 2): after the search the top-4 measured
+    configs are re-timed and the lowest re-timed one wins, so the choice is one of the top-4 of the
+    recorded search timings and the reported beta is a re-measurement (not the search's best-ever)."""
+    import json
+    L = ConvLayer("t", 8, 64, 28, 28, 128, 3, 3, 1, 1)
+    from paper_2008_04567_b200 import Conv2dPlan
+    plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype="bf16")
+    rec, log = str(tmp_path / "rec.jsonl"), str(tmp_path / "log.jsonl")
+    res = plan.tune("ga", 24, seed=2, record_path=rec, log_path=log, warmup=2, reps=5, finalists=4)
+    recs = sorted((json.loads(l) for l in open(rec)), key=lambda r: r["beta_us"])
+    top = [r["genes"] for r in recs[:4]]
+    assert res.genes in top
+    fin = [json.loads(l) for l in open(log) if '"finalist"' in l]
+    assert len(fin) == 4 and [f["genes"] for f in fin] == top
+    assert res.best_us == min(f["median_beta"] for f in fin)
