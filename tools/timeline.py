@@ -51,6 +51,11 @@ for i, n in enumerate(names):
     col = rel[:, i]
     col = col[col > -1e6]
     print(f"  {n:14s} min {col.min():8.2f}  median {np.median(col):8.2f}  max {col.max():8.2f} us")
+if int(os.environ.get("WPK_DBG_FLAGS", "0")) & 128:   # MMA-loop cycle accounting, first tile
+    c = t64[t64[:, 0] > 0][:, 60:64]
+    nkb = np.maximum(c[:, 3], 1)
+    print("  MMA loop, clk per K block (median over CTAs): wait %.0f  issue %.0f  total %.0f  (kb %d)" % (
+        np.median(c[:, 0] / nkb), np.median(c[:, 1] / nkb), np.median(c[:, 2] / nkb), int(np.median(c[:, 3]))))
 if int(os.environ.get("WPK_DBG_FLAGS", "0")) & 8:   # per-K-block stamps of the first tile, CTA 0
     r0 = t64[0]
     print("  CTA0 first tile, us:  A issued / B issued / stage full (MMA)")
