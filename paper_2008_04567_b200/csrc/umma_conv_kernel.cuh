@@ -206,57 +206,213 @@ __device__ __forceinline__ void epi_chunk_tma(EpiCtx &E, const UmmaArgs &a, cons
     stage_and_store<FINAL>(E, a, tmY, pk, k0, mrow, split);
 }
 
-// Split-K owner chunk (the last split of a tile): sums the other splits' fp32 partials (read from
-// L2) and its own accumulator (TMEM) in the fixed split order 0..S-1, then +bias, ReLU, one RN
-// rounding and the TMA store of the final output. 32 columns at a time.
+// The split-K owner's whole slab (its chunks ci0, ci0 + cstep, ... of one 32-row group), software
+// pipelined: the previous splits' fp32 partials of the next 32 columns are loaded from L2 while the
+// current 32 columns are reduced, so an L2 round trip (~1-2 us under load) is paid once per slab
+// instead of once per 32 columns (measured: pair split-2 owners finished up to 11 us after the
+// last MMA, tools/timeline.py). Same arithmetic and order as before: partials of splits 0..S-2 in
+// split order, then the owner's own TMEM accumulator, bias, ReLU, one rounding. Each 32-column
+// half goes straight into the swizzled staging row (no packed copy of the whole chunk is held).
 template <typename T>
-__device__ __forceinline__ void epi_chunk_owner(EpiCtx &E, const UmmaArgs &a, const CUtensorMap *tmY, uint32_t taddr,
-                                                int k0, int mrow) {
+__device__ __forceinline__ void epi_owner_run(EpiCtx &E, const UmmaArgs &a, const CUtensorMap *tmY, uint32_t tbase,
+                                              int n0, int mrow, int ci0, int cstep, int nchunks) {
     constexpr int CW = 128 / sizeof(T);          // columns per 128-byte output chunk (64 or 32)
+    constexpr int HPC = CW / 32;                 // 32-column halves per chunk
+    constexpr int JPH = 8 / HPC;                 // 16-byte row pieces per half
     const long long m = (long long)mrow + E.lane;
     const bool mok = m < a.M;
     const long long MK = a.M * (long long)a.K;
     const float *prow = a.partial + m * a.K;
     const int nprev = a.splits - 1;
-    uint32_t pk[32];
+    auto chunk_of = [&](int j) { return ci0 + (j / HPC) * cstep; };
+    auto valid = [&](int j) { const int ci = chunk_of(j); return ci < nchunks && n0 + ci * CW < a.K; };
+    auto col_of = [&](int j) { return n0 + chunk_of(j) * CW + (j % HPC) * 32; };
+    auto ld8 = [&](float4 *v, const float *src, int kh) {
 #pragma unroll
-    for (int half = 0; half < CW / 32; ++half) {
-        const int kh = k0 + half * 32;
+        for (int q = 0; q < 8; ++q)
+            v[q] = (mok && kh + 4 * q < a.K) ? __ldcg(reinterpret_cast<const float4 *>(src + kh + 4 * q))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    // reduce 32 columns (partials in cur) and write them into the staging row
+    auto step = [&](int j, float4 *cur, uint32_t row_addr) {
+        const int half = j % HPC, kh = col_of(j);
         uint32_t raw[32];
-        ptx::tmem_ld32_nowait(taddr + half * 32, raw);
-        float acc[32];
-        for (int sp = 0; sp < nprev; ++sp) {
+        ptx::tmem_ld32_nowait(tbase + (uint32_t)(chunk_of(j) * CW + half * 32), raw);
+        for (int sp = 1; sp < nprev; ++sp) {                  // splits 1 .. S-2 (S > 2), in order
             float4 v[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                v[q] = (mok && kh + 4 * q < a.K) ? __ldcg(reinterpret_cast<const float4 *>(prow + sp * MK + kh + 4 * q))
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            ld8(v, prow + sp * MK, kh);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                if (sp == 0) {
-                    acc[4 * q] = v[q].x; acc[4 * q + 1] = v[q].y; acc[4 * q + 2] = v[q].z; acc[4 * q + 3] = v[q].w;
-                } else {
-                    acc[4 * q] += v[q].x; acc[4 * q + 1] += v[q].y; acc[4 * q + 2] += v[q].z; acc[4 * q + 3] += v[q].w;
-                }
+                cur[q].x += v[q].x; cur[q].y += v[q].y; cur[q].z += v[q].z; cur[q].w += v[q].w;
             }
         }
         ptx::tmem_wait_ld();
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            float v[4];
+        for (int jj = 0; jj < JPH; ++jj) {
+            uint32_t w4[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) v[j] = acc[4 * q + j] + __uint_as_float(raw[4 * q + j]);
-            bias_relu4(v, E.sBias, kh + 4 * q, a.epilogue == 2);
-            if constexpr (sizeof(T) == 2) {
-                pk[half * 16 + 2 * q] = pack2(v[0], v[1], (T *)nullptr);
-                pk[half * 16 + 2 * q + 1] = pack2(v[2], v[3], (T *)nullptr);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) pk[4 * q + j] = __float_as_uint(v[j]);
+            for (int e = 0; e < 4; ++e) {   // 16 bytes: 8 (16-bit) or 4 (fp32) columns
+                if constexpr (sizeof(T) == 2) {
+                    const int q = jj * 2 + e / 2;
+                    float v2[4] = {cur[q].x + __uint_as_float(raw[4 * q]), cur[q].y + __uint_as_float(raw[4 * q + 1]),
+                                   cur[q].z + __uint_as_float(raw[4 * q + 2]), cur[q].w + __uint_as_float(raw[4 * q + 3])};
+                    bias_relu4(v2, E.sBias, kh + 4 * q, a.epilogue == 2);
+                    w4[e] = (e & 1) ? pack2(v2[2], v2[3], (T *)nullptr) : pack2(v2[0], v2[1], (T *)nullptr);
+                } else {
+                    const int q = jj;
+                    float v2[4] = {cur[q].x + __uint_as_float(raw[4 * q]), cur[q].y + __uint_as_float(raw[4 * q + 1]),
+                                   cur[q].z + __uint_as_float(raw[4 * q + 2]), cur[q].w + __uint_as_float(raw[4 * q + 3])};
+                    bias_relu4(v2, E.sBias, kh + 4 * q, a.epilogue == 2);
+                    w4[e] = __float_as_uint(v2[e]);
+                }
             }
+            const int piece = half * JPH + jj;
+            ptx::st_shared_v4(row_addr + ((uint32_t)(piece ^ (E.lane & 7)) << 4), w4[0], w4[1], w4[2], w4[3]);
+        }
+    };
+    float4 bA[8], bB[8];
+    if (valid(0)) ld8(bA, prow, col_of(0));
+    uint32_t row_addr = 0;
+    for (int j = 0; valid(j); j += 2) {
+        // (j even: bA holds its partials; j + 1 uses bB)
+        if (j % HPC == 0) {   // a new output chunk: its staging buffer must be free
+            if (E.nbufs == 2) ptx::bulk_wait_read<1>();
+            else ptx::bulk_wait_read<0>();
+            __syncwarp();
+            row_addr = ptx::smem_u32(E.sEpi + E.ebuf * 4096) + (uint32_t)E.lane * 128;
+        }
+        const bool v1 = valid(j + 1);
+        if (v1) ld8(bB, prow, col_of(j + 1));
+        step(j, bA, row_addr);
+        if ((j + 1) % HPC == 0 || !v1) {   // chunk complete
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (E.lane == 0 && !(WPK_DBG_FLAGS(a) & 2)) {
+                ptx::tma_store_2d(tmY, E.sEpi + E.ebuf * 4096, n0 + chunk_of(j) * CW, mrow);
+                ptx::bulk_commit();
+            }
+            if (E.nbufs == 2) E.ebuf ^= 1;
+        }
+        if (!v1) break;
+        if ((j + 1) % HPC == 0) {
+            if (E.nbufs == 2) ptx::bulk_wait_read<1>();
+            else ptx::bulk_wait_read<0>();
+            __syncwarp();
+            row_addr = ptx::smem_u32(E.sEpi + E.ebuf * 4096) + (uint32_t)E.lane * 128;
+        }
+        if (valid(j + 2)) ld8(bA, prow, col_of(j + 2));
+        step(j + 1, bB, row_addr);
+        if ((j + 2) % HPC == 0 || !valid(j + 2)) {
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (E.lane == 0 && !(WPK_DBG_FLAGS(a) & 2)) {
+                ptx::tma_store_2d(tmY, E.sEpi + E.ebuf * 4096, n0 + chunk_of(j + 1) * CW, mrow);
+                ptx::bulk_commit();
+            }
+            if (E.nbufs == 2) E.ebuf ^= 1;
         }
     }
-    stage_and_store<true>(E, a, tmY, pk, k0, mrow, 0);
+}
+
+// Split-K owner, bulk variant (the CTA's last work item, so its pipeline stages are idle): every
+// epilogue warp TMA-loads the previous splits' fp32 partials of ITS rows and chunks into the stage
+// area (32 x 32 boxes through the partials' tensor map), all 8 warps wait on one barrier, then each
+// lane reads its row back from the 128-byte-swizzled boxes. One L2 round trip per tile instead of
+// one per 32 columns of per-lane row loads (measured: ~10 us of owner reduction).
+// Sum order as everywhere: splits 0..S-2, then the owner's own TMEM accumulator; bias, ReLU, one
+// rounding. Slab layout: box (sp, rq = 32-row group, c = 32-column block) at
+// ((sp * nrq + rq) * ncb + c) * 4 KB.
+template <typename T>
+__device__ __forceinline__ void epi_owner_bulk(EpiCtx &E, const UmmaArgs &a, const CUtensorMap *tmY,
+                                               const CUtensorMap *tmP, uint8_t *slab, uint64_t *pbar,
+                                               uint32_t tbase, int n0, int mrow, int rq, int nrq, int ci0,
+                                               int cstep, int nchunks) {
+    constexpr int CW = 128 / sizeof(T);
+    constexpr int HPC = CW / 32;
+    const int ncb = a.bn / 32;
+    const int nprev = a.splits - 1;
+    // (1) this warp's loads: every previous split x its chunks' 32-column blocks, its 32 rows
+    uint32_t bytes = 0;
+    for (int ci = ci0; ci < nchunks && n0 + ci * CW < a.K; ci += cstep) bytes += (uint32_t)(nprev * HPC) * 4096u;
+    if (E.lane == 0) {
+        ptx::mbar_arrive_expect_tx(pbar, bytes);
+        for (int ci = ci0; ci < nchunks && n0 + ci * CW < a.K; ci += cstep)
+            for (int sp = 0; sp < nprev; ++sp)
+                for (int hf = 0; hf < HPC; ++hf) {
+                    const int c = ci * HPC + hf;
+                    ptx::tma_load_3d(slab + (size_t)((sp * nrq + rq) * ncb + c) * 4096u, tmP, pbar, n0 + c * 32, mrow, sp);
+                }
+    }
+    __syncwarp();
+    ptx::mbar_wait(pbar, 0);   // (2) all 8 warps' boxes landed (one phase per launch: the CTA's last item)
+    const uint32_t slab_u = ptx::smem_u32(slab);
+    const uint32_t swz = (uint32_t)(E.lane & 7);
+    // (3) reduce chunk by chunk into the staging buffers, TMA store
+    for (int ci = ci0; ci < nchunks; ci += cstep) {
+        const int k0 = n0 + ci * CW;
+        if (k0 >= a.K) break;
+        if (E.nbufs == 2) ptx::bulk_wait_read<1>();
+        else ptx::bulk_wait_read<0>();
+        __syncwarp();
+        const uint32_t row_addr = ptx::smem_u32(E.sEpi + E.ebuf * 4096) + (uint32_t)E.lane * 128;
+#pragma unroll
+        for (int hf = 0; hf < HPC; ++hf) {
+            const int c = ci * HPC + hf;
+#pragma unroll
+            for (int sb = 0; sb < 2; ++sb) {   // 16 columns at a time (register pressure)
+                const int kh = k0 + hf * 32 + sb * 16;
+                uint32_t raw[16];
+                ptx::tmem_ld16_nowait(tbase + (uint32_t)(ci * CW + hf * 32 + sb * 16), raw);
+                float acc[16];
+                for (int sp = 0; sp < nprev; ++sp) {
+                    const uint32_t rb = slab_u + (uint32_t)((sp * nrq + rq) * ncb + c) * 4096u + (uint32_t)E.lane * 128u;
+#pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        uint32_t x0, x1, x2, x3;
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                                     : "r"(rb + (((uint32_t)(sb * 4 + p) ^ swz) << 4)));
+                        const float f[4] = {__uint_as_float(x0), __uint_as_float(x1), __uint_as_float(x2), __uint_as_float(x3)};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) acc[4 * p + e] = (sp == 0) ? f[e] : acc[4 * p + e] + f[e];
+                    }
+                }
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc[4 * q + e] += __uint_as_float(raw[4 * q + e]);
+                    bias_relu4(acc + 4 * q, E.sBias, kh + 4 * q, a.epilogue == 2);
+                }
+                if constexpr (sizeof(T) == 2) {   // 16 columns = two 16-byte pieces
+#pragma unroll
+                    for (int pc = 0; pc < 2; ++pc) {
+                        const float *v = acc + 8 * pc;
+                        const int piece = hf * 4 + sb * 2 + pc;
+                        ptx::st_shared_v4(row_addr + (((uint32_t)piece ^ swz) << 4), pack2(v[0], v[1], (T *)nullptr),
+                                          pack2(v[2], v[3], (T *)nullptr), pack2(v[4], v[5], (T *)nullptr),
+                                          pack2(v[6], v[7], (T *)nullptr));
+                    }
+                } else {                          // fp32: four pieces
+#pragma unroll
+                    for (int pc = 0; pc < 4; ++pc) {
+                        const float *v = acc + 4 * pc;
+                        const int piece = sb * 4 + pc;
+                        ptx::st_shared_v4(row_addr + (((uint32_t)piece ^ swz) << 4), __float_as_uint(v[0]),
+                                          __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
+                    }
+                }
+            }
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (E.lane == 0 && !(WPK_DBG_FLAGS(a) & 2)) {
+            ptx::tma_store_2d(tmY, E.sEpi + E.ebuf * 4096, k0, mrow);
+            ptx::bulk_commit();
+        }
+        __syncwarp();
+        if (E.nbufs == 2) E.ebuf ^= 1;
+    }
 }
 
 // Cluster split-K owner chunk: columns [k0, k0 + 128 B) of this CTA's output slice; the other
@@ -721,6 +877,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
     volatile int *sFlag = reinterpret_cast<volatile int *>(bars + 25);
     uint64_t *freeb = bars + 26;      // EK_CSPLIT: every peer's stages are idle (S - 1 remote arrives)
     uint64_t *datab = bars + 27;      // EK_CSPLIT: every peer delivered its partials (8 (S - 1) arrives)
+    uint64_t *pbar = bars + 28;       // EK_SPLIT owner: the other splits' partial slab landed (8 warps)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef WPK_TIMELINE   // per-CTA globaltimer stamps for tools/timeline.py (libwpk_timeline.so only)
@@ -748,6 +905,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             ptx::mbar_init(freeb, a.splits - 1);
             ptx::mbar_init(datab, 8 * (a.splits - 1));
         }
+        if (EK == EK_SPLIT) ptx::mbar_init(pbar, 8);
         ptx::fence_mbar_init();
     }
     if (warp == 1) {
@@ -963,7 +1121,9 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             const int ctile = (wp.mt * a.n_tiles + wp.nt) * (kPair ? 2 : 1) + (int)crank;
             if (EK == EK_SPLIT && owner) {
                 if (warp == 4 && lane == 0) {
+                    if (dbg && w == wstart) dbg[59] = ptx::globaltimer();   // owner starts waiting
                     while (ptx::ld_acquire_gpu(a.counters + ctile) < a.splits - 1) __nanosleep(32);
+                    if (dbg && w == wstart) dbg[57] = ptx::globaltimer();   // owner saw every split published
                 }
                 ptx::named_bar_sync(1, 256);
             }
@@ -1031,6 +1191,14 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 if (nsub == 2 && h != grp) continue;
                 const int mrow = wp.mt * a.bm + (int)crank * 128 + h * 128 + quarter * 32;
                 const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * acc_cols + h * a.bn;
+                if (EK == EK_SPLIT && owner) {
+                    if (a.owner_bulk && w + wstep >= a.work)   // the CTA's last item: its stages are idle
+                        epi_owner_bulk<T>(E, a, &tmY, &tmP, smem, pbar, tbase, n0, mrow, h * 4 + quarter, nsub * 4,
+                                          nsub == 2 ? 0 : grp, nsub == 2 ? 1 : 2, nchunks);
+                    else
+                        epi_owner_run<T>(E, a, &tmY, tbase, n0, mrow, nsub == 2 ? 0 : grp, nsub == 2 ? 1 : 2, nchunks);
+                    continue;
+                }
                 for (int ci = (nsub == 2 ? 0 : grp); ci < nchunks; ci += (nsub == 2 ? 1 : 2)) {
                     const int c0 = ci * cw;
                     const int k0 = n0 + c0;
@@ -1038,8 +1206,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                     if constexpr (EK == EK_TMA) {
                         epi_chunk_tma<T, true, RES>(E, a, &tmY, tbase + c0, k0, mrow, 0);
                     } else if constexpr (EK == EK_SPLIT) {
-                        if (owner) epi_chunk_owner<T>(E, a, &tmY, tbase + c0, k0, mrow);
-                        else epi_chunk_tma<T, false>(E, a, &tmP, tbase + c0, k0, mrow, wp.split);
+                        epi_chunk_tma<T, false>(E, a, &tmP, tbase + c0, k0, mrow, wp.split);   // (owner: above)
                     } else {
                         epi_chunk_direct<T>(a, sBias, tbase + c0, k0, (long long)mrow + lane, wp.split, a.splits == 1);
                     }
@@ -1064,9 +1231,11 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                     __threadfence();
                     ptx::named_bar_sync(1, 256);
                     if (warp == 4 && lane == 0) atomicAdd(a.counters + ctile, 1);
+                    if (dbg && warp == 4 && lane == 0 && w == wstart) dbg[56] = ptx::globaltimer();   // published
                 } else {        // all 8 warps have consumed the partials: reset for the next launch
                     ptx::named_bar_sync(1, 256);
                     if (warp == 4 && lane == 0) a.counters[ctile] = 0;
+                    if (dbg && warp == 4 && lane == 0 && w == wstart) dbg[58] = ptx::globaltimer();   // owner done
                 }
             }
             if (EK == EK_DIRECT && a.splits > 1) splitk_fixup<T>(a, sBias, sFlag, wp, nsub, warp, lane, crank, kPair ? 1 : 0);

@@ -70,6 +70,13 @@ for it in range(8):
     row = ev[0, it, :6] if ev[0, it, 5] > 0 else ev[0, it, :5]
     if row[0] > 0:
         print("   tile", it, np.round((row - t0) / 1000.0, 2))
+sk = t64[t64[:, 0] > 0][:, 56:60]
+if (sk > 0).any():   # split-K (EK_SPLIT) first work item: publish / owner wait start / wait done / done
+    for i, n in [(0, "splitk_published"), (3, "owner_wait_start"), (1, "owner_saw_all"), (2, "owner_done")]:
+        col = sk[:, i]
+        col = (col[col > 0] - t0) / 1000.0
+        if len(col):
+            print(f"  {n:16s} min {col.min():8.2f}  median {np.median(col):8.2f}  max {col.max():8.2f} us  (n={len(col)})")
 fx = t[:, 8:14]
 if os.environ.get("SPLITK_FIX") and (fx[:, 0] > 0).any():
     sel = fx[:, 0] > 0
