@@ -84,9 +84,18 @@ typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 
  *                     VEC_C | K/groups), genes = (VEC_C, PIX_PER_THREAD, THREADS, -, -, -, -)
  *   WPK_FAMILY_GEMM32 : exact-fp32 implicit GEMM on CUDA cores (WPK_F32, groups == 1), genes =
  *                     (BLOCK_M, BLOCK_N, BLOCK_K, THREAD_TILE, SPLIT_K, -, -); the F32 default;
- *                     SPLIT_K > 1 sums per-split fp32 partials in split order (deterministic) */
+ *                     SPLIT_K > 1 sums per-split fp32 partials in split order (deterministic)
+ *   WPK_FAMILY_JIT  : the SIMT template generated per candidate with every shape parameter and gene
+ *                     a compile-time constant and compiled just in time with NVRTC for sm_100a
+ *                     (PAPER.md:68 Step2 "compile the generated codes just-in-time ... then execute
+ *                     them"); same genes and arithmetic as SIMT (bit-identical results), every Tile_rz
+ *                     for every dtype. Compiled cubins are cached per process and, with a cache
+ *                     directory, on disk; the tuner compiles each generation's new candidates on a
+ *                     pool of host threads before measuring them. Opt-in (never a
+ *                     plan's default): tune with family = WPK_FAMILY_JIT or set_config. */
 typedef enum {
-    WPK_FAMILY_SIMT = 0, WPK_FAMILY_UMMA = 1, WPK_FAMILY_DW = 2, WPK_FAMILY_GEMM32 = 3, WPK_FAMILY_AUTO = -1
+    WPK_FAMILY_SIMT = 0, WPK_FAMILY_UMMA = 1, WPK_FAMILY_DW = 2, WPK_FAMILY_GEMM32 = 3, WPK_FAMILY_JIT = 4,
+    WPK_FAMILY_AUTO = -1
 } wpk_family;
 
 /* Operator shape: the first 9 entries of the paper's O_conv generalised with
@@ -249,6 +258,20 @@ WPK_API int32_t wpk_conv2d_last_launch_count(wpk_plan plan);
  * generations/steps, wall seconds. */
 WPK_API wpk_status wpk_conv2d_tune_stats(wpk_plan plan, double *best_us, int32_t *measured, int32_t *rounds,
                                  double *seconds);
+
+/* JIT family (WPK_FAMILY_JIT). wpk_jit_compile: generate and compile (NVRTC, sm_100a) the kernel of
+ * the plan's shape with `genes`, or take it from the cache; no GPU is needed. *cubin_bytes (may be
+ * NULL) receives the cubin size. WPK_ERR_INVALID_CONFIG if the genes are invalid for the JIT family,
+ * WPK_ERR_INTERNAL with the NVRTC log in wpk_last_error if compilation fails.
+ * wpk_jit_set_cache_dir: directory for the on-disk cubin cache (NULL or "" = memory only; default
+ * from the environment variable WPK_JIT_CACHE_DIR). The directory must exist; files are written
+ * atomically (temp + rename) and carry their key, so concurrent processes may share it.
+ * wpk_jit_stats: process-wide counters since load: NVRTC compiles, in-memory hits, disk hits,
+ * failed compiles, and the summed compile wall time in seconds (any pointer may be NULL). */
+WPK_API wpk_status wpk_jit_compile(wpk_plan plan, const int32_t *genes, size_t *cubin_bytes);
+WPK_API wpk_status wpk_jit_set_cache_dir(const char *dir);
+WPK_API wpk_status wpk_jit_stats(int64_t *compiles, int64_t *mem_hits, int64_t *disk_hits, int64_t *failures,
+                                 double *compile_seconds);
 
 /* RL-search learner primitives, exported so the C++ learner can be checked against the oracle
  * (tests/test_tuner_parity.py). dims[0..5] = {obs, h1, h2, h3, h4, A+1}. params is the flat

@@ -26,7 +26,7 @@ LAYOUTS = {"nchw": 0, "nhwc": 1}
 EPILOGUES = {"none": 0, "bias": 1, "bias_relu": 2, "bias_add_relu": 3}
 SEARCHES = {"ga": 0, "rl": 1, "random": 2}
 EVAL_MODES = {"measured": 0, "replay": 1, "synthetic": 2}
-FAMILIES = {"simt": 0, "umma": 1, "dw": 2, "gemm32": 3, "auto": -1}
+FAMILIES = {"simt": 0, "umma": 1, "dw": 2, "gemm32": 3, "jit": 4, "auto": -1}
 
 
 class WpkError(RuntimeError):
@@ -113,6 +113,9 @@ def load():
         "wpk_ppo_loss_grad": (I32, [I32P, DP, I32, DP, I32P, DP, DP, DP, DP, DP, D, DP, DP]),
         "wpk_gae": (I32, [I32, DP, DP, D, D, DP]),
         "wpk_observation": (I32, [ctypes.POINTER(Shape), I32P, D, DP]),
+        "wpk_jit_compile": (I32, [P, I32P, ctypes.POINTER(ctypes.c_size_t)]),
+        "wpk_jit_set_cache_dir": (I32, [ctypes.c_char_p]),
+        "wpk_jit_stats": (I32, [ctypes.POINTER(ctypes.c_int64)] * 4 + [DP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -153,3 +156,17 @@ def family_describe(family: str | int):
     check(load().wpk_family_describe(fam, counts, values, names))
     doms = [[values[g * 32 + i] for i in range(counts[g])] for g in range(NUM_GENES)]
     return [n.decode() for n in names], doms
+
+
+def jit_set_cache_dir(path: str | None):
+    """On-disk cubin cache of the JIT family (None = memory only)."""
+    check(load().wpk_jit_set_cache_dir(path.encode() if path else None))
+
+
+def jit_stats() -> dict:
+    """Process-wide JIT counters: NVRTC compiles, memory / disk cache hits, failures, compile seconds."""
+    v = [ctypes.c_int64() for _ in range(4)]
+    sec = ctypes.c_double()
+    check(load().wpk_jit_stats(*[ctypes.byref(x) for x in v], ctypes.byref(sec)))
+    return {"compiles": v[0].value, "mem_hits": v[1].value, "disk_hits": v[2].value, "failures": v[3].value,
+            "compile_seconds": sec.value}

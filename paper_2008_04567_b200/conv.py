@@ -78,6 +78,14 @@ class Conv2dPlan:
         L.check(self.lib.wpk_conv2d_set_config(self.handle, fam, arr))
         self._ws_bytes = -1
 
+    def jit_compile(self, genes) -> int:
+        """Generate + NVRTC-compile this shape's JIT-family kernel for `genes` (no GPU needed);
+        returns the cubin size in bytes (cached per process / on disk)."""
+        arr = (ctypes.c_int32 * L.NUM_GENES)(*genes)
+        n = ctypes.c_size_t()
+        L.check(self.lib.wpk_jit_compile(self.handle, arr, ctypes.byref(n)))
+        return n.value
+
     def config_valid(self, family, genes) -> bool:
         fam = L.FAMILIES[family] if isinstance(family, str) else int(family)
         arr = (ctypes.c_int32 * L.NUM_GENES)(*genes)

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "wpk_internal.h"
+#include "jit.h"
 
 namespace wpk {
 
@@ -62,8 +63,9 @@ static wpk_status to_desc(const wpk_conv2d_shape *s, int dtype, ConvDesc *d) {
 static Space make_space(int family) {
     Space sp;
     sp.family = family;
-    if (family == WPK_FAMILY_SIMT) {
-        // the paper's own gene set: threads per block and outputs per thread
+    if (family == WPK_FAMILY_SIMT || family == WPK_FAMILY_JIT) {
+        // the paper's own gene set: threads per block and outputs per thread (the JIT
+        // family compiles the same template per candidate with NVRTC)
         sp.dom = {{1, 2, 4, 8, 16, 32}, {1, 2, 4, 8, 16, 32}, {1, 2, 4, 8, 16, 32},
                   {1, 2, 4}, {1, 2, 4}, {1, 2, 4}, {1, 2, 4, 8}};
         sp.names = {"T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"};
@@ -82,8 +84,8 @@ static Space make_space(int family) {
 }
 
 const Space &family_space(int family) {
-    static const Space spaces[4] = {make_space(0), make_space(1), make_space(2), make_space(3)};
-    return spaces[family < 0 || family > 3 ? 0 : family];
+    static const Space spaces[5] = {make_space(0), make_space(1), make_space(2), make_space(3), make_space(4)};
+    return spaces[family < 0 || family > 4 ? 0 : family];
 }
 
 static bool in_domain(const Space &sp, const Config &cfg, std::string *why) {
@@ -100,6 +102,7 @@ static bool in_domain(const Space &sp, const Config &cfg, std::string *why) {
 bool family_applicable(const ConvDesc &d, int family, std::string *why) {
     auto no = [&](const char *m) { if (why) *why = m; return false; };
     if (family == WPK_FAMILY_SIMT) return true;   // the SIMT kernel handles every valid shape, layout and dtype
+    if (family == WPK_FAMILY_JIT) return true;    // so does its NVRTC-specialised twin
     if (family == WPK_FAMILY_DW) {
         if (d.g < 2) return no("DW family needs groups > 1 (depthwise or grouped)");
         return true;
@@ -244,17 +247,17 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
 }
 
 bool config_valid(const ConvDesc &d, const Config &cfg, std::string *why) {
-    if (cfg.family < 0 || cfg.family > 3) { if (why) *why = "bad family"; return false; }
+    if (cfg.family < 0 || cfg.family > 4) { if (why) *why = "bad family"; return false; }
     if (!family_applicable(d, cfg.family, why)) return false;
     if (!in_domain(family_space(cfg.family), cfg, why)) return false;
     const int *gn = cfg.genes;
-    if (cfg.family == WPK_FAMILY_SIMT) {
+    if (cfg.family == WPK_FAMILY_SIMT || cfg.family == WPK_FAMILY_JIT) {
         long long threads = (long long)gn[0] * gn[1] * gn[2];
         if (threads < 1 || threads > 1024) {
             if (why) *why = "T_x*T_y*T_z must be in [1, 1024]";
             return false;
         }
-        if (d.elem() == 2 && gn[6] != 1) {   // 16-bit SIMT variants are instantiated with Tile_rz = 1 only
+        if (cfg.family == WPK_FAMILY_SIMT && d.elem() == 2 && gn[6] != 1) {   // 16-bit SIMT variants are instantiated with Tile_rz = 1 only
             if (why) *why = "Tile_rz must be 1 for 16-bit dtypes on the SIMT family";
             return false;
         }
@@ -300,7 +303,7 @@ int default_family(const ConvDesc &d) {
 Config default_config(const ConvDesc &d, int family) {
     Config c;
     c.family = family;
-    if (family == WPK_FAMILY_SIMT) {
+    if (family == WPK_FAMILY_SIMT || family == WPK_FAMILY_JIT) {
         int g[7] = {16, 4, 4, 1, 1, 1, 1};
         std::memcpy(c.genes, g, sizeof g);
         return c;
@@ -464,8 +467,40 @@ wpk_status wpk_conv2d_invalidate(wpk_plan plan) {
     return WPK_OK;
 }
 
+wpk_status wpk_jit_compile(wpk_plan plan, const int32_t *genes, size_t *cubin_bytes) {
+    if (!plan || !genes) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL argument");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    Config c;
+    c.family = WPK_FAMILY_JIT;
+    for (int g = 0; g < WPK_NUM_GENES; ++g) c.genes[g] = genes[g];
+    std::string why;
+    if (!config_valid(p->d, c, &why)) return fail(WPK_ERR_INVALID_CONFIG, "JIT config invalid: " + why);
+    size_t n = 0;
+    if (!jit_compile_only(p->d, c, &n, &why)) return fail(WPK_ERR_INTERNAL, why);
+    if (cubin_bytes) *cubin_bytes = n;
+    return WPK_OK;
+}
+
+wpk_status wpk_jit_set_cache_dir(const char *dir) {
+    jit_set_cache_dir(dir);
+    return WPK_OK;
+}
+
+wpk_status wpk_jit_stats(int64_t *compiles, int64_t *mem_hits, int64_t *disk_hits, int64_t *failures,
+                         double *compile_seconds) {
+    long long c, m, dh, f;
+    double s;
+    jit_stats(&c, &m, &dh, &f, &s);
+    if (compiles) *compiles = c;
+    if (mem_hits) *mem_hits = m;
+    if (disk_hits) *disk_hits = dh;
+    if (failures) *failures = f;
+    if (compile_seconds) *compile_seconds = s;
+    return WPK_OK;
+}
+
 wpk_status wpk_family_describe(int32_t family, int32_t *counts, int32_t *values, const char **names) {
-    if (family < 0 || family > 3 || !counts || !values) return fail(WPK_ERR_INVALID_ARGUMENT, "bad argument");
+    if (family < 0 || family > 4 || !counts || !values) return fail(WPK_ERR_INVALID_ARGUMENT, "bad argument");
     const Space &sp = family_space(family);
     for (int g = 0; g < WPK_NUM_GENES; ++g) {
         counts[g] = (int)sp.dom[g].size();

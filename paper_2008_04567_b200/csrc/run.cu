@@ -14,6 +14,7 @@
 #include "dwconv.h"
 #include "gemm32.h"
 #include "simt_conv.cuh"
+#include "jit.h"
 #include "umma_conv.h"
 #include "wpk_internal.h"
 
@@ -481,6 +482,24 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
         fn<<<grid, block, 0, st>>>(a);
         cudaError_t ce = cudaGetLastError();
         if (ce != cudaSuccess) { set_error(std::string("simt_conv launch: ") + cudaGetErrorString(ce)); return -1; }
+        return 1;
+    }
+    if (cfg.family == WPK_FAMILY_JIT) {   // NVRTC-specialised direct conv (compiled or cached)
+        const int *g = cfg.genes;
+        cudaKernel_t k;
+        std::string jerr;
+        if (!jit_kernel(d, cfg, p.device, &k, &jerr)) { set_error(jerr); return -1; }
+        const int tz = g[2] * g[5];
+        const int kblocks = (d.k + tz - 1) / tz;
+        dim3 block(g[0], g[1], g[2]);
+        dim3 grid((d.q + g[0] * g[3] - 1) / (g[0] * g[3]), (d.p + g[1] * g[4] - 1) / (g[1] * g[4]),
+                  (unsigned)(d.n * kblocks));
+        const void *xa = x, *wa = w, *ba = b, *za = z ? z : x;
+        void *ya = y;
+        void *args[] = {(void *)&xa, (void *)&wa, (void *)&ba, (void *)&ya, (void *)&za};
+        cudaError_t ce = cudaLaunchKernel((const void *)k, grid, block, args, 0, st);
+        if (ce == cudaSuccess) ce = cudaGetLastError();
+        if (ce != cudaSuccess) { set_error(std::string("jit_conv launch: ") + cudaGetErrorString(ce)); return -1; }
         return 1;
     }
     if (cfg.family == WPK_FAMILY_DW) {

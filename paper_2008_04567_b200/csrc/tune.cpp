@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "tune.h"
+#include "jit.h"
 
 namespace wpk {
 
@@ -257,6 +258,16 @@ std::vector<Config> TuneCtx::measure_batch(const std::vector<Config> &cfgs) {
     const int per = (n + world - 1) / world;
     // per rank: `per` fitness records + one flags record {idx -2, status = bit0 time-up | bit1 fatal}
     std::vector<Rec> send(per + 1), recv((size_t)(per + 1) * world);
+    if (o.eval_mode == WPK_EVAL_MEASURED && family == WPK_FAMILY_JIT && err == WPK_OK) {
+        // this rank's share of the generation is compiled on all host cores first
+        // (NVRTC, cached), then measured one by one on the GPU
+        std::vector<Config> mine;
+        for (int i = 0; i < per; ++i)
+            if (rank + i * world < n) mine.push_back(fresh[rank + i * world]);
+        const double c0 = wall_seconds();
+        jit_precompile(plan->d, mine, 0);
+        compile_seconds += wall_seconds() - c0;
+    }
     for (int i = 0; i < per; ++i) {
         int j = rank + i * world;
         if (j < n && err == WPK_OK) {
@@ -537,6 +548,9 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
         t.default_cfg = dc;
     }
     t.t_start = wall_seconds();
+    // the JIT family's cubins go to the tuning cache directory too, unless WPK_JIT_CACHE_DIR chose one
+    if (t.family == WPK_FAMILY_JIT && t.o.cache_dir && t.o.cache_dir[0] && !getenv("WPK_JIT_CACHE_DIR"))
+        jit_set_cache_dir(t.o.cache_dir);
     std::string cpath;
     if (t.o.cache_dir && t.o.cache_dir[0]) {
         cpath = std::string(t.o.cache_dir) + "/" + cache_key(*p, t.family, t.o.eval_mode == WPK_EVAL_MEASURED) + ".json";
@@ -558,6 +572,8 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
             p->measured = 0;
             p->rounds = 0;
             p->tune_seconds = wall_seconds() - t.t_start;
+    if (t.family == WPK_FAMILY_JIT)
+        log_line(t, "{\"jit_compile_seconds\": " + dbl(t.compile_seconds) + ", \"tune_seconds\": " + dbl(p->tune_seconds) + "}");
             return WPK_OK;
         }
     }
@@ -647,5 +663,7 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
     p->measured = (int)t.order.size();
     p->rounds = t.rounds;
     p->tune_seconds = wall_seconds() - t.t_start;
+    if (t.family == WPK_FAMILY_JIT)
+        log_line(t, "{\"jit_compile_seconds\": " + dbl(t.compile_seconds) + ", \"tune_seconds\": " + dbl(p->tune_seconds) + "}");
     return WPK_OK;
 }

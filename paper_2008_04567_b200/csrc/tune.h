@@ -32,6 +32,7 @@ struct TuneCtx {
     Config best;
     double best_beta = 1e300;
     int rounds = 0;
+    double compile_seconds = 0;         // JIT family: host NVRTC time spent inside this tune
     bool has_default = false;
     Config default_cfg;
 
