@@ -71,7 +71,7 @@ static Space make_space(int family) {
         sp.names = {"T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"};
     } else if (family == WPK_FAMILY_UMMA) {
         sp.dom = {{16, 32, 64, 96, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8}, {1, 2, 4, 8, 16},
-                  {0, 1, 2, 3}, {0, 1, 2, 3}, {1, 2, 4}, {128, 256}};
+                  {0, 1, 2, 3, 4, 5}, {0, 1, 2, 3}, {1, 2, 4}, {128, 256}};
         sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "MODE", "A_MODE", "ACC_STAGES", "BLOCK_M"};
     } else if (family == WPK_FAMILY_GEMM32) {
         sp.dom = {{64, 128}, {64, 128}, {8, 16}, {4, 8}, {1, 2, 4, 8}, {0}, {0}};
@@ -138,6 +138,10 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->splits = cfg.genes[2];
     g->raster = cfg.genes[3] & 1;
     g->pair = (cfg.genes[3] >> 1) & 1;   // tcgen05 CTA pair (cta_group::2): 256-row tiles over two SMs
+    // MODE bit 2: dual accumulators. Consecutive MMAs into one accumulator wait for its
+    // read-modify-write (~107 cycles for 128 x 128 x 16 vs 64 of tensor work, tools/mma_ring.cu);
+    // a 128-row tile alternates its K steps between two accumulators, summed by the epilogue
+    g->kdual = (cfg.genes[3] >> 2) & 1;
     g->ctas_per_sm = 1;
     g->a_mode = cfg.genes[4];
     g->acc_stages = cfg.genes[5];
@@ -190,6 +194,11 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->n_tiles = (d.k + g->bn - 1) / g->bn;
     g->work = (long long)g->m_tiles * g->n_tiles * g->splits;
     if (g->work >= 2147483647LL / 2) return no("too many work items (tiles x splits >= 2^30)");
+    if (g->kdual) {
+        if (g->pair || g->bm != 128) return no("dual accumulators are for 1-CTA 128-row tiles (MODE bit 2 with BLOCK_M 128, no pair)");
+        if (g->splits != 1) return no("dual accumulators need SPLIT_K = 1");
+        if (g->a_mode != 0) return no("dual accumulators are instantiated for the TMA A producer (A_MODE 0)");
+    }
     if (g->pair) {
         if (g->bm != 256) return no("a CTA pair computes 256-row tiles (BLOCK_M must be 256)");
         if (g->a_mode >= 2) return no("CTA pairs do not support the gather producers");
@@ -237,7 +246,7 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     off += 256;
     g->smem_bytes = 1024 /*align slack*/ + off;
     if (g->smem_bytes > smem_cap) return no("STAGES x tile exceeds shared memory");
-    int cols = g->acc_stages * (g->pair ? 1 : g->bm / 128) * g->bn;
+    int cols = g->acc_stages * (g->pair ? 1 : g->bm / 128) * g->bn * (g->kdual ? 2 : 1);
     int alloc = 32;
     while (alloc < cols) alloc <<= 1;
     g->tmem_cols = alloc;

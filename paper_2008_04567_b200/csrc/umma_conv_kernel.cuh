@@ -141,12 +141,80 @@ __device__ __forceinline__ void stage_and_store(EpiCtx &E, const UmmaArgs &a, co
     if (E.nbufs == 2) E.ebuf ^= 1;
 }
 
+// Final-output chunk of a dual-accumulator tile (MODE bit 2): 32 columns at a time, the two
+// accumulators (even K steps at taddr, odd at taddr + BN) summed in fp32, then bias, residual, ReLU and
+// one rounding as in epi_chunk_tma.
+template <typename T, bool RES>
+__device__ __forceinline__ void epi_chunk_tma_dual(EpiCtx &E, const UmmaArgs &a, const CUtensorMap *tmY, uint32_t taddr,
+                                                int k0, int mrow) {
+    constexpr int CW = 128 / sizeof(T);   // 64 (16-bit) or 32 (fp32) columns per chunk
+    uint32_t pk[32];
+#pragma unroll
+    for (int half = 0; half < CW / 32; ++half) {
+        uint32_t ra[32], rb[32];
+        ptx::tmem_ld32_nowait(taddr + half * 32, ra);
+        ptx::tmem_ld32_nowait(taddr + (uint32_t)a.bn + half * 32, rb);
+        uint4 zr[RES ? 4 : 1];   // this lane's row: 32 columns of the residual
+        if constexpr (RES) {
+            const long long m = (long long)mrow + E.lane;
+            const int kz = k0 + half * 32;
+            constexpr int EPV = 16 / sizeof(T);   // elements per 16-byte vector
+            const uint4 *zp = reinterpret_cast<const uint4 *>(static_cast<const T *>(a.z) + m * a.K + kz);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                zr[j] = (m < a.M && kz + (j + 1) * EPV <= a.K && (sizeof(T) == 2 || j < 32 / EPV)) ? __ldg(zp + j)
+                                                                                                : make_uint4(0u, 0u, 0u, 0u);
+        }
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            float v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = __uint_as_float(ra[4 * q + j]) + __uint_as_float(rb[4 * q + j]);
+            bias_relu4(v, E.sBias, k0 + half * 32 + 4 * q, false);
+            if constexpr (RES) {
+                if constexpr (sizeof(T) == 2) {   // 4 16-bit residual values = half of zr[q / 2]
+                    const uint32_t lo = (q & 1) ? zr[q >> 1].z : zr[q >> 1].x, hi = (q & 1) ? zr[q >> 1].w : zr[q >> 1].y;
+                    v[0] += to_f2(lo, 0, (T *)nullptr); v[1] += to_f2(lo, 1, (T *)nullptr);
+                    v[2] += to_f2(hi, 0, (T *)nullptr); v[3] += to_f2(hi, 1, (T *)nullptr);
+                } else {
+                    // fp32: 32 columns = 8 vectors, but zr holds 4 (the first 16 columns); reload the rest
+                    const long long m = (long long)mrow + E.lane;
+                    const int kk = k0 + half * 32 + 4 * q;
+                    const uint4 z4 = (q < 4) ? zr[q]
+                                             : ((m < a.M && kk + 4 <= a.K)
+                                                    ? __ldg(reinterpret_cast<const uint4 *>(static_cast<const T *>(a.z) + m * a.K + kk))
+                                                    : make_uint4(0u, 0u, 0u, 0u));
+                    v[0] += __uint_as_float(z4.x); v[1] += __uint_as_float(z4.y);
+                    v[2] += __uint_as_float(z4.z); v[3] += __uint_as_float(z4.w);
+                }
+            }
+            if (a.epilogue >= 2) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = fmaxf(v[j], 0.f);
+            }
+            if constexpr (sizeof(T) == 2) {
+                pk[half * 16 + 2 * q] = pack2(v[0], v[1], (T *)nullptr);
+                pk[half * 16 + 2 * q + 1] = pack2(v[2], v[3], (T *)nullptr);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) pk[4 * q + j] = __float_as_uint(v[j]);
+            }
+        }
+    }
+    stage_and_store<true>(E, a, tmY, pk, k0, mrow, 0);
+}
+
 // One 32-row x 128-byte chunk through smem + TMA store. FINAL: +bias, ReLU, RN-round to T (64
 // columns for 16-bit T, 32 for fp32); else fp32 split-K partials (32 columns) into [split][M][K].
-template <typename T, bool FINAL, bool RES = false>
+template <typename T, bool FINAL, bool RES = false, bool DUAL = false>
 __device__ __forceinline__ void epi_chunk_tma(EpiCtx &E, const UmmaArgs &a, const CUtensorMap *tmY, uint32_t taddr,
                                               int k0, int mrow, int split) {
     constexpr bool k16 = FINAL && sizeof(T) == 2;
+    if constexpr (FINAL && DUAL) {   // dual accumulators: (even K steps at taddr) + (odd at taddr + BN)
+        epi_chunk_tma_dual<T, RES>(E, a, tmY, taddr, k0, mrow);
+        return;
+    }
     uint32_t raw[k16 ? 64 : 32];
     ptx::tmem_ld32_nowait(taddr, raw);
     if constexpr (k16) ptx::tmem_ld32_nowait(taddr + 32, raw + 32);
@@ -469,11 +537,17 @@ __device__ __forceinline__ void epi_chunk_csplit(EpiCtx &E, const UmmaArgs &a, c
 }
 
 // Direct-store epilogue for one 32-row x 16-column chunk (NCHW output, unaligned K, partials).
-template <typename T>
+template <typename T, bool DUAL = false>
 __device__ __noinline__ void epi_chunk_direct(const UmmaArgs &a, const float *sBias, uint32_t taddr, int k0,
                                               long long m, int split, bool final_out) {
     float v[16];
     ptx::tmem_ld16(taddr, v);
+    if constexpr (DUAL) {   // dual accumulators: + the odd K steps' accumulator, BN columns further
+        float v2[16];
+        ptx::tmem_ld16(taddr + (uint32_t)a.bn, v2);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += v2[j];
+    }
     if (m >= a.M) return;
     const bool full16 = (k0 + 16 <= a.K);
     if (!final_out) {
@@ -843,7 +917,7 @@ __device__ __forceinline__ void prefetch_a_rows(const UmmaArgs &a, long long m0,
 // 12 warps (16 with gather producers): 0 = A producer, 1 = TMEM allocator + MMA issuer,
 // 2 = B producer, 3 = spare, 4..11 = epilogue (two groups of four; warp w reads TMEM lanes
 // [32*(w%4), +32)), 12..15 = gather producers.
-template <int DT, int AK, int EK, bool RES = false>
+template <int DT, int AK, int EK, bool RES = false, bool DUAL = false>
 __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
     umma_conv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmP,
@@ -1040,11 +1114,16 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (single thread; the leader CTA of a pair) =====================
-        if (lane == 0 && leader) {
+#ifdef WPK_MMA_LANE0
+        constexpr bool kConv = false;   // A/B experiment: the old single-lane issue loop
+#else
+        constexpr bool kConv = true;    // the whole warp runs the loop; elect_one() issues
+#endif
+        if (leader && (kConv || lane == 0)) {
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
             const uint64_t a_desc0 = ptx::sw128_kmajor_desc(ptx::smem_u32(smA));
             const uint64_t b_desc0 = ptx::sw128_kmajor_desc(ptx::smem_u32(smB));
-            const uint32_t acc_cols = (uint32_t)(nsub * a.bn);
+            const uint32_t acc_cols = (uint32_t)(nsub * a.bn * (DUAL ? 2 : 1));
             for (long long w = wstart; w < a.work; w += wstep) {
                 const WorkPos wp = decode_work(w, a);
                 const int kb0 = wp.split * a.kb_per_split;
@@ -1054,32 +1133,59 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 const long long dit = (w - wstart) / wstep;     // debug: per-tile events of the first 8 tiles
                 if (dbg && dit < 8 && !(WPK_DBG_FLAGS(a) & 8)) dbg[16 + dit * 6 + 0] = ptx::globaltimer();
                 const uint32_t d_tmem = tmem_base + acc * acc_cols;
+                const bool cyc = dbg && (WPK_DBG_FLAGS(a) & 128) && w == wstart;   // cycle accounting, first tile
+                long long c_wait = 0, c_issue = 0, c_t0 = cyc ? clock64() : 0, c1 = 0;
                 for (int kb = kb0; kb < kb1; ++kb) {
+                    const long long c0 = cyc ? clock64() : 0;
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
+                    if (cyc) {
+                        c1 = clock64();
+                        c_wait += c1 - c0;
+                    }
                     if (dbg && w == wstart && kb == kb0) dbg[2] = ptx::globaltimer();
                     if (dbg && dit < 8 && kb == kb0 && !(WPK_DBG_FLAGS(a) & 8)) dbg[16 + dit * 6 + 1] = ptx::globaltimer();
                     if (dbg && (WPK_DBG_FLAGS(a) & 8) && w == wstart && kb - kb0 < 16) dbg[48 + (kb - kb0)] = ptx::globaltimer();
                     const uint64_t ad = a_desc0 + (uint64_t)((stage * a_bytes) >> 4);
                     const uint64_t bd = b_desc0 + (uint64_t)((stage * b_bytes) >> 4);
+                    if (!kConv || ptx::elect_one()) {
                     if constexpr (kPair) {
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
                             ptx::umma2<kTF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
                         ptx::umma_commit2_multicast(&empty[stage]);   // frees the stage in both CTAs
                     } else {
-                        for (int h = 0; h < nsub; ++h) {
+                        if constexpr (DUAL) {   // even K steps -> accumulator 0, odd -> accumulator 1 (BN columns on)
 #pragma unroll
-                            for (int kk = 0; kk < 4; ++kk)   // 4 x 32 bytes of K per 128-byte stage (+2 desc units)
-                                ptx::umma<kTF32>(d_tmem + h * a.bn, ad + h * (16384 >> 4) + 2 * kk, bd + 2 * kk, a.idesc,
-                                                 (kb > kb0 || kk > 0) ? 1u : 0u);
+                            for (int kk = 0; kk < 4; ++kk)
+                                ptx::umma<kTF32>(d_tmem + (kk & 1) * a.bn, ad + 2 * kk, bd + 2 * kk, a.idesc,
+                                                 (kb > kb0 || kk > 1) ? 1u : 0u);
+                        } else {
+                            for (int h = 0; h < nsub; ++h) {
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk)   // 4 x 32 bytes of K per 128-byte stage (+2 desc units)
+                                    ptx::umma<kTF32>(d_tmem + h * a.bn, ad + h * (16384 >> 4) + 2 * kk, bd + 2 * kk, a.idesc,
+                                                     (kb > kb0 || kk > 0) ? 1u : 0u);
+                            }
                         }
                         ptx::umma_commit(&empty[stage]);   // frees this smem stage when the MMAs finish
                     }
+                    }
+                    if (kConv) __syncwarp();
+                    if (cyc) c_issue += clock64() - c1;
                     if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
                 }
-                if constexpr (kPair) ptx::umma_commit2_multicast(&tfull[acc]);   // both CTAs' halves ready
-                else ptx::umma_commit(&tfull[acc]);                               // accumulator ready
+                if (cyc && lane == 0) {
+                    dbg[60] = (unsigned long long)c_wait;
+                    dbg[61] = (unsigned long long)c_issue;
+                    dbg[62] = (unsigned long long)(clock64() - c_t0);
+                    dbg[63] = (unsigned long long)(kb1 - kb0);
+                }
+                if (!kConv || ptx::elect_one()) {
+                    if constexpr (kPair) ptx::umma_commit2_multicast(&tfull[acc]);   // both CTAs' halves ready
+                    else ptx::umma_commit(&tfull[acc]);                               // accumulator ready
+                }
+                if (kConv) __syncwarp();
                 if (dbg && w == wstart) dbg[3] = ptx::globaltimer();
                 if (dbg && dit < 8 && !(WPK_DBG_FLAGS(a) & 8)) dbg[16 + dit * 6 + 2] = ptx::globaltimer();
                 if (dbg && dit < 8 && (WPK_DBG_FLAGS(a) & 4) && !(WPK_DBG_FLAGS(a) & 8)) {   // experiment: MMA completion seen by a spinning thread
@@ -1104,7 +1210,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
         const int grp = (warp - 4) >> 2;       // 0 or 1
         uint32_t acc = 0, acc_phase = 0;
         EpiCtx E{sBias, sEpi + (size_t)(warp - 4) * a.epi_bufs * 4096, 0u, lane, a.epi_bufs};
-        const uint32_t acc_cols = (uint32_t)(nsub * a.bn);
+        const uint32_t acc_cols = (uint32_t)(nsub * a.bn * (DUAL ? 2 : 1));
         constexpr int cwf = (EK == EK_DIRECT) ? 16 : (int)(128 / sizeof(T));   // final-output chunk width
         constexpr int cwp = (EK == EK_DIRECT) ? 16 : 32;                        // fp32-partial chunk width
         for (long long w = wstart; w < a.work; w += wstep) {
@@ -1204,11 +1310,11 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                     const int k0 = n0 + c0;
                     if (k0 >= a.K) break;   // warp-uniform
                     if constexpr (EK == EK_TMA) {
-                        epi_chunk_tma<T, true, RES>(E, a, &tmY, tbase + c0, k0, mrow, 0);
+                        epi_chunk_tma<T, true, RES, DUAL>(E, a, &tmY, tbase + c0, k0, mrow, 0);
                     } else if constexpr (EK == EK_SPLIT) {
                         epi_chunk_tma<T, false>(E, a, &tmP, tbase + c0, k0, mrow, wp.split);   // (owner: above)
                     } else {
-                        epi_chunk_direct<T>(a, sBias, tbase + c0, k0, (long long)mrow + lane, wp.split, a.splits == 1);
+                        epi_chunk_direct<T, DUAL>(a, sBias, tbase + c0, k0, (long long)mrow + lane, wp.split, a.splits == 1);
                     }
                 }
             }
@@ -1257,7 +1363,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
 }
 
 // ---- launch of one (dtype) instantiation family -----------------------------------------------
-template <int DT, int AK, int EK, bool RES = false>
+template <int DT, int AK, int EK, bool RES = false, bool DUAL = false>
 static cudaError_t launch_variant(cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                                   const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
     // the shared-memory opt-in is per device context: remember it per device (bit d), so a plan
@@ -1267,25 +1373,34 @@ static cudaError_t launch_variant(cudaLaunchConfig_t &lc, const CUtensorMap &tmA
     if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(attr_done.load(std::memory_order_acquire) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK, RES, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e != cudaSuccess) return e;
         // one shared-memory carveout for every variant and config: consecutive convs whose dynamic
         // smem differs would otherwise get different L1/smem splits, and an SM can only switch
         // carveout once drained -- no overlap of one conv's tail with the next conv's CTAs
         if (!getenv("WPK_NO_CARVEOUT")) {
-            e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK, RES>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            e = cudaFuncSetAttribute(umma_conv_kernel<DT, AK, EK, RES, DUAL>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      (int)cudaSharedmemCarveoutMaxShared);
             if (e != cudaSuccess) return e;
         }
         attr_done.fetch_or(bit, std::memory_order_acq_rel);
     }
-    return cudaLaunchKernelEx(&lc, umma_conv_kernel<DT, AK, EK, RES>, tmA, tmB, tmY, tmP, a);
+    return cudaLaunchKernelEx(&lc, umma_conv_kernel<DT, AK, EK, RES, DUAL>, tmA, tmB, tmY, tmP, a);
 }
 
 template <int DT, int AK>
 static cudaError_t launch_ak(int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                              const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
+    if constexpr (AK == AK_TMA) {   // dual accumulators (MODE bit 2): TMA A producer only (plan validation)
+        if (a.kdual) {
+            if (ek == EK_TMA)
+                return a.epilogue == 3 ? launch_variant<DT, AK, EK_TMA, true, true>(lc, tmA, tmB, tmY, tmP, a)
+                                       : launch_variant<DT, AK, EK_TMA, false, true>(lc, tmA, tmB, tmY, tmP, a);
+            if (ek == EK_DIRECT) return launch_variant<DT, AK, EK_DIRECT, false, true>(lc, tmA, tmB, tmY, tmP, a);
+            return cudaErrorInvalidConfiguration;
+        }
+    }
     if (ek == EK_TMA)
         return a.epilogue == 3 ? launch_variant<DT, AK, EK_TMA, true>(lc, tmA, tmB, tmY, tmP, a)
                                : launch_variant<DT, AK, EK_TMA, false>(lc, tmA, tmB, tmY, tmP, a);

@@ -14,7 +14,7 @@ import oracle
 import workloads
 from workloads import ConvLayer
 
-from _util import TOL, assert_bit_exact, oracle_full, rel_error, run_product
+from _util import TOL, assert_bit_exact, from_layout, oracle_full, rel_error, run_product, to_layout
 
 pytestmark = pytest.mark.gpu
 
@@ -68,7 +68,7 @@ def test_epilogues(dtype, epilogue):
 def _umma_space():
     bns = [16, 32, 64, 96, 128, 192, 256]
     out = []
-    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1, 2, 3], [0, 1, 2],
+    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1, 2, 3, 4, 5], [0, 1, 2],
                                                           [1, 2, 4], [128, 256]):
         out.append((bn, st, sp, ra, amode, acc, bm))
     return out
@@ -505,3 +505,35 @@ def test_random_shapes_random_configs(case):
         y = plan.run(xl, wl, bc)
         torch.cuda.synchronize()
         assert_bit_exact(from_layout(y.cpu(), layout), ref)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16", "tf32"])
+@pytest.mark.parametrize("layout", ["nhwc", "nchw"])
+def test_umma_dual_accumulators(dtype, layout):
+    """MODE bit 2 (two accumulators per 128-row tile, even / odd K steps, summed by the epilogue):
+    bit-exact on exact-integer inputs through the TMA-store and the direct (NCHW) epilogues, within
+    tolerance on uniform inputs, and with the residual epilogue."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    import oracle
+    L = ConvLayer("dual", 3, 128, 14, 14, 192, 3, 3, 1, 1)
+    for mode in ["int", "uniform"]:
+        x, w, b = workloads.generate(L, dtype, mode, seed=31)
+        ref = oracle_full(L, x, w, b)
+        for genes in ([128, 4, 1, 4, 0, 2, 128], [64, 5, 1, 5, 0, 1, 128], [192, 3, 1, 4, 0, 1, 128]):
+            y, plan = run_product(L, dtype, layout, x, w, b, config=(1, genes))
+            assert plan.config[1][3] == genes[3]
+            if mode == "int":
+                assert_bit_exact(y, ref)
+            else:
+                assert rel_error(dtype, y, ref) <= TOL[dtype]
+    # residual epilogue through the dual variant
+    x, w, b = workloads.generate(L, dtype, "int", seed=32)
+    z = torch.randint(-3, 4, (L.n, L.k, 14, 14)).to(x.dtype)
+    plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout=layout, dtype=dtype,
+                      epilogue="bias_add_relu")
+    plan.set_config(1, [128, 4, 1, 4, 0, 2, 128])
+    xl, wl = to_layout(x, w, layout)
+    zl = z.permute(0, 2, 3, 1).contiguous() if layout == "nhwc" else z
+    yd = plan.run(xl.cuda(), wl.cuda(), b.cuda(), z=zl.cuda())
+    torch.cuda.synchronize()
+    assert_bit_exact(from_layout(yd.cpu(), layout), oracle.conv2d(x, w, b, stride=1, pad=1, residual=z))
