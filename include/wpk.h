@@ -122,7 +122,12 @@ typedef struct {
     void *exchange_ctx;
     int32_t warmup, reps;     /* timing protocol: W untimed + R reps (1..1024) bracketed by device
                                  globaltimer stamps, interquartile mean (defaults 3, 11) */
-    int32_t l2_flush;         /* 1: overwrite a >= 2x L2 buffer before every timed rep (default) */
+    int32_t l2_flush;         /* cache policy of a timed rep: 0 = warm (back-to-back single launches),
+                               * 1 = read a 2x-L2 buffer before each single-launch rep, 2 (default) = one
+                               * rep is a CUDA graph of P back-to-back launches over P copies of x / y
+                               * with P x (|x| + |y|) >= 2 x L2 (every launch reads cold inputs; the
+                               * stamps, ~2-us steps on this part, span P launches; consecutive
+                               * launches overlap through PDL as in a network step), beta = span / P */
     int32_t eval_mode;        /* wpk_eval_mode (default MEASURED)                               */
     int32_t family;           /* wpk_family to search; WPK_FAMILY_AUTO = the plan's default      */
     const char *record_path;  /* if set: append every measured record as JSONL (with world > 1
@@ -183,7 +188,8 @@ WPK_API wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t bud
 
 /* Time the plan's current config with the tuner's protocol (the fitness measurement of a candidate,
  * PAPER.md:68): `warmup` untimed runs, then `reps` runs each bracketed by device %globaltimer
- * stamps (L2 evicted before each when l2_flush != 0), interquartile mean in microseconds -> *us.
+ * stamps under the cache policy l2_flush (0 / 1 / 2, see wpk_tune_options), interquartile mean in
+ * microseconds -> *us.
  * Uses its own synthetic buffers and stream, synchronises; WPK_ERR_CUDA if the launch fails. */
 WPK_API wpk_status wpk_conv2d_measure(wpk_plan plan, int32_t warmup, int32_t reps, int32_t l2_flush, double *us);
 

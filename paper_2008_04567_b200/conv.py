@@ -218,10 +218,13 @@ class Conv2dPlan:
         self._ws_bytes = -1
         return self.tune_stats()
 
-    def measure(self, warmup: int = 3, reps: int = 11, l2_flush: bool = True) -> float:
-        """Microseconds of the current config under the tuner's timing protocol (wpk_conv2d_measure)."""
+    def measure(self, warmup: int = 3, reps: int = 11, l2_flush: int | bool = 2) -> float:
+        """Microseconds of the current config under the tuner's timing protocol (wpk_conv2d_measure).
+        l2_flush: 2 (default) rotating cold buffer copies in one graph per rep, 1 flush before each
+        single launch, 0 warm; True means 2, False 0."""
+        mode = (2 if l2_flush else 0) if isinstance(l2_flush, bool) else int(l2_flush)
         us = ctypes.c_double()
-        L.check(self.lib.wpk_conv2d_measure(self.handle, int(warmup), int(reps), int(bool(l2_flush)), ctypes.byref(us)))
+        L.check(self.lib.wpk_conv2d_measure(self.handle, int(warmup), int(reps), mode, ctypes.byref(us)))
         return us.value
 
     def tune_stats(self) -> TuneResult:

@@ -387,7 +387,7 @@ void wpk_tune_options_init(wpk_tune_options *o) {
     o->world = 1;
     o->warmup = 3;
     o->reps = 11;
-    o->l2_flush = 1;
+    o->l2_flush = 2;
     o->eval_mode = WPK_EVAL_MEASURED;
     o->family = WPK_FAMILY_AUTO;
     o->ga_pop = 48; o->ga_elites = 4; o->ga_pool = 48; o->ga_max_gen = 50;

@@ -64,6 +64,11 @@ void log_line(TuneCtx &t, const std::string &s) {
 struct GpuBench {
     cudaStream_t st = nullptr;
     void *x = nullptr, *w = nullptr, *b = nullptr, *y = nullptr, *z = nullptr, *ws = nullptr, *flush = nullptr;
+    // rotating mode (l2_flush == 2): P copies of x and y, one timed rep = one CUDA graph of P
+    // back-to-back convs over all copies, so every launch reads an input last touched P launches ago
+    // (P x footprint >= 2 x L2: cold) and one stamp pair spans P launches (the device timestamps
+    // advance in ~2-us steps here, as coarse as a small layer)
+    std::vector<void *> xr, yr;
     unsigned long long *stamps = nullptr;   // [2 * reps] device timestamps
     size_t ws_bytes = 0, flush_bytes = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -100,7 +105,32 @@ struct GpuBench {
         err = std::string(m) + ": " + cudaGetErrorString(e);
         return false;
     }
+    bool init_rotation(Plan &p) {   // lazily, on the first rotating measurement
+        if (!xr.empty()) return true;
+        const ConvDesc &d = p.d;
+        const size_t e = d.elem();
+        const size_t xb = (size_t)d.n * d.c * d.h * d.w * e, yb = (size_t)d.M() * d.k * e;
+        const size_t foot = xb + yb;
+        size_t P = (2 * (size_t)device_l2_bytes(p.device) + foot - 1) / foot;
+        P = std::max<size_t>(2, std::min<size_t>(P, 64));
+        while (P > 2 && P * foot > ((size_t)3 << 30)) --P;   // <= 3 GB of copies
+        for (size_t i = 0; i < P; ++i) {
+            void *xx = nullptr, *yy = nullptr;
+            if (cudaMalloc(&xx, xb) || cudaMalloc(&yy, yb)) {
+                if (xx) cudaFree(xx);
+                cudaGetLastError();
+                break;
+            }
+            cudaMemcpyAsync(xx, x, xb, cudaMemcpyDeviceToDevice, st);
+            xr.push_back(xx);
+            yr.push_back(yy);
+        }
+        if (xr.size() < 2) return fail_("cudaMalloc of the rotating buffers");
+        return cudaStreamSynchronize(st) == cudaSuccess;
+    }
     ~GpuBench() {
+        for (void *ptr : xr) cudaFree(ptr);
+        for (void *ptr : yr) cudaFree(ptr);
         for (void *ptr : {x, w, b, y, z, ws, flush, (void *)stamps})
             if (ptr) cudaFree(ptr);
         if (e0) cudaEventDestroy(e0);
@@ -117,8 +147,57 @@ struct GpuBench {
             if (wall_seconds() - t0 > seconds) { err = "candidate exceeded the watchdog deadline"; return false; }
         }
     }
+    // Rotating mode: microseconds per conv of a graph of P back-to-back convs on P cold buffer copies
+    // (interquartile mean over reps), the graph's kernels overlapping through PDL as in a network step.
+    double measure_rotating(Plan &p, const Config &cfg, int warmup, int reps, bool *fatal) {
+        if (!init_rotation(p)) { *fatal = true; return INFINITY; }
+        const size_t P = xr.size();
+        for (int i = 0; i < std::max(1, warmup); ++i)   // eager: weight packing, workspace state, first-use maps
+            if (launch_conv(p, cfg, xr[i % P], w, b, yr[i % P], st, (char *)ws, ws_bytes, z) < 0) return INFINITY;
+        if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { *fatal = true; return INFINITY; }
+        bool ok = true;
+        for (size_t i = 0; i < P && ok; ++i)
+            ok = launch_conv(p, cfg, xr[i], w, b, yr[i], st, (char *)ws, ws_bytes, z) >= 0;
+        if (cudaStreamEndCapture(st, &g) != cudaSuccess || !ok || !g) {
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            return INFINITY;
+        }
+        if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) {
+            cudaGraphDestroy(g);
+            cudaGetLastError();
+            return INFINITY;
+        }
+        cudaGraphDestroy(g);
+        std::vector<unsigned long long> hs(2 * (size_t)reps);
+        cudaGraphLaunch(ge, st);   // one untimed pass of the graph
+        for (int i = 0; i < reps; ++i) {
+            timestamp_device(stamps + 2 * i, st);
+            cudaGraphLaunch(ge, st);
+            timestamp_device(stamps + 2 * i + 1, st);
+        }
+        const bool done = sync_with_deadline(30.0);
+        cudaGraphExecDestroy(ge);
+        if (!done || cudaMemcpy(hs.data(), stamps, hs.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            *fatal = true;
+            return INFINITY;
+        }
+        std::vector<double> t;
+        for (int i = 0; i < reps; ++i) t.push_back((double)(hs[2 * i + 1] - hs[2 * i]) * 1e-3 / (double)P);
+        std::sort(t.begin(), t.end());
+        const size_t lo = t.size() / 4, hi = t.size() - t.size() / 4;
+        double sum = 0;
+        for (size_t i = lo; i < hi; ++i) sum += t[i];
+        return sum / (double)(hi - lo);
+    }
     // Returns the median microseconds, +inf on a recoverable failure; sets *fatal on a sticky error.
-    double measure(Plan &p, const Config &cfg, int warmup, int reps, bool l2flush, bool *fatal) {
+    // l2mode: 0 warm (no eviction), 1 read-flush of a 2 x L2 buffer before each single-launch rep,
+    // 2 rotating cold buffers (measure_rotating).
+    double measure(Plan &p, const Config &cfg, int warmup, int reps, int l2mode, bool *fatal) {
+        const bool l2flush = (l2mode == 1);
         size_t need = workspace_bytes(p, cfg, false);
         if (need > ws_bytes) {
             if (ws) cudaFree(ws);
@@ -128,6 +207,7 @@ struct GpuBench {
             ws_bytes = need;
         }
         p.reset_ws_state();
+        if (l2mode == 2) return measure_rotating(p, cfg, warmup, reps, fatal);
         for (int i = 0; i < warmup; ++i)
             if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes, z) < 0) return INFINITY;
         if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
@@ -235,7 +315,7 @@ static double evaluate_one(TuneCtx &t, const Config &c, int32_t *status) {
     }
     default: {
         bool fatal = false;
-        double b = t.gb->measure(*t.plan, c, t.o.warmup, t.o.reps, t.o.l2_flush != 0, &fatal);
+        double b = t.gb->measure(*t.plan, c, t.o.warmup, t.o.reps, t.o.l2_flush, &fatal);
         if (fatal) { t.err = WPK_ERR_CUDA; set_error("tune: " + t.gb->err); *status = 3; }
         else if (!std::isfinite(b)) *status = 4;
         return b;
@@ -513,7 +593,7 @@ extern "C" wpk_status wpk_conv2d_measure(wpk_plan plan, int32_t warmup, int32_t 
     if (!gb.init(*p)) return fail(WPK_ERR_CUDA, "measure: " + gb.err);
     bool fatal = false;
     const Config cfg = p->cfg;
-    *us = gb.measure(*p, cfg, warmup, reps, l2_flush != 0, &fatal);
+    *us = gb.measure(*p, cfg, warmup, reps, l2_flush, &fatal);
     p->reset_ws_state();   // the measurement ran on its own workspace
     if (fatal) return fail(WPK_ERR_CUDA, "measure: " + gb.err);
     if (!std::isfinite(*us)) return fail(WPK_ERR_CUDA, "measure: the launch failed: " + std::string(wpk_last_error()));
@@ -615,7 +695,7 @@ extern "C" wpk_status wpk_conv2d_tune(wpk_plan plan, wpk_search search, int32_t 
         std::vector<Rec> mine(k), all((size_t)k * world);
         for (int i = 0; i < k; ++i) {
             bool fatal = false;
-            double b = (t.err == WPK_OK) ? gb.measure(*p, fin[i], t.o.warmup, t.o.reps, t.o.l2_flush != 0, &fatal) : INFINITY;
+            double b = (t.err == WPK_OK) ? gb.measure(*p, fin[i], t.o.warmup, t.o.reps, t.o.l2_flush, &fatal) : INFINITY;
             if (fatal && t.err == WPK_OK) { t.err = WPK_ERR_CUDA; set_error("tune: " + gb.err); }
             mine[i] = Rec{i, (fatal || t.err != WPK_OK) ? 3 : 0, b};
         }

@@ -2,8 +2,9 @@
 kernel and a third-party implementation -- here the same box's cuDNN reached through torch
 (BASELINE.json north_star). Ties go to the own kernel (reading c25).
 
-The timing protocol is the one the tuner uses: W warm-ups, then R CUDA-event-timed
-reps with an L2 flush before each, median. The C library never sees torch: the choice lives here,
+The timing protocol is the one the tuner uses (wpk_tune_options.l2_flush = 2): W
+warm-ups, then R reps, each one CUDA graph of P calls on P cold copies of the input between CUDA
+events, interquartile mean of span / P. The C library never sees torch: the choice lives here,
 in SelectedConv2d, which persists it next to the tuning cache and dispatches each call to it.
 """
 from __future__ import annotations
@@ -51,6 +52,50 @@ def time_fn(fn, warmup: int = 3, reps: int = 11, flush: bool = True, stream=None
             e1.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e3)
     return statistics.median(ts)
+
+
+def rotating_copies(t: torch.Tensor, other_bytes: int = 0, cap: int = 64) -> list:
+    """P copies of t (the first is t itself) with P * (|t| + other_bytes) >= 2 x L2, <= cap, <= 3 GB:
+    a graph that cycles through them reads every input cold."""
+    l2 = getattr(torch.cuda.get_device_properties(t.device), "L2_cache_size", 126 << 20)
+    foot = t.numel() * t.element_size() + other_bytes
+    p = max(2, min(cap, -(-2 * l2 // max(foot, 1))))
+    while p > 2 and p * foot > (3 << 30):
+        p -= 1
+    return [t] + [t.clone() for _ in range(p - 1)]
+
+
+def time_rotating(fns, warmup: int = 3, reps: int = 11, stream=None) -> float:
+    """Microseconds per call: the P callables (each bound to its own cold input copy) are captured in
+    one CUDA graph, replayed `reps` times between CUDA events; interquartile mean of span / P. The
+    same protocol as the tuner's (wpk_tune_options.l2_flush = 2): the events' ~2-us steps are spread
+    over P calls, and consecutive calls overlap as in a network step."""
+    stream = stream or torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, warmup)):
+            for f in fns:
+                f()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for f in fns:
+            f()
+    torch.cuda.synchronize()
+    ts = []
+    with torch.cuda.stream(stream):
+        g.replay()
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3 / len(fns))
+    del g
+    ts.sort()
+    lo, hi = len(ts) // 4, len(ts) - len(ts) // 4
+    return sum(ts[lo:hi]) / (hi - lo)
 
 
 def cudnn_conv_fn(x, w, b, stride, pad, dil, groups, layout, dtype, fused: bool, z=None, epilogue="bias_relu"):
@@ -109,15 +154,18 @@ _VARIANT_NAMES = {("bias_relu", True): "cudnn_convolution_relu", ("bias_relu", F
 
 
 def select(plan, x, w, b, y, stride, pad, dil, groups, warmup=3, reps=11, z=None) -> Selection:
-    """Time the plan's current config and both cuDNN variants; pick the argmin (ties -> wpk)."""
-    own = time_fn(lambda: plan.run(x, w, b, y, z=z), warmup, reps)
+    """Time the plan's current config and both cuDNN variants with the same protocol (time_rotating:
+    a graph over cold input copies); pick the argmin (ties -> wpk)."""
+    xs = rotating_copies(x, y.numel() * y.element_size())
+    ys = [y] + [torch.empty_like(y) for _ in xs[1:]]
+    own = time_rotating([lambda i=i: plan.run(xs[i], w, b, ys[i], z=z) for i in range(len(xs))], warmup, reps)
     best, variant = float("inf"), "none"
     for fused in (False, True):
         try:
-            f = cudnn_conv_fn(x, w, b, stride, pad, dil, groups, plan.layout, plan.dtype, fused, z=z,
-                              epilogue=plan.epilogue)
-            f()
-            t = time_fn(f, warmup, reps)
+            fns = [cudnn_conv_fn(xi, w, b, stride, pad, dil, groups, plan.layout, plan.dtype, fused, z=z,
+                                 epilogue=plan.epilogue) for xi in xs]
+            fns[0]()
+            t = time_rotating(fns, warmup, reps)
         except (RuntimeError, TypeError):
             continue
         if t < best:
