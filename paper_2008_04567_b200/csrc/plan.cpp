@@ -71,7 +71,7 @@ static Space make_space(int family) {
         sp.names = {"T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"};
     } else if (family == WPK_FAMILY_UMMA) {
         sp.dom = {{16, 32, 64, 96, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8}, {1, 2, 4, 8, 16},
-                  {0, 1, 2, 3, 4, 5}, {0, 1, 2, 3}, {1, 2, 4}, {128, 256}};
+                  {0, 1, 2, 3, 4, 5}, {0, 1, 2, 3, 4}, {1, 2, 4}, {128, 256}};
         sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "MODE", "A_MODE", "ACC_STAGES", "BLOCK_M"};
     } else if (family == WPK_FAMILY_GEMM32) {
         sp.dom = {{64, 128}, {64, 128}, {8, 16}, {4, 8}, {1, 2, 4, 8}, {0}, {0}};
@@ -144,6 +144,13 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->kdual = (cfg.genes[3] >> 2) & 1;
     g->ctas_per_sm = 1;
     g->a_mode = cfg.genes[4];
+    // A_MODE 4: the TMA producer of A_MODE 0 with its K blocks dealt round robin over three
+    // producer warps (A and B boxes of a stage from one thread) instead of an A / B warp split
+    g->prod_rr = 0;
+    if (g->a_mode == 4) {
+        g->a_mode = 0;
+        g->prod_rr = 1;
+    }
     g->acc_stages = cfg.genes[5];
     g->seg_sp = 0; g->seg_hp = 0; g->seg_wp = 0; g->seg_fast = 0; g->seg_two = 0;
     if ((g->a_mode == 1 || g->a_mode == 2) && d.c >= 64)

@@ -189,6 +189,7 @@ launch:
     a.a_mode = g.a_mode; a.seg_sp = g.seg_sp; a.seg_fast = g.seg_fast; a.seg_two = g.seg_two;
     a.kpad_bias = (L.K + 255) / 256 * 256;
     a.kdual = g.kdual;
+    a.prod_rr = (g.prod_rr && !a_split) ? 1 : 0;
     {
         const long long stage_bytes = g.pair ? 128LL * 128 + (long long)(g.bn / 2) * 128 : (long long)g.bm * 128 + (long long)g.bn * 128;
         const long long slab = (long long)(g.splits - 1) * (g.pair ? 128 : g.bm) * g.bn * 4;

@@ -968,7 +968,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
         if (EK == EK_SPLIT) ptx::prefetch_tmap(&tmP);
         for (int s = 0; s < a.stages; ++s) {
             // A (TMA: 1 or 2 issuing threads; or 4 gather warps) + B producer
-            ptx::mbar_init(&full[s], kGather ? 5 : (a.a_split ? 3 : 2));
+            ptx::mbar_init(&full[s], kGather ? 5 : a.prod_rr ? 1 : (a.a_split ? 3 : 2));
             ptx::mbar_init(&empty[s], 1);      // MMA commit
         }
         for (int s = 0; s < a.acc_stages; ++s) {
@@ -1003,7 +1003,90 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
     const uint32_t tmem_base = *tmem_holder;
     if (dbg && threadIdx.x == 0) dbg[1] = ptx::globaltimer();
 
-    if (warp == 0 || warp == 2 || (warp == 3 && !kGather && a.a_split)) {
+    if (!kGather && a.prod_rr && (warp == 0 || warp == 2 || warp == 3)) {
+        // ===================== TMA producers, round robin (a.prod_rr) =====================
+        // K block g of this CTA's schedule (ring stage g % STAGES) is loaded by producer warp
+        // g % NPROD (warps 0, 2, 3; lane 0): its A box and B box under one expect_tx (full barrier
+        // count 1). One issuing thread sustains ~1 box per 200-450 ns while the SM ingests far more
+        // (tools/kloop_feed.cu: 3 producers 279 ns per 128x128 K block vs 548-575 ns for the A/B split).
+        // A producer may run ahead of the others; before loading block g it waits on the parity of
+        // the stage's empty barrier for block g - STAGES, unambiguous only if block g - 2 STAGES has
+        // been consumed: its own previous wait (block g - NPROD) saw g - NPROD - STAGES consumed, so
+        // NPROD <= STAGES suffices.
+        const int NPROD = min(3, a.stages);
+        const int pid = (warp == 0) ? 0 : warp - 1;
+        if (lane == 0 && pid < NPROD) {
+            const uint32_t a_rows = kPair ? 128u : (uint32_t)a.bm;
+            const uint32_t tx = (a_rows * 128u + b_bytes) * (kPair ? 2u : 1u);   // a pair's loads land on the leader's barrier
+            struct ItemPos {
+                int m0, nimg, wc, hc, n0;
+            };
+            auto walk = [&](auto &&fn) {
+                long long g = 0;
+                for (long long w = wstart; w < a.work; w += wstep) {
+                    const WorkPos wp = decode_work(w, a);
+                    const int kb0 = wp.split * a.kb_per_split;
+                    const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+                    int kb = kb0 + (int)((pid - g % NPROD + NPROD) % NPROD);
+                    g += kb - kb0;
+                    if (kb < kb1) {
+                        ItemPos ip;
+                        ip.m0 = wp.mt * a.bm + (int)crank * 128;   // M < 2^31 (plan validation)
+                        ip.nimg = ip.m0 / (int)a.PQ;
+                        const int rem = ip.m0 - ip.nimg * (int)a.PQ;
+                        const int p = rem / a.Q, q = rem - p * a.Q;
+                        ip.wc = q * a.stride_w - a.pad_w;
+                        ip.hc = p * a.stride_h - a.pad_h;
+                        ip.n0 = wp.nt * a.bn + (int)crank * (a.bn / 2);
+                        for (; kb < kb1; kb += NPROD, g += NPROD)
+                            if (!fn(g, ip, kb)) return;
+                    }
+                    g -= kb - kb1;   // back to the first K block of the next work item
+                }
+            };
+            auto load_b = [&](long long g, const ItemPos &ip, int kb) {
+                const uint32_t stage = (uint32_t)(g % a.stages);
+                const int rs = kb / a.c_blocks, cb = kb - rs * a.c_blocks;
+                if (leader) ptx::mbar_arrive_expect_tx(&full[stage], tx);
+                if constexpr (kPair) ptx::tma_load_3d_pair(smB + stage * b_bytes, &tmB, &full[stage], cb * a.bk, rs, ip.n0);
+                else ptx::tma_load_3d(smB + stage * b_bytes, &tmB, &full[stage], cb * a.bk, rs, ip.n0);
+            };
+            auto load_a = [&](long long g, const ItemPos &ip, int kb) {
+                const uint32_t stage = (uint32_t)(g % a.stages);
+                uint8_t *dst = smA + stage * a_bytes;
+                const int rs = kb / a.c_blocks, cb = kb - rs * a.c_blocks;
+                if (a.a_tiled) {
+                    if constexpr (kPair) ptx::tma_load_2d_pair(dst, &tmA, &full[stage], cb * a.bk, ip.m0);
+                    else ptx::tma_load_2d(dst, &tmA, &full[stage], cb * a.bk, ip.m0);
+                } else {
+                    const int r = rs / a.S, s = rs - r * a.S;
+                    if constexpr (kPair)
+                        ptx::tma_load_im2col_4d_pair(dst, &tmA, &full[stage], cb * a.bk, ip.wc, ip.hc, ip.nimg,
+                                                     (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                    else
+                        ptx::tma_load_im2col_4d(dst, &tmA, &full[stage], cb * a.bk, ip.wc, ip.hc, ip.nimg,
+                                                (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                }
+            };
+            // PDL: the ring starts empty, so this producer's first-pass weight boxes go out before
+            // griddepcontrol.wait (the previous grid may still write this conv's input, never its weights)
+            walk([&](long long g, const ItemPos &ip, int kb) {
+                if (g >= a.stages) return false;
+                load_b(g, ip, kb);
+                return true;
+            });
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (dbg && pid == 0) dbg[7] = ptx::globaltimer();
+            walk([&](long long g, const ItemPos &ip, int kb) {
+                if (g >= a.stages) {
+                    ptx::mbar_wait(&empty[(uint32_t)(g % a.stages)], (uint32_t)((g / a.stages) & 1) ^ 1u);
+                    load_b(g, ip, kb);
+                }
+                load_a(g, ip, kb);
+                return true;
+            });
+        }
+    } else if (warp == 0 || warp == 2 || (warp == 3 && !kGather && a.a_split)) {
         // ===================== TMA producers: warp 0 -> A (activations), warp 2 -> B (weights) ====
         // With a_split, warp 3 loads the second half of each A stage: one thread issues one TMA
         // instruction per ~430 cycles whatever the box size (tools/tma_bench.cu), so two issuing
