@@ -77,8 +77,8 @@ typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 
  *   WPK_FAMILY_UMMA : tcgen05 implicit GEMM, genes = (BLOCK_N, STAGES, SPLIT_K, MODE,
  *                     A_MODE, ACC_STAGES, BLOCK_M); MODE bit 0 = raster order, bit 1 = CTA pair
  *                     (cta_group::2, 256-row tiles across two SMs, BLOCK_M must be 256), bit 2 =
- *                     dual accumulators (BLOCK_M 128, no pair, SPLIT_K 1: even / odd K steps into
- *                     two TMEM accumulators summed by the epilogue); A_MODE 0 = TMA im2col producer
+ *                     dual accumulators (1-CTA BLOCK_M 128 or a pair, SPLIT_K 1: even / odd K steps
+ *                     into two TMEM accumulators summed by the epilogue); A_MODE 0 = TMA im2col producer
  *                     (plain TMA tiles for 1x1/s1/p0), 1 = explicit im2col matrix in the workspace,
  *                     2 = fused gather producer (im2col built in shared memory; small-C layers),
  *                     3 = pixel-segment gather (C <= 4), 4 = A_MODE 0 with the K blocks dealt round

@@ -71,7 +71,7 @@ static Space make_space(int family) {
         sp.names = {"T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"};
     } else if (family == WPK_FAMILY_UMMA) {
         sp.dom = {{16, 32, 64, 96, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8}, {1, 2, 4, 8, 16},
-                  {0, 1, 2, 3, 4, 5}, {0, 1, 2, 3, 4}, {1, 2, 4}, {128, 256}};
+                  {0, 1, 2, 3, 4, 5, 6, 7}, {0, 1, 2, 3, 4}, {1, 2, 4}, {128, 256}};
         sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "MODE", "A_MODE", "ACC_STAGES", "BLOCK_M"};
     } else if (family == WPK_FAMILY_GEMM32) {
         sp.dom = {{64, 128}, {64, 128}, {8, 16}, {4, 8}, {1, 2, 4, 8}, {0}, {0}};
@@ -202,7 +202,7 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->work = (long long)g->m_tiles * g->n_tiles * g->splits;
     if (g->work >= 2147483647LL / 2) return no("too many work items (tiles x splits >= 2^30)");
     if (g->kdual) {
-        if (g->pair || g->bm != 128) return no("dual accumulators are for 1-CTA 128-row tiles (MODE bit 2 with BLOCK_M 128, no pair)");
+        if (!g->pair && g->bm != 128) return no("dual accumulators: 1-CTA 128-row tiles or CTA pairs (BLOCK_M 256 over two SMs alternates its MMAs already)");
         if (g->splits != 1) return no("dual accumulators need SPLIT_K = 1");
         if (g->a_mode != 0) return no("dual accumulators are instantiated for the TMA A producer (A_MODE 0)");
     }

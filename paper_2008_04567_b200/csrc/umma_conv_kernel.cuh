@@ -1234,8 +1234,13 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                     if (!kConv || ptx::elect_one()) {
                     if constexpr (kPair) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            ptx::umma2<kTF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < 4; ++kk) {
+                            if constexpr (DUAL)   // even K steps -> accumulator 0, odd -> accumulator 1
+                                ptx::umma2<kTF32>(d_tmem + (kk & 1) * a.bn, ad + 2 * kk, bd + 2 * kk, a.idesc,
+                                                  (kb > kb0 || kk > 1) ? 1u : 0u);
+                            else
+                                ptx::umma2<kTF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        }
                         ptx::umma_commit2_multicast(&empty[stage]);   // frees the stage in both CTAs
                     } else {
                         if constexpr (DUAL) {   // even K steps -> accumulator 0, odd -> accumulator 1 (BN columns on)
@@ -1475,7 +1480,7 @@ static cudaError_t launch_variant(cudaLaunchConfig_t &lc, const CUtensorMap &tmA
 template <int DT, int AK>
 static cudaError_t launch_ak(int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                              const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
-    if constexpr (AK == AK_TMA) {   // dual accumulators (MODE bit 2): TMA A producer only (plan validation)
+    if constexpr (AK == AK_TMA || AK == AK_PAIR) {   // dual accumulators (MODE bit 2): TMA A producers only (plan validation)
         if (a.kdual) {
             if (ek == EK_TMA)
                 return a.epilogue == 3 ? launch_variant<DT, AK, EK_TMA, true, true>(lc, tmA, tmB, tmY, tmP, a)

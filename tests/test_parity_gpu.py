@@ -68,7 +68,7 @@ def test_epilogues(dtype, epilogue):
 def _umma_space():
     bns = [16, 32, 64, 96, 128, 192, 256]
     out = []
-    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1, 2, 3, 4, 5], [0, 1, 2, 4],
+    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1, 2, 3, 4, 5, 6, 7], [0, 1, 2, 4],
                                                           [1, 2, 4], [128, 256]):
         out.append((bn, st, sp, ra, amode, acc, bm))
     return out
