@@ -114,17 +114,21 @@ def _worker(rank, world, port, path, budget, search, out):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("search", ["ga", "random"])
-def test_world_size_invariance_gloo(replay_file, tmp_path, search):
+def test_world_size_invariance_gloo(replay_file, tmp_path, search, world):
+    """Sharded candidate evaluation (north star: GA population evaluated in parallel, fitness
+    all-gathered): with the same recorded timing set, every world size takes the same decisions
+    as one process -- identical history, choice and budget use."""
     path, table = replay_file
     budget = 150
     plan, res1 = _run_cpp(search, budget, 4, path, str(tmp_path / "w1.jsonl"))
-    out = str(tmp_path / "w2")
-    mp.start_processes(_worker, args=(2, 29517 + hash(search) % 100, path, budget, search, out), nprocs=2,
-                       start_method="spawn")
-    r0, r1 = (json.load(open(out + f".{r}")) for r in (0, 1))
-    assert r0 == r1
-    assert r0["genes"] == res1.genes and r0["best"] == res1.best_us and r0["measured"] == res1.measured
+    out = str(tmp_path / f"w{world}")
+    mp.start_processes(_worker, args=(world, 29517 + 10 * world + hash(search) % 7, path, budget, search, out),
+                       nprocs=world, start_method="spawn")
+    rs = [json.load(open(out + f".{r}")) for r in range(world)]
+    assert all(r == rs[0] for r in rs)
+    assert rs[0]["genes"] == res1.genes and rs[0]["best"] == res1.best_us and rs[0]["measured"] == res1.measured
     assert open(out + ".log0").read() == open(str(tmp_path / "w1.jsonl")).read()
 
 
