@@ -5,7 +5,8 @@ layer"; each sampled output is an independent dot product, so the check is exact
 
   * ResNet-50 N=32 bf16 (configs[1]) in the bench's committed tuned configs;
   * ResNet-50 N=32 TF32 (configs[1]) and VGG-16 N=64 fp16 (configs[2], RL-tuned) in the suite's
-    committed tuned configs (profiles/r1j_suite_tuned_configs.json), sampled;
+    committed tuned configs (profiles/r2_suite_tuned_configs.json), sampled;
+  * MobileNet-V2 N=32 bf16 in its suite configs, sampled;
   * ResNet-50 N=1 bf16 (configs[1]) and MobileNet-V2 N=1 bf16 (configs[3]): the WHOLE output tensor.
 
 Exact-integer inputs must be bit-exact (reading c11); uniform inputs must meet BASELINE.json's
@@ -25,7 +26,7 @@ from _util import TOL, assert_bit_exact, oracle_full, rel_error, run_product
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SUITE = json.load(open(os.path.join(ROOT, "profiles", "r1j_suite_tuned_configs.json")))
+SUITE = json.load(open(os.path.join(ROOT, "profiles", "r2_suite_tuned_configs.json")))
 BENCH_CFG = os.path.join(ROOT, "profiles", "bench_tuned_configs.json")
 NCPU = os.cpu_count() or 8
 
@@ -111,3 +112,12 @@ def test_mobilenet_v2_n1_bf16_suite_configs_full_tensor(layer, mode):
     else:
         assert rel_error("bf16", y, ref) <= TOL["bf16"]
 
+
+
+@pytest.mark.parametrize("mode", ["int", "uniform"])
+@pytest.mark.parametrize("layer", workloads.mobilenet_v2(32), ids=lambda l: l.name)
+def test_mobilenet_v2_n32_bf16_suite_configs(layer, mode):
+    fam, genes = SUITE["mobilenet_v2_n32"]["layers"][layer.name]
+    x, w, b = workloads.generate(layer, "bf16", mode, seed=workloads.config_seed(3, 90))
+    y, _ = run_product(layer, "bf16", "nhwc", x, w, b, config=(fam, genes))
+    _sampled_check(layer, "bf16", mode, y, x, w, b, seed=5)
