@@ -22,10 +22,16 @@
  *      WPK_NCHW: x [N][C][H][W],  w [K][C/g][R][S] (KCRS),  y [N][K][P][Q]
  *      WPK_NHWC: x [N][H][W][C],  w [K][R][S][C/g] (KRSC),  y [N][P][Q][K]
  *      b [K] (or NULL iff epilogue == WPK_EPI_NONE); residual z (WPK_EPI_BIAS_ADD_RELU) laid out as y.
- *  - dtypes: x, w, b, y share one element type:
+ *  - dtypes: x, w, b, y share one element type (except WPK_FP8E4M3, below):
  *      WPK_F32  float32, exact fp32 FMA on CUDA cores (strict-comparison path)
  *      WPK_TF32 float32 in/out, tf32 tensor-core products, fp32 accumulate
  *      WPK_BF16 bfloat16 in/out, fp32 accumulate;  WPK_F16 float16 in/out, fp32 accumulate.
+ *      WPK_FP8E4M3 (NEXT-4): x and w are OCP float8 e4m3 ("e4m3fn": 1 sign, 4 exponent, 3 mantissa
+ *               bits, bias 7, no infinities; torch.float8_e4m3fn), b, z and y are bfloat16;
+ *               tcgen05.mma kind::f8f6f4 with fp32 accumulate. Tensor-core family only
+ *               (WPK_FAMILY_UMMA, A_MODE 0 or 4, groups 1); other families return
+ *               WPK_ERR_UNSUPPORTED at plan time. x and w are taken as given (no scaling: a
+ *               per-tensor scale folds into w and b outside the library).
  *    The accumulator is fp32; bias is up-converted to fp32 and added before ReLU; the output is
  *    rounded to nearest-even once.
  */
@@ -60,7 +66,7 @@ typedef enum {
     WPK_ERR_INTERNAL = 8          /* broken invariant (e.g. ranks disagree on the chosen config) */
 } wpk_status;
 
-typedef enum { WPK_F32 = 0, WPK_TF32 = 1, WPK_BF16 = 2, WPK_F16 = 3 } wpk_dtype;
+typedef enum { WPK_F32 = 0, WPK_TF32 = 1, WPK_BF16 = 2, WPK_F16 = 3, WPK_FP8E4M3 = 4 } wpk_dtype;
 typedef enum { WPK_NCHW = 0, WPK_NHWC = 1 } wpk_layout;
 /* WPK_EPI_BIAS_ADD_RELU: y = max(conv + b + z, 0) with a residual z of y's shape, layout and dtype
  * (the last conv of a ResNet block fused with its shortcut add). Run it
@@ -209,6 +215,30 @@ WPK_API wpk_status wpk_conv2d_run(wpk_plan plan, const void *x, const void *w, c
  * or b is NULL, or if z is not 16-byte aligned; wpk_conv2d_run on such a plan fails the same way. */
 WPK_API wpk_status wpk_conv2d_run_residual(wpk_plan plan, const void *x, const void *w, const void *b, const void *z,
                                            void *y, void *stream);
+
+/* Fused depthwise + pointwise convolution ("the MobileNet block"; the
+ * operator fusion of PAPER.md:15 and :35 -- "one CUDA kernel function for the fused operator"):
+ *   t = RN(dw_epilogue(depthwise_conv(x, w_dw) + b_dw))        (PAPER.md:47's conv with groups = C)
+ *   y = pw_epilogue(t (*) w_pw + b_pw)                          (a 1x1 conv, stride 1, pad 0)
+ * in ONE kernel: the tcgen05 pointwise GEMM's A operand (row = output pixel of the depthwise conv,
+ * K = its C channels) is computed by producer warps in shared memory and never written to global
+ * memory. t is rounded to the I/O dtype exactly as the unfused depthwise conv would store it, so the
+ * fused result equals the unfused chain's (bit for bit on exact-integer inputs).
+ *  dw:  the depthwise conv's shape (groups == C == K, NHWC, C % 8 == 0; stride / pad / dilation
+ *       any; dw->epilogue = NONE / BIAS / BIAS_RELU is applied to t); k_out = pointwise output
+ *       channels; pw_epilogue = NONE / BIAS / BIAS_RELU. dtype BF16 or F16.
+ *  Errors: WPK_ERR_SHAPE (not depthwise, k_out < 1, as wpk_conv2d_plan), WPK_ERR_UNSUPPORTED
+ *  (NCHW, other dtypes, C % 8 != 0, residual epilogues), WPK_ERR_INVALID_ARGUMENT.
+ *  The plan is tuned, configured and sized with the wpk_conv2d_* calls (tcgen05 family, A_MODE 0 =
+ *  the depthwise producer; no CTA pairs); run it with wpk_dwpw_run only. */
+WPK_API wpk_status wpk_dwpw_plan(const wpk_conv2d_shape *dw, int32_t k_out, wpk_epilogue pw_epilogue, wpk_dtype dtype,
+                                 int device, wpk_plan *out);
+/* x [N][H][W][C]; w_dw [C][R][S] (torch's depthwise weight [C][1][R][S], or NHWC [C][R][S][1]);
+ * b_dw [C] (NULL iff dw epilogue NONE); w_pw [K][C] (torch [K][C][1][1] or NHWC [K][1][1][C]);
+ * b_pw [K] (NULL iff pw epilogue NONE); y [N][P][Q][K]. All device pointers, 16-byte aligned, the
+ * plan's dtype. Asynchronous on `stream`; the repacked w_dw is cached per pointer. */
+WPK_API wpk_status wpk_dwpw_run(wpk_plan plan, const void *x, const void *w_dw, const void *b_dw, const void *w_pw,
+                                const void *b_pw, void *y, void *stream);
 
 /* Same as run, but x and y are HOST pointers: copies x host->device, runs, copies y back, all on
  * `stream`, then synchronises the stream. Device staging buffers live in the workspace. */

@@ -21,7 +21,7 @@ OK, ERR_INVALID_ARGUMENT, ERR_SHAPE, ERR_UNSUPPORTED, ERR_INVALID_CONFIG, ERR_EX
     ERR_OUT_OF_MEMORY, ERR_INTERNAL = range(9)
 STATUS_NAMES = ["OK", "INVALID_ARGUMENT", "SHAPE", "UNSUPPORTED", "INVALID_CONFIG", "EXHAUSTED", "CUDA",
                 "OUT_OF_MEMORY", "INTERNAL"]
-DTYPES = {"f32": 0, "tf32": 1, "bf16": 2, "f16": 3}
+DTYPES = {"f32": 0, "tf32": 1, "bf16": 2, "f16": 3, "fp8": 4}   # fp8 = WPK_FP8E4M3
 LAYOUTS = {"nchw": 0, "nhwc": 1}
 EPILOGUES = {"none": 0, "bias": 1, "bias_relu": 2, "bias_add_relu": 3}
 SEARCHES = {"ga": 0, "rl": 1, "random": 2}

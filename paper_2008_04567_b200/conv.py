@@ -11,7 +11,10 @@ import torch
 
 from . import _lib as L
 
-_TORCH_DT = {"f32": torch.float32, "tf32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}
+# dtype of b / z / y; x and w use _TORCH_IN_DT (they differ for "fp8": e4m3 operands, bf16 output)
+_TORCH_DT = {"f32": torch.float32, "tf32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16,
+             "fp8": torch.bfloat16}
+_TORCH_IN_DT = dict(_TORCH_DT, fp8=torch.float8_e4m3fn)
 
 
 def output_dims(n, c, h, w, k, r, s, stride=1, pad=0, dil=1, groups=1):
@@ -55,6 +58,7 @@ class Conv2dPlan:
         self._ws_bytes = -1
         # per-call checks against precomputed values (the eager call path is host-latency bound)
         self._tdt = _TORCH_DT[dtype]
+        self._idt = _TORCH_IN_DT[dtype]
         self._xs, self._wsh, self._ys = torch.Size(self.x_shape()), torch.Size(self.w_shape()), torch.Size(self.y_shape())
         self._hval = self.handle.value
 
@@ -120,10 +124,10 @@ class Conv2dPlan:
     def run(self, x: torch.Tensor, w: torch.Tensor, b: torch.Tensor | None, y: torch.Tensor | None = None,
             stream: torch.cuda.Stream | None = None, z: torch.Tensor | None = None) -> torch.Tensor:
         """y = epilogue(conv(x, w)); for epilogue "bias_add_relu" z is the residual (y's shape)."""
-        dt = self._tdt
+        dt, it = self._tdt, self._idt
         for t, nm, shp in ((x, "x", self._xs), (w, "w", self._wsh)):
-            if t.dtype is not dt or t.shape != shp or not t.is_cuda or not t.is_contiguous():
-                raise ValueError(f"{nm}: expected contiguous cuda {dt} of shape {tuple(shp)}, got {t.dtype} {tuple(t.shape)}")
+            if t.dtype is not it or t.shape != shp or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{nm}: expected contiguous cuda {it} of shape {tuple(shp)}, got {t.dtype} {tuple(t.shape)}")
         if y is None:
             y = torch.empty(self._ys, dtype=dt, device=x.device)
         elif y.dtype is not dt or y.shape != self._ys or not y.is_cuda or not y.is_contiguous():
@@ -152,13 +156,13 @@ class Conv2dPlan:
         return y
 
     def _check_host(self, x_host, w, b, y_host):
-        dt = self._tdt
-        for t, nm, shp in ((x_host, "x_host", self._xs), (y_host, "y_host", self._ys)):
-            if t.dtype is not dt or t.shape != shp or t.is_cuda or not t.is_contiguous():
-                raise ValueError(f"{nm}: expected contiguous CPU {dt} of shape {tuple(shp)}, got "
+        dt, it = self._tdt, self._idt
+        for t, nm, shp, tdt in ((x_host, "x_host", self._xs, it), (y_host, "y_host", self._ys, dt)):
+            if t.dtype is not tdt or t.shape != shp or t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{nm}: expected contiguous CPU {tdt} of shape {tuple(shp)}, got "
                                  f"{t.dtype} {tuple(t.shape)} on {t.device}")
-        if w.dtype is not dt or w.shape != self._wsh or not w.is_cuda or not w.is_contiguous():
-            raise ValueError(f"w: expected contiguous cuda {dt} of shape {tuple(self._wsh)}")
+        if w.dtype is not it or w.shape != self._wsh or not w.is_cuda or not w.is_contiguous():
+            raise ValueError(f"w: expected contiguous cuda {it} of shape {tuple(self._wsh)}")
         if b is not None and (b.dtype is not dt or b.shape != (self.k,) or not b.is_cuda or not b.is_contiguous()):
             raise ValueError(f"b: expected contiguous cuda {dt} of shape ({self.k},)")
 

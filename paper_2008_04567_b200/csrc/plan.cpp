@@ -35,7 +35,7 @@ static wpk_status to_desc(const wpk_conv2d_shape *s, int dtype, ConvDesc *d) {
     if (!s) return fail(WPK_ERR_INVALID_ARGUMENT, "shape is NULL");
     if (s->struct_size != sizeof(wpk_conv2d_shape))
         return fail(WPK_ERR_INVALID_ARGUMENT, "wpk_conv2d_shape.struct_size mismatch (ABI version)");
-    if (dtype < WPK_F32 || dtype > WPK_F16) return fail(WPK_ERR_INVALID_ARGUMENT, "bad dtype");
+    if (dtype < WPK_F32 || dtype > WPK_FP8E4M3) return fail(WPK_ERR_INVALID_ARGUMENT, "bad dtype");
     if (s->layout != WPK_NCHW && s->layout != WPK_NHWC) return fail(WPK_ERR_INVALID_ARGUMENT, "bad layout");
     if (s->epilogue < WPK_EPI_NONE || s->epilogue > WPK_EPI_BIAS_ADD_RELU)
         return fail(WPK_ERR_INVALID_ARGUMENT, "bad epilogue");
@@ -101,6 +101,13 @@ static bool in_domain(const Space &sp, const Config &cfg, std::string *why) {
 
 bool family_applicable(const ConvDesc &d, int family, std::string *why) {
     auto no = [&](const char *m) { if (why) *why = m; return false; };
+    if (d.dtype == WPK_FP8E4M3 && family != WPK_FAMILY_UMMA)
+        return no("FP8 (e4m3) runs on the tcgen05 family only (kind::f8f6f4)");
+    if (d.fused_dw) {   // the depthwise result is the A operand of the tcgen05 pointwise GEMM
+        if (family != WPK_FAMILY_UMMA) return no("fused depthwise+pointwise runs on the tcgen05 family only");
+        if (d.dtype != WPK_BF16 && d.dtype != WPK_F16) return no("fused depthwise+pointwise needs bf16 or fp16 data");
+        return true;
+    }
     if (family == WPK_FAMILY_SIMT) return true;   // the SIMT kernel handles every valid shape, layout and dtype
     if (family == WPK_FAMILY_JIT) return true;    // so does its NVRTC-specialised twin
     if (family == WPK_FAMILY_DW) {
@@ -130,7 +137,8 @@ static int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
 bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::string *why) {
     auto no = [&](const std::string &m) { if (why) *why = m; return false; };
-    const int e = d.elem();
+    const int e = d.in_elem();    // bytes per x / w element (the K-major operands)
+    const int eo = d.elem();      // bytes per y element
     g->bm = cfg.genes[6];
     g->bn = cfg.genes[0];
     g->bk = 128 / e;           // one 128-byte swizzle atom of K per stage
@@ -153,9 +161,23 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     }
     g->acc_stages = cfg.genes[5];
     g->seg_sp = 0; g->seg_hp = 0; g->seg_wp = 0; g->seg_fast = 0; g->seg_two = 0;
-    if ((g->a_mode == 1 || g->a_mode == 2) && d.c >= 64)
+    if (d.dtype == WPK_FP8E4M3 && g->a_mode != 0)
+        return no("FP8 (e4m3) is instantiated for the TMA A producers only (A_MODE 0 / 4)");
+    if (d.fused_dw) {
+        // fused depthwise + pointwise: the A producer computes the depthwise conv (internal A_MODE 5);
+        // the gene's other producers do not apply, K = the depthwise channels (C % 8 == 0)
+        if (cfg.genes[4] != 0) return no("fused depthwise+pointwise: A_MODE must be 0 (the depthwise producer)");
+        if ((cfg.genes[3] >> 1) & 3) return no("fused depthwise+pointwise: no CTA pairs / dual accumulators");
+        g->a_mode = 5;
+        g->cpad = d.c;
+        g->c_blocks = (d.c + g->bk - 1) / g->bk;
+        g->num_kb = g->c_blocks;
+    } else if ((g->a_mode == 1 || g->a_mode == 2) && d.c >= 64) {
         return no("A_MODE 1/2 (explicit im2col / gather) is reserved for layers with C < 64");
-    if (g->a_mode == 3) {
+    }
+    if (g->a_mode == 5) {
+        // (fused depthwise producer: set above)
+    } else if (g->a_mode == 3) {
         // pixel-segment gather (C <= 4): activations stored NHWC with 4 channels per pixel (8 or 16
         // bytes); K row = (r, s', c) with s' padded to Sp so that one 16-byte smem chunk holds whole
         // pixels of a single filter row; weights for s' >= S and c >= C are zero.
@@ -214,13 +236,13 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     if (g->bm == 256 && g->a_mode == 0 && !(d.r == 1 && d.s == 1 && d.sh == 1 && d.sw == 1 && d.ph == 0 && d.pw == 0))
         ;   // a 256-pixel im2col box is one TMA (pixelsPerColumn <= 1024)
     // A operand: a 1x1 / stride-1 / unpadded conv is a plain GEMM on x viewed as [N*H*W][C]
-    g->a_tiled = (g->a_mode == 1 || (d.r == 1 && d.s == 1 && d.sh == 1 && d.sw == 1 && d.ph == 0 && d.pw == 0 &&
+    g->a_tiled = (g->a_mode == 1 || (g->a_mode != 5 && d.r == 1 && d.s == 1 && d.sh == 1 && d.sw == 1 && d.ph == 0 && d.pw == 0 &&
                                       g->cpad == d.c && !getenv("WPK_A_IM2COL"))) ? 1 : 0;
     // epilogue through shared memory + TMA store: NHWC output, whole 128-byte column chunks
     // (split-K: the owner split stores the output the same way; the others store fp32 partials in
     // 32-column chunks, which always divide a 128-byte output chunk)
-    const int cw = 128 / e;
-    g->epi_tma = (d.layout == WPK_NHWC && g->bn % cw == 0 && ((long long)d.k * e) % 16 == 0 &&
+    const int cw = 128 / eo;
+    g->epi_tma = (d.layout == WPK_NHWC && g->bn % cw == 0 && ((long long)d.k * eo) % 16 == 0 &&
                   !getenv("WPK_EPI_DIRECT")) ? 1 : 0;
     const size_t smem_cap = 227 * 1024;
     const size_t bias_bytes = (size_t)round_up(d.k, 256) * 4;   // fp32, zero-padded past K
@@ -310,6 +332,7 @@ bool config_valid(const ConvDesc &d, const Config &cfg, std::string *why) {
 }
 
 int default_family(const ConvDesc &d) {
+    if (d.dtype == WPK_FP8E4M3) return WPK_FAMILY_UMMA;   // the only family with an e4m3 kernel
     if (d.g > 1) return WPK_FAMILY_DW;   // depthwise and grouped kernels
     if (family_applicable(d, WPK_FAMILY_UMMA, nullptr)) return WPK_FAMILY_UMMA;
     if (family_applicable(d, WPK_FAMILY_GEMM32, nullptr)) return WPK_FAMILY_GEMM32;
@@ -350,6 +373,15 @@ Config default_config(const ConvDesc &d, int family) {
     }
     const long long mt = (d.M() + 127) / 128;
     if (bn == 256 && mt * ((d.k + 255) / 256) < 120) bn = 128;
+    if (d.fused_dw) {   // fused depthwise + pointwise: 128-row 1-CTA tiles, the depthwise producer
+        int g[7] = {bn, 4, 1, 0, 0, 2, 128};
+        std::memcpy(c.genes, g, sizeof g);
+        for (int st = 8; st >= 2; --st) {
+            c.genes[1] = st;
+            if (config_valid(d, c, nullptr)) return c;
+        }
+        return c;   // (the plan call reports it invalid)
+    }
     // large layers: a tcgen05 CTA pair (256 x BLOCK_N over two SMs) halves B traffic per SM
     // (not for short-K layers: with 1-2 K blocks per tile a pair's accumulators are seen ~3 us
     // after the commit, DESIGN.md §10 finding 13, while 1-CTA 128 x 256 tiles stream)
@@ -432,11 +464,53 @@ wpk_status wpk_conv2d_plan(const wpk_conv2d_shape *shape, wpk_dtype dtype, int d
     wpk_status st = to_desc(shape, (int)dtype, &d);
     if (st != WPK_OK) return st;
     d.device = device;
+    if (d.dtype == WPK_FP8E4M3) {
+        std::string why;
+        if (!family_applicable(d, WPK_FAMILY_UMMA, &why)) return fail(WPK_ERR_UNSUPPORTED, "FP8 (e4m3): " + why);
+    }
     Plan *p = new (std::nothrow) Plan();
     if (!p) return fail(WPK_ERR_OUT_OF_MEMORY, "host allocation failed");
     p->d = d;
     p->device = device;
     p->cfg = default_config(d, default_family(d));
+    std::string why;
+    if (!config_valid(d, p->cfg, &why)) {
+        delete p;
+        return fail(WPK_ERR_EXHAUSTED, "no valid default config: " + why);
+    }
+    *out = reinterpret_cast<wpk_plan>(p);
+    return WPK_OK;
+}
+
+wpk_status wpk_dwpw_plan(const wpk_conv2d_shape *dw, int32_t k_out, wpk_epilogue pw_epilogue, wpk_dtype dtype,
+                         int device, wpk_plan *out) {
+    if (!out) return fail(WPK_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (device < 0) return fail(WPK_ERR_INVALID_ARGUMENT, "device must be >= 0");
+    if (k_out < 1) return fail(WPK_ERR_SHAPE, "k_out must be >= 1");
+    if (pw_epilogue < WPK_EPI_NONE || pw_epilogue > WPK_EPI_BIAS_RELU)
+        return fail(WPK_ERR_INVALID_ARGUMENT, "fused depthwise+pointwise: pointwise epilogue NONE / BIAS / BIAS_RELU");
+    ConvDesc d;
+    wpk_status st = to_desc(dw, (int)dtype, &d);
+    if (st != WPK_OK) return st;
+    if (d.g != d.c || d.k != d.c) return fail(WPK_ERR_SHAPE, "fused depthwise+pointwise: the first conv must be depthwise (groups == C == K)");
+    if (d.epilogue == WPK_EPI_BIAS_ADD_RELU) return fail(WPK_ERR_UNSUPPORTED, "fused depthwise+pointwise: no residual epilogue on the depthwise conv");
+    if (d.layout != WPK_NHWC) return fail(WPK_ERR_UNSUPPORTED, "fused depthwise+pointwise: NHWC only");
+    if (d.dtype != WPK_BF16 && d.dtype != WPK_F16) return fail(WPK_ERR_UNSUPPORTED, "fused depthwise+pointwise: bf16 / fp16 only");
+    if (d.c % 8) return fail(WPK_ERR_UNSUPPORTED, "fused depthwise+pointwise: C must be a multiple of 8 (16-byte vectors)");
+    if ((double)d.n * d.c * d.h * d.w >= 2147483647.0) return fail(WPK_ERR_UNSUPPORTED, "fused depthwise+pointwise: input >= 2^31 elements");
+    d.device = device;
+    d.fused_dw = 1;
+    d.dw_epi = d.epilogue;
+    d.epilogue = pw_epilogue;
+    d.k = k_out;
+    d.g = 1;
+    if ((double)d.n * d.p * d.q * d.k > 4.0e9) return fail(WPK_ERR_UNSUPPORTED, "tensor larger than 2^32 elements");
+    Plan *p = new (std::nothrow) Plan();
+    if (!p) return fail(WPK_ERR_OUT_OF_MEMORY, "host allocation failed");
+    p->d = d;
+    p->device = device;
+    p->cfg = default_config(d, WPK_FAMILY_UMMA);
     std::string why;
     if (!config_valid(d, p->cfg, &why)) {
         delete p;

@@ -3,6 +3,7 @@
 // inference constants ("kept invariant during inference").
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -275,6 +276,7 @@ static void launch_aux(int which, const void *src, void *dst, const ConvDesc &d,
                        int sp = 0) {
     if (d.dtype == WPK_BF16) launch_aux_t<__nv_bfloat16>(which, src, dst, d, cp, sm, st, sp);
     else if (d.dtype == WPK_F16) launch_aux_t<__half>(which, src, dst, d, cp, sm, st, sp);
+    else if (d.dtype == WPK_FP8E4M3) launch_aux_t<uint8_t>(which, src, dst, d, cp, sm, st, sp);   // byte moves only
     else launch_aux_t<float>(which, src, dst, d, cp, sm, st, sp);
 }
 
@@ -295,6 +297,7 @@ void fill_random_device(void *p, size_t n, int dtype, uint64_t seed, void *strea
     unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 4096);
     if (blocks == 0) return;
     if (dtype == WPK_BF16) fill_random_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((__nv_bfloat16 *)p, n, seed);
+    else if (dtype == WPK_FP8E4M3) fill_random_kernel<__nv_fp8_e4m3><<<blocks, 256, 0, st>>>((__nv_fp8_e4m3 *)p, n, seed);
     else if (dtype == WPK_F16) fill_random_kernel<__half><<<blocks, 256, 0, st>>>((__half *)p, n, seed);
     else fill_random_kernel<float><<<blocks, 256, 0, st>>>((float *)p, n, seed);
 }
@@ -381,12 +384,14 @@ static bool plan_geom(Plan &p, const Config &cfg, UmmaGeom *out, std::string *wh
 static WsLayout ws_layout(Plan &p, const Config &cfg, bool host_staging) {
     const ConvDesc &d = p.d;
     WsLayout L;
-    const size_t e = d.elem();
+    const size_t e = d.in_elem();   // x / w element bytes (y's are d.elem(); they differ for FP8)
     size_t off = 0;
     if (cfg.family == WPK_FAMILY_UMMA) {
         UmmaGeom g;
         if (!plan_geom(p, cfg, &g, nullptr)) return L;
-        if (g.a_mode == 1) {
+        if (g.a_mode == 5) {   // fused depthwise: its weights re-laid [R][S][C]
+            L.w_off = off; L.w_bytes = al256((size_t)d.c * d.r * d.s * e); off += L.w_bytes;
+        } else if (g.a_mode == 1) {
             L.x_off = off; L.x_bytes = al256((size_t)d.M() * g.cpad * e); off += L.x_bytes;
             L.w_off = off; L.w_bytes = al256((size_t)d.k * g.cpad * e); off += L.w_bytes;
         } else if (g.a_mode == 2) {
@@ -415,7 +420,7 @@ static WsLayout ws_layout(Plan &p, const Config &cfg, bool host_staging) {
     }
     if (host_staging) {
         L.hx_off = off; L.hx_bytes = al256((size_t)d.n * d.c * d.h * d.w * e); off += L.hx_bytes;
-        L.hy_off = off; L.hy_bytes = al256((size_t)d.M() * d.k * e); off += L.hy_bytes;
+        L.hy_off = off; L.hy_bytes = al256((size_t)d.M() * d.k * d.elem()); off += L.hy_bytes;
     }
     L.total = off;
     return L;
@@ -427,7 +432,7 @@ size_t workspace_bytes(Plan &p, const Config &cfg, bool host_staging) {
 
 // ---- one run ------------------------------------------------------------------------------------------
 int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const void *b, void *y, void *stream,
-                char *ws, size_t ws_bytes, const void *z) {
+                char *ws, size_t ws_bytes, const void *z, const void *w_dw, const void *b_dw) {
     const ConvDesc &d = p.d;
     cudaStream_t st = (cudaStream_t)stream;
     const int sm = device_sm_count(p.device);
@@ -568,7 +573,19 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     if (!plan_geom(p, cfg, &g, &why)) { set_error("invalid UMMA config: " + why); return -1; }
     const void *xk = x, *wk = w;
     const int pack_kind = WPK_FAMILY_UMMA * 10 + g.a_mode;
-    if (g.a_mode == 3) {
+    const void *dwk = nullptr;
+    if (g.a_mode == 5) {
+        // fused depthwise + pointwise: x and the pointwise weights [K][C] are used as given; the
+        // depthwise weights [C][R][S] are re-laid [R][S][C] once per weight pointer
+        if (!w_dw) { set_error("fused depthwise+pointwise plan: depthwise weights missing"); return -1; }
+        if (p.packed_for != w_dw || p.packed_cfg_family != pack_kind) {
+            launch_aux(3, w_dw, ws + L.w_off, d, 0, sm, st);
+            ++launches;
+            p.packed_for = w_dw;
+            p.packed_cfg_family = pack_kind;
+        }
+        dwk = ws + L.w_off;
+    } else if (g.a_mode == 3) {
         // activations -> zero-padded NHWC image with 4 channels per pixel
         launch_aux(g.seg_two ? 8 : 7, x, ws + L.x_off, d, g.seg_hp, sm, st, g.seg_wp);
         ++launches;
@@ -617,6 +634,8 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     if (ce != cudaSuccess) { set_error(std::string("aux kernel launch: ") + cudaGetErrorString(ce)); return -1; }
     UmmaLaunch U{};
     U.dtype = d.dtype; U.x = xk; U.w = wk; U.b = b; U.y = y; U.z = z;
+    U.dw_w = dwk; U.dw_b = (g.a_mode == 5 && d.dw_epi != WPK_EPI_NONE) ? b_dw : nullptr;
+    U.dw_relu = (g.a_mode == 5 && d.dw_epi == WPK_EPI_BIAS_RELU) ? 1 : 0;
     U.partial = (g.splits > 1 && !g.csplit) ? reinterpret_cast<float *>(ws + L.p_off) : nullptr;
     if (g.splits > 1 && !g.csplit) {
         // counters are self-resetting; zero them once per (workspace, layout) they live at
@@ -712,9 +731,11 @@ wpk_status wpk_conv2d_set_workspace(wpk_plan plan, void *dev_ptr, size_t bytes) 
 }
 
 static wpk_status run_impl(wpk_plan plan, const void *x, const void *w, const void *b, const void *z, void *y,
-                           void *stream);
+                           void *stream, const void *w_dw = nullptr, const void *b_dw = nullptr);
 
 wpk_status wpk_conv2d_run(wpk_plan plan, const void *x, const void *w, const void *b, void *y, void *stream) {
+    if (plan && reinterpret_cast<Plan *>(plan)->d.fused_dw)
+        return fail(WPK_ERR_INVALID_ARGUMENT, "a fused depthwise+pointwise plan runs through wpk_dwpw_run");
     if (plan && reinterpret_cast<Plan *>(plan)->d.epilogue == WPK_EPI_BIAS_ADD_RELU)
         return fail(WPK_ERR_INVALID_ARGUMENT, "the plan's residual epilogue needs wpk_conv2d_run_residual");
     return run_impl(plan, x, w, b, nullptr, y, stream);
@@ -723,7 +744,7 @@ wpk_status wpk_conv2d_run(wpk_plan plan, const void *x, const void *w, const voi
 wpk_status wpk_conv2d_run_residual(wpk_plan plan, const void *x, const void *w, const void *b, const void *z, void *y,
                                    void *stream) {
     if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
-    if (reinterpret_cast<Plan *>(plan)->d.epilogue != WPK_EPI_BIAS_ADD_RELU)
+    if (reinterpret_cast<Plan *>(plan)->d.epilogue != WPK_EPI_BIAS_ADD_RELU || reinterpret_cast<Plan *>(plan)->d.fused_dw)
         return fail(WPK_ERR_INVALID_ARGUMENT, "wpk_conv2d_run_residual needs a WPK_EPI_BIAS_ADD_RELU plan");
     if (!z) return fail(WPK_ERR_INVALID_ARGUMENT, "z must be non-NULL");
     if ((reinterpret_cast<uintptr_t>(z) & 15) != 0) return fail(WPK_ERR_INVALID_ARGUMENT, "z must be 16-byte aligned");
@@ -731,8 +752,21 @@ wpk_status wpk_conv2d_run_residual(wpk_plan plan, const void *x, const void *w, 
     return run_impl(plan, x, w, b, z, y, stream);
 }
 
+wpk_status wpk_dwpw_run(wpk_plan plan, const void *x, const void *w_dw, const void *b_dw, const void *w_pw,
+                        const void *b_pw, void *y, void *stream) {
+    if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
+    Plan *p = reinterpret_cast<Plan *>(plan);
+    if (!p->d.fused_dw) return fail(WPK_ERR_INVALID_ARGUMENT, "wpk_dwpw_run needs a plan from wpk_dwpw_plan");
+    if (!w_dw) return fail(WPK_ERR_INVALID_ARGUMENT, "w_dw must be non-NULL");
+    if ((p->d.dw_epi != WPK_EPI_NONE) != (b_dw != nullptr))
+        return fail(WPK_ERR_INVALID_ARGUMENT, "b_dw must be non-NULL iff the depthwise epilogue uses a bias");
+    if (!aligned16(w_dw) || (b_dw && !aligned16(b_dw)))
+        return fail(WPK_ERR_INVALID_ARGUMENT, "pointers must be 16-byte aligned");
+    return run_impl(plan, x, w_pw, b_pw, nullptr, y, stream, w_dw, b_dw);
+}
+
 static wpk_status run_impl(wpk_plan plan, const void *x, const void *w, const void *b, const void *z, void *y,
-                           void *stream) {
+                           void *stream, const void *w_dw, const void *b_dw) {
     if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
     Plan *p = reinterpret_cast<Plan *>(plan);
     if (!x || !w || !y) return fail(WPK_ERR_INVALID_ARGUMENT, "x, w and y must be non-NULL");
@@ -750,7 +784,7 @@ static wpk_status run_impl(wpk_plan plan, const void *x, const void *w, const vo
     size_t bytes;
     wpk_status st = ensure_ws(p, workspace_bytes(*p, p->cfg, false), &ws, &bytes);
     if (st != WPK_OK) return st;
-    int n = launch_conv(*p, p->cfg, x, w, b, y, stream, ws, bytes, z);
+    int n = launch_conv(*p, p->cfg, x, w, b, y, stream, ws, bytes, z, w_dw, b_dw);
     if (n < 0) return WPK_ERR_CUDA;
     p->last_launches = n;
     return WPK_OK;
@@ -774,6 +808,7 @@ static wpk_status run_host_impl(wpk_plan plan, const void *x_host, const void *w
     if (!plan) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL plan");
     Plan *p = reinterpret_cast<Plan *>(plan);
     if (!x_host || !y_host || !w) return fail(WPK_ERR_INVALID_ARGUMENT, "NULL pointer");
+    if (p->d.fused_dw) return fail(WPK_ERR_INVALID_ARGUMENT, "the host-buffer calls do not take fused depthwise+pointwise plans");
     if (p->d.epilogue == WPK_EPI_BIAS_ADD_RELU)
         return fail(WPK_ERR_INVALID_ARGUMENT, "the host-buffer calls support epilogues NONE / BIAS / BIAS_RELU");
     const ConvDesc &d = p->d;
@@ -783,7 +818,7 @@ static wpk_status run_host_impl(wpk_plan plan, const void *x_host, const void *w
     wpk_status st = ensure_ws(p, L.total, &ws, &bytes);
     if (st != WPK_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t xb = (size_t)d.n * d.c * d.h * d.w * d.elem(), yb = (size_t)d.M() * d.k * d.elem();
+    const size_t xb = (size_t)d.n * d.c * d.h * d.w * d.in_elem(), yb = (size_t)d.M() * d.k * d.elem();
     if (cudaMemcpyAsync(ws + L.hx_off, x_host, xb, cudaMemcpyHostToDevice, s) != cudaSuccess) {
         cudaGetLastError();
         return fail(WPK_ERR_CUDA, "H2D copy failed");
@@ -807,6 +842,8 @@ wpk_status wpk_conv2d_fold_batchnorm(wpk_plan plan, const void *w, const void *b
     if (!(eps >= 0.f)) return fail(WPK_ERR_INVALID_ARGUMENT, "fold_batchnorm: eps must be >= 0");
     Plan *p = reinterpret_cast<Plan *>(plan);
     const ConvDesc &d = p->d;
+    if (d.dtype == WPK_FP8E4M3)
+        return fail(WPK_ERR_UNSUPPORTED, "fold_batchnorm: FP8 plans take pre-folded (and pre-quantised) weights");
     const long long per_k = (long long)(d.c / d.g) * d.r * d.s;
     const long long total = (long long)d.k * per_k + d.k;
     const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 4096);

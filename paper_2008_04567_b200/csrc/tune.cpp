@@ -64,6 +64,7 @@ void log_line(TuneCtx &t, const std::string &s) {
 struct GpuBench {
     cudaStream_t st = nullptr;
     void *x = nullptr, *w = nullptr, *b = nullptr, *y = nullptr, *z = nullptr, *ws = nullptr, *flush = nullptr;
+    void *wdw = nullptr, *bdw = nullptr;   // fused depthwise+pointwise plans: the depthwise weights / bias
     // rotating mode (l2_flush == 2): P copies of x and y, one timed rep = one CUDA graph of P
     // back-to-back convs over all copies, so every launch reads an input last touched P launches ago
     // (P x footprint >= 2 x L2: cold) and one stamp pair spans P launches (the device timestamps
@@ -79,17 +80,24 @@ struct GpuBench {
         const ConvDesc &d = p.d;
         if (cudaSetDevice(p.device) != cudaSuccess) return fail_("cudaSetDevice");
         if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return fail_("stream");
-        const size_t e = d.elem();
+        const size_t e = d.in_elem(), eo = d.elem();   // x / w and y / b / z element bytes
         size_t xb = (size_t)d.n * d.c * d.h * d.w * e, wb = (size_t)d.k * (d.c / d.g) * d.r * d.s * e;
-        size_t yb = (size_t)d.M() * d.k * e;
-        if (cudaMalloc(&x, xb) || cudaMalloc(&w, wb) || cudaMalloc(&b, d.k * e + 16) || cudaMalloc(&y, yb))
+        size_t yb = (size_t)d.M() * d.k * eo;
+        if (cudaMalloc(&x, xb) || cudaMalloc(&w, wb) || cudaMalloc(&b, d.k * eo + 16) || cudaMalloc(&y, yb))
             return fail_("cudaMalloc of tuning buffers");
         fill_random_device(x, xb / e, d.dtype, 1, st);
         fill_random_device(w, wb / e, d.dtype, 2, st);
-        fill_random_device(b, d.k, d.dtype, 3, st);
+        fill_random_device(b, d.k, d.out_dtype(), 3, st);
+        if (d.fused_dw) {   // w / b above are the pointwise [K][C] (C = d.c) and [K]; add the depthwise ones
+            const size_t wdb = (size_t)d.c * d.r * d.s * e;
+            if (cudaMalloc(&wdw, wdb) || cudaMalloc(&bdw, d.c * e + 16))
+                return fail_("cudaMalloc of the depthwise buffers");
+            fill_random_device(wdw, wdb / e, d.dtype, 5, st);
+            fill_random_device(bdw, d.c, d.dtype, 6, st);
+        }
         if (d.epilogue == WPK_EPI_BIAS_ADD_RELU) {   // a residual plan reads z of y's shape
             if (cudaMalloc(&z, yb)) return fail_("cudaMalloc of the residual buffer");
-            fill_random_device(z, yb / e, d.dtype, 4, st);
+            fill_random_device(z, yb / eo, d.out_dtype(), 4, st);
         }
         flush_bytes = (size_t)2 * device_l2_bytes(p.device);
         if (cudaMalloc(&flush, flush_bytes + 256)) return fail_("cudaMalloc of the L2 flush buffer");
@@ -108,8 +116,7 @@ struct GpuBench {
     bool init_rotation(Plan &p) {   // lazily, on the first rotating measurement
         if (!xr.empty()) return true;
         const ConvDesc &d = p.d;
-        const size_t e = d.elem();
-        const size_t xb = (size_t)d.n * d.c * d.h * d.w * e, yb = (size_t)d.M() * d.k * e;
+        const size_t xb = (size_t)d.n * d.c * d.h * d.w * d.in_elem(), yb = (size_t)d.M() * d.k * d.elem();
         const size_t foot = xb + yb;
         size_t P = (2 * (size_t)device_l2_bytes(p.device) + foot - 1) / foot;
         P = std::max<size_t>(2, std::min<size_t>(P, 64));
@@ -131,7 +138,7 @@ struct GpuBench {
     ~GpuBench() {
         for (void *ptr : xr) cudaFree(ptr);
         for (void *ptr : yr) cudaFree(ptr);
-        for (void *ptr : {x, w, b, y, z, ws, flush, (void *)stamps})
+        for (void *ptr : {x, w, b, y, z, ws, flush, wdw, bdw, (void *)stamps})
             if (ptr) cudaFree(ptr);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
@@ -153,14 +160,14 @@ struct GpuBench {
         if (!init_rotation(p)) { *fatal = true; return INFINITY; }
         const size_t P = xr.size();
         for (int i = 0; i < std::max(1, warmup); ++i)   // eager: weight packing, workspace state, first-use maps
-            if (launch_conv(p, cfg, xr[i % P], w, b, yr[i % P], st, (char *)ws, ws_bytes, z) < 0) return INFINITY;
+            if (launch_conv(p, cfg, xr[i % P], w, b, yr[i % P], st, (char *)ws, ws_bytes, z, wdw, bdw) < 0) return INFINITY;
         if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;
         if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { *fatal = true; return INFINITY; }
         bool ok = true;
         for (size_t i = 0; i < P && ok; ++i)
-            ok = launch_conv(p, cfg, xr[i], w, b, yr[i], st, (char *)ws, ws_bytes, z) >= 0;
+            ok = launch_conv(p, cfg, xr[i], w, b, yr[i], st, (char *)ws, ws_bytes, z, wdw, bdw) >= 0;
         if (cudaStreamEndCapture(st, &g) != cudaSuccess || !ok || !g) {
             if (g) cudaGraphDestroy(g);
             cudaGetLastError();
@@ -209,7 +216,7 @@ struct GpuBench {
         p.reset_ws_state();
         if (l2mode == 2) return measure_rotating(p, cfg, warmup, reps, fatal);
         for (int i = 0; i < warmup; ++i)
-            if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes, z) < 0) return INFINITY;
+            if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes, z, wdw, bdw) < 0) return INFINITY;
         if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
         // Each rep is bracketed by two 1-thread kernels that write %globaltimer (256-ns steps; CUDA
         // events on this part advance in ~2-us steps, too coarse for 5-30 us layers). The constant
@@ -219,7 +226,7 @@ struct GpuBench {
         for (int i = 0; i < reps; ++i) {
             if (l2flush) l2_flush_device(flush, flush_bytes, (char *)flush + flush_bytes, st);
             timestamp_device(stamps + 2 * i, st);
-            if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes, z) < 0) return INFINITY;
+            if (launch_conv(p, cfg, x, w, b, y, st, (char *)ws, ws_bytes, z, wdw, bdw) < 0) return INFINITY;
             timestamp_device(stamps + 2 * i + 1, st);
             if (!sync_with_deadline(10.0)) { *fatal = true; return INFINITY; }
         }

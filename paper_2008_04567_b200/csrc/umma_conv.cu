@@ -39,7 +39,8 @@ static EncodeIm2colFn encode_im2col() {
 }
 
 static uint32_t make_idesc(int dt, int bm, int bn) {
-    uint32_t fmt = (dt == DT_F16) ? 0u : (dt == DT_BF16) ? 1u : 2u;
+    // operand formats: kind::f16 F16 = 0 / BF16 = 1, kind::tf32 TF32 = 2, kind::f8f6f4 E4M3 = 0
+    uint32_t fmt = (dt == DT_F16 || dt == DT_FP8) ? 0u : (dt == DT_BF16) ? 1u : 2u;
     uint32_t d = 0;
     d |= 1u << 4;                          // c_format = F32
     d |= fmt << 7;                         // a_format
@@ -51,11 +52,15 @@ static uint32_t make_idesc(int dt, int bm, int bn) {
 }
 
 int umma_launch(const UmmaLaunch &L, std::string *err) {
-    const int dt = L.dtype == WPK_F16 ? DT_F16 : L.dtype == WPK_BF16 ? DT_BF16 : DT_TF32;
-    const int e = (dt == DT_TF32) ? 4 : 2;
+    const int dt = L.dtype == WPK_F16 ? DT_F16 : L.dtype == WPK_BF16 ? DT_BF16 : L.dtype == WPK_FP8E4M3 ? DT_FP8 : DT_TF32;
+    // x / w (the K-major operands) and y may differ in element type: e4m3 operands, bf16 output
+    const int e = (dt == DT_TF32) ? 4 : (dt == DT_FP8) ? 1 : 2;
+    const int eo = (dt == DT_TF32) ? 4 : 2;
     const CUtensorMapDataType tdt = (dt == DT_F16)    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                     : (dt == DT_BF16) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                    : (dt == DT_FP8)  ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                                       : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const CUtensorMapDataType tdt_out = (dt == DT_FP8) ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : tdt;
     if (!encode_tiled() || !encode_im2col()) {
         *err = "cuTensorMapEncode* driver entry points unavailable";
         return -1;
@@ -116,10 +121,10 @@ int umma_launch(const UmmaLaunch &L, std::string *err) {
         CUresult r;
         {
             cuuint64_t dims[2] = {(cuuint64_t)L.K, (cuuint64_t)M};
-            cuuint64_t strides[1] = {(cuuint64_t)L.K * e};
-            cuuint32_t box[2] = {(cuuint32_t)(128 / e), 32};
+            cuuint64_t strides[1] = {(cuuint64_t)L.K * eo};
+            cuuint32_t box[2] = {(cuuint32_t)(128 / eo), 32};
             cuuint32_t estr[2] = {1, 1};
-            r = encode_tiled()(&tmY, tdt, 2, L.y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            r = encode_tiled()(&tmY, tdt_out, 2, L.y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         }
@@ -199,6 +204,9 @@ launch:
     a.recv_stride = g.recv_stride;
     a.a_split = a_split;
     a.z = L.z;
+    a.dw_w = L.dw_w;
+    a.dw_b = L.dw_b;
+    a.dw_relu = L.dw_relu;
     static const int dbg_flags = env_knob("WPK_DBG_FLAGS", 0);
     a.dbg_flags = dbg_flags;
     static const int l2pf = env_knob("WPK_L2PF", 0);   // measured: neutral (weights) to -8% (activations), off
@@ -235,10 +243,11 @@ launch:
     }
     lc.attrs = attr;
     lc.numAttrs = nattr;
-    const int ak = g.a_mode == 3 ? AK_SEG : g.a_mode == 2 ? AK_GATHER : g.pair ? AK_PAIR : AK_TMA;
+    const int ak = g.a_mode == 5 ? AK_DW : g.a_mode == 3 ? AK_SEG : g.a_mode == 2 ? AK_GATHER : g.pair ? AK_PAIR : AK_TMA;
     const int ek = !g.epi_tma ? EK_DIRECT : g.csplit ? EK_CSPLIT : g.splits > 1 ? EK_SPLIT : EK_TMA;
     if (dt == DT_F16) ce = umma_launch_f16(ak, ek, lc, tmA, tmB, tmY, tmP, a);
     else if (dt == DT_BF16) ce = umma_launch_bf16(ak, ek, lc, tmA, tmB, tmY, tmP, a);
+    else if (dt == DT_FP8) ce = umma_launch_fp8(ak, ek, lc, tmA, tmB, tmY, tmP, a);
     else ce = umma_launch_tf32(ak, ek, lc, tmA, tmB, tmY, tmP, a);
     if (ce == cudaSuccess) ce = cudaGetLastError();
     if (ce != cudaSuccess) {

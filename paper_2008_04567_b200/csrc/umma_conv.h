@@ -10,10 +10,10 @@
 
 namespace wpk {
 
-enum { DT_F16 = 0, DT_BF16 = 1, DT_TF32 = 2 };
+enum { DT_F16 = 0, DT_BF16 = 1, DT_TF32 = 2, DT_FP8 = 3 };   // DT_FP8: e4m3 x / w, bf16 b / z / y
 // A producer kinds: TMA (im2col / tiled), TMA for a CTA pair, element gather (A_MODE 2),
 // pixel-segment gather (A_MODE 3)
-enum { AK_TMA = 0, AK_PAIR = 1, AK_GATHER = 2, AK_SEG = 3 };
+enum { AK_TMA = 0, AK_PAIR = 1, AK_GATHER = 2, AK_SEG = 3, AK_DW = 4 };   // AK_DW: fused depthwise producer (wpk_dwpw_*)
 // epilogue kinds: final output via TMA store, split-K partials via TMA store (+ in-kernel fixup),
 // direct global stores (NCHW output or K not a multiple of the 128-byte chunk; final or partial)
 enum { EK_TMA = 0, EK_SPLIT = 1, EK_DIRECT = 2, EK_CSPLIT = 3 };   // EK_CSPLIT: split-K over a cluster (DSMEM)
@@ -52,6 +52,9 @@ struct UmmaArgs {
     const void *wgt;                // packed weights [K][R*S][C] as the B tensor map sees them
     long long w_bytes;
     int e_size;                     // bytes per element of x / w
+    const void *dw_w;               // AK_DW: depthwise weights packed [R][S][C] (I/O dtype)
+    const void *dw_b;               // AK_DW: depthwise bias [C] or NULL
+    int dw_relu;                    // AK_DW: ReLU after the depthwise bias
 };
 
 // Tensor maps of the last launch, reused while pointers and config are unchanged (host-side
@@ -72,6 +75,9 @@ struct UmmaLaunch {
     const void *b;
     void *y;
     const void *z = nullptr;         // residual (epilogue 3), laid out as y
+    const void *dw_w = nullptr;      // fused depthwise (A_MODE 5): weights [R][S][C], bias [C] or NULL
+    const void *dw_b = nullptr;
+    int dw_relu = 0;
     float *partial;                  // split-K workspace (splits x M x K fp32) or nullptr
     int *counters = nullptr;         // split-K tile counters (zeroed once per workspace)
     int N, H, W, K, R, S, P, Q;
@@ -97,6 +103,8 @@ cudaError_t umma_launch_f16(int ak, int ek, cudaLaunchConfig_t &lc, const CUtens
 cudaError_t umma_launch_bf16(int ak, int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                              const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a);
 cudaError_t umma_launch_tf32(int ak, int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
+                             const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a);
+cudaError_t umma_launch_fp8(int ak, int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                              const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a);
 
 }  // namespace wpk

@@ -48,6 +48,7 @@ template <int DT> struct OutT;
 template <> struct OutT<DT_F16> { using T = __half; };
 template <> struct OutT<DT_BF16> { using T = __nv_bfloat16; };
 template <> struct OutT<DT_TF32> { using T = float; };
+template <> struct OutT<DT_FP8> { using T = __nv_bfloat16; };   // e4m3 operands, bf16 output
 
 __device__ __forceinline__ float ld_bias(const __half *b, int k) { return __half2float(b[k]); }
 __device__ __forceinline__ float ld_bias(const __nv_bfloat16 *b, int k) { return __bfloat162float(b[k]); }
@@ -787,6 +788,107 @@ __device__ __forceinline__ void element_gather(const UmmaArgs &a, uint8_t *smA, 
     }
 }
 
+// Fused depthwise producer (wpk_dwpw_*, NEXT-4: the MobileNet-V2 block's depthwise 3x3 feeding its
+// 1x1 projection in ONE kernel): the A operand of the pointwise GEMM -- row m = output pixel of the
+// depthwise conv, K = its C channels -- is computed here, never stored to global memory:
+//   a[m][c] = RN_T(dw_epilogue(sum_{r,s} x[n][p*sh - ph + r*dh][q*sw - pw + s*dw][c] * w_dw[r][s][c] + b_dw[c]))
+// (fp32 products and sum in (r, s) order, the bias added after the sum, one rounding to the I/O
+// dtype: what the unfused depthwise conv stores). NHWC x, C % 8 == 0, 16-bit T. Thread t of the 4
+// producer warps owns rows t and 128 + t of every stage: per K block it accumulates the 64 channels
+// of its pixel over the taps (16-byte vector loads of x and of the [R][S][C] weights, the latter
+// the same address across the warp), applies bias / ReLU, converts and writes the 128-byte row
+// into the swizzled stage; channels >= C and rows >= M are written as zeros.
+template <typename T>
+__device__ __forceinline__ void dw_producer(const UmmaArgs &a, uint8_t *smA, uint32_t a_bytes, uint64_t *full,
+                                           uint64_t *empty, int nsub, long long wstart, long long wstep, int t,
+                                           int lane) {
+    const uint4 *xv = reinterpret_cast<const uint4 *>(a.x);
+    const uint4 *wv = reinterpret_cast<const uint4 *>(a.dw_w);
+    const uint4 *bv = reinterpret_cast<const uint4 *>(a.dw_b);
+    const int cv = a.C >> 3;                                    // 16-byte vectors per pixel
+    uint32_t stage = 0, phase = 0;
+    for (long long w = wstart; w < a.work; w += wstep) {
+        const WorkPos wp = decode_work(w, a);
+        const int kb0 = wp.split * a.kb_per_split;
+        const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
+        int rh0[2], rw0[2], rn[2];
+        bool rv[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const long long m = (long long)wp.mt * a.bm + hh * 128 + t;
+            rv[hh] = hh < nsub && m < a.M;
+            const long long mm = rv[hh] ? m : 0;
+            const int n = (int)(mm / a.PQ);
+            const int rem = (int)(mm - (long long)n * a.PQ);
+            const int p = rem / a.Q, q = rem - (rem / a.Q) * a.Q;
+            rn[hh] = n;
+            rh0[hh] = p * a.stride_h - a.pad_h;
+            rw0[hh] = q * a.stride_w - a.pad_w;
+        }
+        for (int kb = kb0; kb < kb1; ++kb) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            const int c0 = kb * 8;                              // first 16-byte channel vector of the block
+#pragma unroll 1
+            for (int hh = 0; hh < 2; ++hh) {
+                if (hh >= nsub) break;
+                const int row = hh * 128 + t;
+                const uint32_t rbase = ptx::smem_u32(smA + stage * a_bytes) + (uint32_t)(row >> 3) * 1024u +
+                                       (uint32_t)(row & 7) * 128u;
+                float acc[64];
+#pragma unroll
+                for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+                if (rv[hh]) {
+#pragma unroll 1
+                    for (int r = 0; r < a.R; ++r) {
+                        const int hi = rh0[hh] + r * a.dil_h;
+                        if (hi < 0 || hi >= a.H) continue;
+#pragma unroll 1
+                        for (int s = 0; s < a.S; ++s) {
+                            const int wi = rw0[hh] + s * a.dil_w;
+                            if (wi < 0 || wi >= a.W) continue;
+                            const uint4 *xp = xv + ((long long)(rn[hh] * a.H + hi) * a.W + wi) * cv;
+                            const uint4 *wt = wv + (long long)(r * a.S + s) * cv;
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                if (c0 + j >= cv) break;
+                                const uint4 xx = __ldg(xp + c0 + j), ww = __ldg(wt + c0 + j);
+                                const uint32_t xs[4] = {xx.x, xx.y, xx.z, xx.w}, ws[4] = {ww.x, ww.y, ww.z, ww.w};
+#pragma unroll
+                                for (int e = 0; e < 8; ++e)
+                                    acc[j * 8 + e] = fmaf(to_f2(xs[e >> 1], e & 1, (T *)nullptr),
+                                                          to_f2(ws[e >> 1], e & 1, (T *)nullptr), acc[j * 8 + e]);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    uint32_t o[4] = {0u, 0u, 0u, 0u};
+                    if (rv[hh] && c0 + j < cv) {
+                        uint32_t bb[4] = {0u, 0u, 0u, 0u};
+                        if (bv) {
+                            const uint4 b4 = __ldg(bv + c0 + j);
+                            bb[0] = b4.x; bb[1] = b4.y; bb[2] = b4.z; bb[3] = b4.w;
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            float v0 = acc[j * 8 + 2 * e] + to_f2(bb[e], 0, (T *)nullptr);
+                            float v1 = acc[j * 8 + 2 * e + 1] + to_f2(bb[e], 1, (T *)nullptr);
+                            if (a.dw_relu) { v0 = fmaxf(v0, 0.f); v1 = fmaxf(v1, 0.f); }
+                            o[e] = pack2(v0, v1, (T *)nullptr);
+                        }
+                    }
+                    ptx::st_shared_v4(rbase + ((uint32_t)(j ^ (row & 7)) << 4), o[0], o[1], o[2], o[3]);
+                }
+            }
+            ptx::fence_proxy_async_smem();                 // generic-proxy writes -> async-proxy (MMA) reads
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&full[stage]);
+            if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
+        }
+    }
+}
+
 // A_MODE 3 producer: pixel-segment gather (C <= 4). x is re-laid as a zero-padded NHWC image
 // with 4 channels per pixel (a.H x a.W = padded size), so every tap is in bounds. K row =
 // (r, s', c), s' < Sp; a 16-byte smem chunk holds PPC whole pixels of one filter row. FAST: the
@@ -924,6 +1026,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                      const __grid_constant__ UmmaArgs a) {
     using T = typename OutT<DT>::T;
     constexpr bool kTF32 = (DT == DT_TF32);
+    constexpr int kKind = (DT == DT_TF32) ? 1 : (DT == DT_FP8) ? 2 : 0;   // tcgen05.mma kind
     constexpr bool kPair = (AK == AK_PAIR);
     constexpr bool kGather = (AK >= AK_GATHER);
 
@@ -1194,6 +1297,8 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
 #undef WPK_SEG
         } else if constexpr (AK == AK_GATHER) {
             element_gather<kTF32>(a, smA, a_bytes, full, empty, nsub, wstart, wstep, t, lane);
+        } else if constexpr (AK == AK_DW) {
+            dw_producer<T>(a, smA, a_bytes, full, empty, nsub, wstart, wstep, t, lane);
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (single thread; the leader CTA of a pair) =====================
@@ -1236,23 +1341,23 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             if constexpr (DUAL)   // even K steps -> accumulator 0, odd -> accumulator 1
-                                ptx::umma2<kTF32>(d_tmem + (kk & 1) * a.bn, ad + 2 * kk, bd + 2 * kk, a.idesc,
+                                ptx::umma2<kKind>(d_tmem + (kk & 1) * a.bn, ad + 2 * kk, bd + 2 * kk, a.idesc,
                                                   (kb > kb0 || kk > 1) ? 1u : 0u);
                             else
-                                ptx::umma2<kTF32>(d_tmem, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                                ptx::umma2<kKind>(d_tmem, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
                         }
                         ptx::umma_commit2_multicast(&empty[stage]);   // frees the stage in both CTAs
                     } else {
                         if constexpr (DUAL) {   // even K steps -> accumulator 0, odd -> accumulator 1 (BN columns on)
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk)
-                                ptx::umma<kTF32>(d_tmem + (kk & 1) * a.bn, ad + 2 * kk, bd + 2 * kk, a.idesc,
+                                ptx::umma<kKind>(d_tmem + (kk & 1) * a.bn, ad + 2 * kk, bd + 2 * kk, a.idesc,
                                                  (kb > kb0 || kk > 1) ? 1u : 0u);
                         } else {
                             for (int h = 0; h < nsub; ++h) {
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)   // 4 x 32 bytes of K per 128-byte stage (+2 desc units)
-                                    ptx::umma<kTF32>(d_tmem + h * a.bn, ad + h * (16384 >> 4) + 2 * kk, bd + 2 * kk, a.idesc,
+                                    ptx::umma<kKind>(d_tmem + h * a.bn, ad + h * (16384 >> 4) + 2 * kk, bd + 2 * kk, a.idesc,
                                                      (kb > kb0 || kk > 0) ? 1u : 0u);
                             }
                         }
@@ -1504,8 +1609,15 @@ template <int DT>
 cudaError_t umma_launch_dt(int ak, int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                            const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
     if (ak == AK_PAIR) return launch_ak<DT, AK_PAIR>(ek, lc, tmA, tmB, tmY, tmP, a);
-    if (ak == AK_GATHER) return launch_ak<DT, AK_GATHER>(ek, lc, tmA, tmB, tmY, tmP, a);
-    if (ak == AK_SEG) return launch_ak<DT, AK_SEG>(ek, lc, tmA, tmB, tmY, tmP, a);
+    if constexpr (DT == DT_FP8) {   // e4m3: TMA A producers only (plan validation)
+        if (ak != AK_TMA) return cudaErrorInvalidConfiguration;
+    } else {
+        if (ak == AK_GATHER) return launch_ak<DT, AK_GATHER>(ek, lc, tmA, tmB, tmY, tmP, a);
+        if (ak == AK_SEG) return launch_ak<DT, AK_SEG>(ek, lc, tmA, tmB, tmY, tmP, a);
+        if constexpr (DT == DT_BF16 || DT == DT_F16) {   // fused depthwise producer: 16-bit data
+            if (ak == AK_DW) return launch_ak<DT, AK_DW>(ek, lc, tmA, tmB, tmY, tmP, a);
+        }
+    }
     return launch_ak<DT, AK_TMA>(ek, lc, tmA, tmB, tmY, tmP, a);
 }
 

@@ -23,9 +23,21 @@ struct ConvDesc {
     int p, q;          // output spatial size
     int dtype;         // wpk_dtype
     int device = 0;    // CUDA device of the plan (SM count for one-wave checks)
+    // fused depthwise + pointwise plan (wpk_dwpw_plan): (n, c, h, w, r, s, strides, pads, dils) are
+    // the depthwise conv's (groups = C), k the pointwise output channels; p, q the depthwise output;
+    // `epilogue` applies to the pointwise output, dw_epi to the depthwise intermediate
+    int fused_dw = 0;
+    int dw_epi = 0;
     long long M() const { return (long long)n * p * q; }
-    long long flops() const { return 2LL * n * k * p * q * (c / g) * r * s; }
-    int elem() const { return (dtype == WPK_BF16 || dtype == WPK_F16) ? 2 : 4; }
+    long long flops() const {
+        if (fused_dw) return 2LL * n * p * q * c * ((long long)r * s + k);
+        return 2LL * n * k * p * q * (c / g) * r * s;
+    }
+    // bytes per element of y / b / z (the output side) and of x / w (the input side): they differ
+    // only for WPK_FP8E4M3 (e4m3 x and w, bf16 b, z and y)
+    int elem() const { return (dtype == WPK_BF16 || dtype == WPK_F16 || dtype == WPK_FP8E4M3) ? 2 : 4; }
+    int in_elem() const { return dtype == WPK_FP8E4M3 ? 1 : elem(); }
+    int out_dtype() const { return dtype == WPK_FP8E4M3 ? WPK_BF16 : dtype; }
 };
 
 struct Config {
@@ -93,8 +105,10 @@ struct Workspace {
 struct Plan;
 size_t workspace_bytes(Plan &p, const Config &cfg, bool host_staging);
 // Launch everything for one run on `stream`; returns number of kernel launches or -1 (error set).
+// (w_dw, b_dw: the depthwise weights / bias of a fused depthwise+pointwise plan, else unused)
 int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const void *b, void *y,
-                void *stream, char *ws, size_t ws_bytes, const void *z = nullptr);
+                void *stream, char *ws, size_t ws_bytes, const void *z = nullptr, const void *w_dw = nullptr,
+                const void *b_dw = nullptr);
 int device_sm_count(int device);
 // environment knob read once per process (experiments and debugging only)
 int env_knob(const char *name, int dflt);

@@ -183,3 +183,25 @@ def test_missing_library_fails_loudly(tmp_path):
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=120)
     assert "RAISED True" in out.stdout, out.stdout + out.stderr
+
+
+def test_fp8_plans_host_validation():
+    """WPK_FP8E4M3 (e4m3 x / w, bf16 y): tcgen05 family only, TMA A producers only (no GPU needed:
+    plan + config validation are host logic)."""
+    lib = L.load()
+    st, h = _plan(L.make_shape(n=2, c=192, h=11, w=13, k=200, r=3, s=3, stride=1, pad=1, layout="nhwc"), dtype="fp8")
+    assert st == 0
+    fam, g = ctypes.c_int32(), (ctypes.c_int32 * L.NUM_GENES)()
+    assert lib.wpk_conv2d_get_config(h, ctypes.byref(fam), g) == 0
+    assert fam.value == 1 and g[4] in (0, 4)            # tcgen05, TMA A producer
+    for am in (1, 2, 3):                                # gather / explicit im2col: not instantiated for e4m3
+        genes = (ctypes.c_int32 * L.NUM_GENES)(128, 4, 1, 0, am, 2, 128)
+        assert lib.wpk_conv2d_config_valid(h, 1, genes) == 0
+    for fam_id, genes in ((0, (16, 4, 4, 1, 1, 1, 1)), (3, (64, 64, 16, 4, 1, 0, 0)), (4, (16, 4, 4, 1, 1, 1, 1))):
+        assert lib.wpk_conv2d_config_valid(h, fam_id, (ctypes.c_int32 * L.NUM_GENES)(*genes)) == 0
+    assert b"FP8" in lib.wpk_last_error()
+    lib.wpk_conv2d_destroy(h)
+    st, h = _plan(L.make_shape(n=1, c=32, h=8, w=8, k=32, r=3, s=3, stride=1, pad=1, groups=32, layout="nhwc"),
+                  dtype="fp8")
+    assert st == L.ERR_UNSUPPORTED
+    assert b"groups" in lib.wpk_last_error()

@@ -32,7 +32,28 @@ NETS = {
     "resnet50_f32_n8": (lambda: workloads.resnet50(8), "f32", "ga"),   # exact-fp32 CUDA-core path
     "resnext50_grouped_bf16_n8": (lambda: workloads.resnext50_grouped(8), "bf16", "ga"),   # general groups (SIMT)
     "resnext50_grouped_f32_n8": (lambda: workloads.resnext50_grouped(8), "f32", "ga"),
+    # NEXT-4: e4m3 operands / bf16 output (tcgen05 kind::f8f6f4). cuDNN has no fp8 conv through torch:
+    # the competitor columns are cuDNN bf16 and our own tuned bf16 kernel on the same (rounded) inputs
+    "resnet50_fp8": (lambda: workloads.resnet50(32), "fp8", "ga"),
 }
+
+
+def _fp8_row(i, L, plan, res, budget):
+    """Own e4m3 kernel vs own bf16 kernel vs cuDNN bf16, all with the selector protocol."""
+    x, w, b = workloads.generate(L, "fp8", "uniform", seed=workloads.config_seed(2, i))
+    xd = x.permute(0, 2, 3, 1).contiguous().cuda()
+    wd = w.permute(0, 2, 3, 1).contiguous().cuda()
+    bd = b.cuda()
+    yd = torch.empty(plan.y_shape(), dtype=torch.bfloat16, device="cuda")
+    xs = selector.rotating_copies(xd, yd.numel() * yd.element_size())
+    ys = [yd] + [torch.empty_like(yd) for _ in xs[1:]]
+    own = selector.time_rotating([lambda i=i: plan.run(xs[i], wd, bd, ys[i]) for i in range(len(xs))])
+    # the same layer in bf16 (own tuned kernel, cuDNN) on the e4m3 values widened to bf16 (exact)
+    p16 = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups, layout="nhwc", dtype="bf16")
+    p16.tune("ga", budget, seed=i)
+    x16, w16 = xd.to(torch.bfloat16), wd.to(torch.bfloat16)
+    sel = selector.select(p16, x16, w16, bd, torch.empty_like(yd), L.stride, L.pad, L.dil, L.groups)
+    return own, sel, xd, wd, bd, yd
 
 
 def run_net(name, budget):
@@ -50,19 +71,26 @@ def run_net(name, budget):
             kw.update(rl_envs=4, rl_horizon=16)
         res = plan.tune(search if fam != 2 else "ga", budget, **kw)
         t_tune += time.perf_counter() - t0
-        x, w, b = workloads.generate(L, dtype, "uniform", seed=workloads.config_seed(2, i))
-        xd = x.permute(0, 2, 3, 1).contiguous().cuda()
-        wd = w.permute(0, 2, 3, 1).contiguous().cuda()
-        bd = b.cuda()
-        yd = torch.empty(plan.y_shape(), dtype=xd.dtype, device="cuda")
-        sel = selector.select(plan, xd, wd, bd, yd, L.stride, L.pad, L.dil, L.groups)
+        extra = {}
+        if dtype == "fp8":
+            own, sel16, xd, wd, bd, yd = _fp8_row(i, L, plan, res, budget)
+            sel = selector.Selection(own, sel16.cudnn_us, sel16.cudnn_variant + " (bf16)",
+                                     "wpk" if own <= sel16.cudnn_us else "cudnn")
+            extra = {"bf16_wpk_us": sel16.own_us, "fp8_speedup_vs_own_bf16": sel16.own_us / own}
+        else:
+            x, w, b = workloads.generate(L, dtype, "uniform", seed=workloads.config_seed(2, i))
+            xd = x.permute(0, 2, 3, 1).contiguous().cuda()
+            wd = w.permute(0, 2, 3, 1).contiguous().cuda()
+            bd = b.cuda()
+            yd = torch.empty(plan.y_shape(), dtype=xd.dtype, device="cuda")
+            sel = selector.select(plan, xd, wd, bd, yd, L.stride, L.pad, L.dil, L.groups)
         fl = 2 * L.n * L.k * plan.p * plan.q * (L.c // L.groups) * L.r * L.s
-        e = xd.element_size()
-        by = e * (xd.numel() + wd.numel() + bd.numel() + yd.numel())
-        # f32 runs on the CUDA cores: 148 SMs x 128 FP32 lanes x 2 flop/FMA x max SM clock (74.4 TF/s)
+        by = (xd.element_size() * (xd.numel() + wd.numel()) + yd.element_size() * (bd.numel() + yd.numel()))
+        # f32 runs on the CUDA cores: 148 SMs x 128 FP32 lanes x 2 flop/FMA x max SM clock (74.4 TF/s);
+        # tf32 = half and fp8 = twice the measured bf16 figure (the guide's nominal ratios)
         peak_tf = (148 * 128 * 2 * PEAKS["sm_max_mhz"] / 1e6 if dtype == "f32"
-                   else PEAKS["bf16_tflops"] * (0.5 if dtype == "tf32" else 1.0))
-        rows.append({"layer": L.name, "count": L.count, "n": L.n, "dtype": dtype, "family": res.family,
+                   else PEAKS["bf16_tflops"] * {"tf32": 0.5, "fp8": 2.0}.get(dtype, 1.0))
+        rows.append({"layer": L.name, "count": L.count, "n": L.n, "dtype": dtype, "family": res.family, **extra,
                      "config": res.genes, "wpk_us": sel.own_us, "cudnn_us": sel.cudnn_us,
                      "cudnn_variant": sel.cudnn_variant, "speedup_vs_cudnn": sel.cudnn_us / sel.own_us,
                      "selector": sel.choice, "gflop": fl / 1e9, "mbytes": by / 1e6,

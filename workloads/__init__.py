@@ -179,18 +179,29 @@ def config_seed(config_id: int, layer_index: int) -> int:
     return 4567 + 1000 * config_id + layer_index
 
 
-_DT = {"f32": torch.float32, "tf32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}
+# element type of b / z / y per dtype name; x and w use _DT_IN ("fp8" = OCP e4m3 operands with a
+# bf16 bias and output, the library's WPK_FP8E4M3)
+_DT = {"f32": torch.float32, "tf32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16,
+       "fp8": torch.bfloat16}
+_DT_IN = dict(_DT, fp8=torch.float8_e4m3fn)
 
 
 def torch_dtype(dtype: str) -> torch.dtype:
+    """Element type of b / z / y for `dtype` (x / w: torch_in_dtype)."""
     return _DT[dtype]
+
+
+def torch_in_dtype(dtype: str) -> torch.dtype:
+    return _DT_IN[dtype]
 
 
 def generate(layer: ConvLayer, dtype: str = "f32", mode: str = "uniform", seed: int = 0,
              bias: bool = True):
     """Seeded CPU tensors in canonical NCHW / KCRS layout, already rounded to `dtype`.
 
-    Returns (x[N,C,H,W], w[K,C/g,R,S], b[K] or None), all torch CPU tensors of the torch dtype.
+    Returns (x[N,C,H,W], w[K,C/g,R,S], b[K] or None), torch CPU tensors: x and w of
+    torch_in_dtype(dtype), b of torch_dtype(dtype) (they differ only for "fp8"). The fp32 draws are
+    rounded to nearest by torch's cast; the uniform ranges stay inside e4m3's finite range (|v| <= 1).
     """
     g = torch.Generator().manual_seed(int(seed))
     cpg = layer.c // layer.groups
@@ -212,8 +223,8 @@ def generate(layer: ConvLayer, dtype: str = "f32", mode: str = "uniform", seed: 
         b = torch.zeros(layer.k)
     else:
         raise ValueError(mode)
-    dt = _DT[dtype]
-    return x.to(dt), w.to(dt), (b.to(dt) if bias else None)
+    dt, it = _DT[dtype], _DT_IN[dtype]
+    return x.to(it), w.to(it), (b.to(dt) if bias else None)
 
 
 def random_points(layer: ConvLayer, p: int, q: int, count: int, seed: int):
