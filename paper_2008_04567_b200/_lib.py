@@ -96,6 +96,8 @@ def load():
         "wpk_conv2d_measure": (I32, [P, I32, I32, I32, DP]),
         "wpk_conv2d_run": (I32, [P, P, P, P, P, P]),
         "wpk_conv2d_run_residual": (I32, [P, P, P, P, P, P, P]),
+        "wpk_dwpw_plan": (I32, [ctypes.POINTER(Shape), I32, I32, I32, ctypes.c_int, ctypes.POINTER(P)]),
+        "wpk_dwpw_run": (I32, [P, P, P, P, P, P, P, P]),
         "wpk_conv2d_fold_batchnorm": (I32, [P, P, P, P, P, P, P, ctypes.c_float, P, P, P]),
         "wpk_conv2d_run_host": (I32, [P, P, P, P, P, P]),
         "wpk_conv2d_run_host_async": (I32, [P, P, P, P, P, P]),

@@ -240,6 +240,65 @@ class Conv2dPlan:
         return TuneResult(fam, genes, best.value, meas.value, rounds.value, secs.value)
 
 
+class DwPwPlan(Conv2dPlan):
+    """Fused depthwise + pointwise convolution (wpk_dwpw_plan / wpk_dwpw_run; SURVEY.md 8(f) NEXT-4,
+    the MobileNet block): y = pw_epilogue(RN(dw_epilogue(dwconv(x, w_dw) + b_dw)) (*) w_pw + b_pw) in
+    one tcgen05 kernel. NHWC only: x [N,H,W,C], w_dw [C,R,S] (or [C,R,S,1] / [C,1,R,S]), b_dw [C],
+    w_pw [K,C] (or [K,1,1,C] / [K,C,1,1]), b_pw [K], y [N,P,Q,K]. Tuning, configs and the workspace
+    go through the inherited Conv2dPlan calls."""
+
+    def __init__(self, n, c, h, w, k_out, r=3, s=3, stride=1, pad=1, dil=1, dw_epilogue="bias_relu",
+                 pw_epilogue="bias", dtype="bf16", device: int | None = None):
+        self.lib = L.load()
+        self.dtype, self.layout, self.epilogue = dtype, "nhwc", pw_epilogue
+        self.dw_epilogue = dw_epilogue
+        self.device = torch.cuda.current_device() if device is None else device
+        self.shape = L.make_shape(n, c, h, w, c, r, s, stride, pad, dil, c, "nhwc", dw_epilogue)
+        self.n, self.c, self.h, self.w, self.k, self.r, self.s = n, c, h, w, k_out, r, s
+        self.groups = 1
+        h_ = ctypes.c_void_p()
+        L.check(self.lib.wpk_dwpw_plan(ctypes.byref(self.shape), int(k_out), L.EPILOGUES[pw_epilogue],
+                                       L.DTYPES[dtype], self.device, ctypes.byref(h_)))
+        self.handle = h_
+        self.p, self.q = output_dims(n, c, h, w, c, r, s, stride, pad, dil, c)
+        self._ws = None
+        self._ws_bytes = -1
+        self._tdt = self._idt = _TORCH_DT[dtype]
+        self._xs, self._ys = torch.Size((n, h, w, c)), torch.Size((n, self.p, self.q, k_out))
+        self._hval = self.handle.value
+
+    def x_shape(self):
+        return tuple(self._xs)
+
+    def y_shape(self):
+        return tuple(self._ys)
+
+    def run(self, x, w_dw, b_dw, w_pw, b_pw, y=None, stream=None, z=None):
+        dt = self._tdt
+        checks = ((x, "x", self.n * self.h * self.w * self.c), (w_dw, "w_dw", self.c * self.r * self.s),
+                  (w_pw, "w_pw", self.k * self.c))
+        if tuple(x.shape) != tuple(self._xs):
+            raise ValueError(f"x: expected shape {tuple(self._xs)}, got {tuple(x.shape)}")
+        for t, nm, numel in checks:
+            if t.dtype is not dt or t.numel() != numel or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{nm}: expected contiguous cuda {dt} with {numel} elements, got {t.dtype} "
+                                 f"{tuple(t.shape)}")
+        for t, nm, numel in ((b_dw, "b_dw", self.c), (b_pw, "b_pw", self.k)):
+            if t is not None and (t.dtype is not dt or t.numel() != numel or not t.is_cuda or not t.is_contiguous()):
+                raise ValueError(f"{nm}: expected contiguous cuda {dt} [{numel}]")
+        if y is None:
+            y = torch.empty(self._ys, dtype=dt, device=x.device)
+        elif y.dtype is not dt or y.shape != self._ys or not y.is_cuda or not y.is_contiguous():
+            raise ValueError(f"y: expected contiguous cuda {dt} of shape {tuple(self._ys)}")
+        if self._ws_bytes < 0:
+            self._ensure_workspace()
+        s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        ptr = (lambda t: t.data_ptr() if t is not None else None)
+        L.check(self.lib.wpk_dwpw_run(self._hval, x.data_ptr(), w_dw.data_ptr(), ptr(b_dw), w_pw.data_ptr(),
+                                      ptr(b_pw), y.data_ptr(), s))
+        return y
+
+
 def make_options(**kw) -> L.TuneOptions:
     """wpk_tune_options with defaults, overridden by keyword arguments (field names of wpk.h)."""
     o = L.TuneOptions()

@@ -111,6 +111,117 @@ __global__ void dw_conv_kernel(const DwArgs a) {
     }
 }
 
+// Depthwise 3x3, NHWC, 16-bit data, 16-byte channel vectors (the VEC_C = 8 instantiations of the
+// common MobileNet case: dilation 1, stride SW in {1, 2}, C % 8 == 0, < 2^31 work items). The same
+// definition and per-output order as dw_conv_kernel -- taps in (r, s) order, one fp32 FMA each, the
+// bias after the sum -- with the memory traffic of a sliding window: a thread's PIX consecutive
+// outputs of one row need (PIX-1)*SW + 3 input columns per filter row, each loaded once (16 B) and
+// reused by every tap that reads it; two channels per FFMA2 (bit-identical to two FFMAs); 32-bit
+// index arithmetic. Consecutive threads take consecutive channel vectors of one pixel (coalesced).
+__device__ __forceinline__ float2 dw_up2(uint32_t u, __nv_bfloat16 *) {
+    return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
+}
+__device__ __forceinline__ float2 dw_up2(uint32_t u, __half *) {
+    return __half22float2(*reinterpret_cast<const __half2 *>(&u));
+}
+__device__ __forceinline__ void dw_ffma2(float2 &acc, float2 a, float2 b) {
+    unsigned long long c = *reinterpret_cast<unsigned long long *>(&acc);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;"
+        : "+l"(c)
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)), "l"(*reinterpret_cast<unsigned long long *>(&b)));
+    acc = *reinterpret_cast<float2 *>(&c);
+}
+__device__ __forceinline__ uint32_t dw_pack2(float a, float b, __nv_bfloat16 *) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ uint32_t dw_pack2(float a, float b, __half *) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+
+template <typename T, int PIX, int SW>
+__global__ void dw3_nhwc_kernel(const DwArgs a) {
+    constexpr int NCOL = (PIX - 1) * SW + 3;
+    const uint4 *__restrict__ x = static_cast<const uint4 *>(a.x);
+    const uint4 *__restrict__ wp = static_cast<const uint4 *>(a.w);   // [3][3][C] in 16-byte vectors
+    const uint4 *__restrict__ b = static_cast<const uint4 *>(a.b);
+    const uint4 *__restrict__ z = static_cast<const uint4 *>(a.z);
+    uint4 *__restrict__ y = static_cast<uint4 *>(a.y);
+    const int cvecs = a.C >> 3;
+    const int qblocks = (a.Q + PIX - 1) / PIX;
+    const int total = a.N * a.P * qblocks * cvecs;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int cv = idx % cvecs;
+        int t = idx / cvecs;
+        const int qb = t % qblocks;
+        t /= qblocks;
+        const int p = t % a.P;
+        const int n = t / a.P;
+        const int q0 = qb * PIX;
+        const int w0 = q0 * SW - a.pw;
+        float2 acc[PIX][4];
+#pragma unroll
+        for (int i = 0; i < PIX; ++i)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[i][e] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const int hi = p * a.sh - a.ph + r;
+            if (hi < 0 || hi >= a.H) continue;
+            const uint4 *xr = x + (size_t)((n * a.H + hi) * a.W) * cvecs + cv;
+            uint4 col[NCOL];
+#pragma unroll
+            for (int c = 0; c < NCOL; ++c) {
+                const int wi = w0 + c;
+                col[c] = (wi >= 0 && wi < a.W) ? __ldg(xr + (size_t)wi * cvecs) : make_uint4(0u, 0u, 0u, 0u);
+            }
+#pragma unroll
+            for (int s = 0; s < 3; ++s) {
+                const uint4 wv = __ldg(wp + (size_t)(r * 3 + s) * cvecs + cv);
+                const float2 w0f = dw_up2(wv.x, (T *)nullptr), w1f = dw_up2(wv.y, (T *)nullptr);
+                const float2 w2f = dw_up2(wv.z, (T *)nullptr), w3f = dw_up2(wv.w, (T *)nullptr);
+#pragma unroll
+                for (int i = 0; i < PIX; ++i) {
+                    const uint4 xv = col[i * SW + s];
+                    dw_ffma2(acc[i][0], dw_up2(xv.x, (T *)nullptr), w0f);
+                    dw_ffma2(acc[i][1], dw_up2(xv.y, (T *)nullptr), w1f);
+                    dw_ffma2(acc[i][2], dw_up2(xv.z, (T *)nullptr), w2f);
+                    dw_ffma2(acc[i][3], dw_up2(xv.w, (T *)nullptr), w3f);
+                }
+            }
+        }
+        float2 bf[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        if (a.epilogue >= 1) {
+            const uint4 bv = __ldg(b + cv);
+            bf[0] = dw_up2(bv.x, (T *)nullptr); bf[1] = dw_up2(bv.y, (T *)nullptr);
+            bf[2] = dw_up2(bv.z, (T *)nullptr); bf[3] = dw_up2(bv.w, (T *)nullptr);
+        }
+#pragma unroll
+        for (int i = 0; i < PIX; ++i) {
+            const int q = q0 + i;
+            if (q >= a.Q) break;
+            const size_t yo = (size_t)((n * a.P + p) * a.Q + q) * cvecs + cv;
+            float2 zf[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            if (a.epilogue == 3) {
+                const uint4 zv = __ldg(z + yo);
+                zf[0] = dw_up2(zv.x, (T *)nullptr); zf[1] = dw_up2(zv.y, (T *)nullptr);
+                zf[2] = dw_up2(zv.z, (T *)nullptr); zf[3] = dw_up2(zv.w, (T *)nullptr);
+            }
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float v0 = acc[i][e].x, v1 = acc[i][e].y;
+                if (a.epilogue >= 1) { v0 += bf[e].x; v1 += bf[e].y; }
+                if (a.epilogue == 3) { v0 += zf[e].x; v1 += zf[e].y; }
+                if (a.epilogue >= 2) { v0 = fmaxf(v0, 0.f); v1 = fmaxf(v1, 0.f); }
+                o[e] = dw_pack2(v0, v1, (T *)nullptr);
+            }
+            y[yo] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+}
+
 // General groups (1 < g, C/g or K/g > 1), the same thread layout with the
 // vector over VEC consecutive OUTPUT channels of one group (K/g % VEC == 0): every output of the
 // thread reads the same C/g input channels of its group, so each activation is loaded once per
@@ -232,9 +343,32 @@ __global__ void grouped_conv_kernel(const DwArgs a) {
     }
 }
 
+// the sliding-window 3x3 NHWC kernel applies (else the generic dw_conv_kernel)
+static bool dw3_fast_ok(const DwArgs &a, int elem, int vec) {
+    if (elem != 2 || vec != 8 || a.Cpg > 0 || a.C % 8 || a.xs_c != 1 || a.ys_c != 1) return false;
+    if (a.R != 3 || a.S != 3 || a.dh != 1 || a.dw != 1 || (a.sw != 1 && a.sw != 2)) return false;
+    if (a.xs_w != a.C || a.ys_q != a.C) return false;   // dense NHWC
+    return (double)a.N * a.P * a.Q * (a.C / 8) < 2.0e9 && (double)a.N * a.H * a.W * a.C < 2.0e9;
+}
+
 template <typename T, int VEC>
 static int dw_launch_pix(const DwArgs &a, int pix, int threads, long long blocks, cudaStream_t st) {
     const bool grouped = a.Cpg > 0;
+    if constexpr (VEC == 8 && sizeof(T) == 2) {
+        if (dw3_fast_ok(a, 2, VEC)) {
+#define WPK_DW3(P)                                                                                   \
+    if (a.sw == 1) dw3_nhwc_kernel<T, P, 1><<<(unsigned)blocks, threads, 0, st>>>(a);                 \
+    else dw3_nhwc_kernel<T, P, 2><<<(unsigned)blocks, threads, 0, st>>>(a);                         \
+    return 0;
+            switch (pix) {
+            case 1: WPK_DW3(1)
+            case 2: WPK_DW3(2)
+            case 4: WPK_DW3(4)
+            }
+#undef WPK_DW3
+            return -1;
+        }
+    }
 #define WPK_DWL(P)                                                                                   \
     if (grouped) grouped_conv_kernel<T, VEC, P><<<(unsigned)blocks, threads, 0, st>>>(a);          \
     else dw_conv_kernel<T, VEC, P><<<(unsigned)blocks, threads, 0, st>>>(a);                        \

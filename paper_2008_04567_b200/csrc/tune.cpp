@@ -563,7 +563,9 @@ static std::string cache_key(const Plan &p, int family, int measured_mode) {
     }
     snprintf(b, sizeof b, "n%d_c%d_h%d_w%d_k%d_r%d_s%d_st%dx%d_p%dx%d_d%dx%d_g%d_l%d_e%d_t%d_f%d_", d.n, d.c, d.h, d.w,
              d.k, d.r, d.s, d.sh, d.sw, d.ph, d.pw, d.dh, d.dw, d.g, d.layout, d.epilogue, d.dtype, family);
-    return std::string(b) + dev + "_abi" + std::to_string(WPK_ABI_VERSION);
+    std::string key(b);
+    if (d.fused_dw) key += "dwpw" + std::to_string(d.dw_epi) + "_";   // fused depthwise+pointwise operator
+    return key + dev + "_abi" + std::to_string(WPK_ABI_VERSION);
 }
 
 static bool cache_lookup(const std::string &path, int budget, Config *cfg, double *beta) {

@@ -793,11 +793,124 @@ __device__ __forceinline__ void element_gather(const UmmaArgs &a, uint8_t *smA, 
 // depthwise conv, K = its C channels -- is computed here, never stored to global memory:
 //   a[m][c] = RN_T(dw_epilogue(sum_{r,s} x[n][p*sh - ph + r*dh][q*sw - pw + s*dw][c] * w_dw[r][s][c] + b_dw[c]))
 // (fp32 products and sum in (r, s) order, the bias added after the sum, one rounding to the I/O
-// dtype: what the unfused depthwise conv stores). NHWC x, C % 8 == 0, 16-bit T. Thread t of the 4
-// producer warps owns rows t and 128 + t of every stage: per K block it accumulates the 64 channels
-// of its pixel over the taps (16-byte vector loads of x and of the [R][S][C] weights, the latter
-// the same address across the warp), applies bias / ReLU, converts and writes the 128-byte row
-// into the swizzled stage; channels >= C and rows >= M are written as zeros.
+// dtype: what the unfused depthwise conv stores). NHWC x, C % 8 == 0, 16-bit T.
+// Work split: a K block is rows x 8 channel vectors (16 B = 8 channels each); thread t of the 4
+// producer warps owns vector j = t & 7 of rows (t >> 3) + 16 i, so the 8 threads of a row read
+// its 128 contiguous bytes per tap (one L1 line: a warp touches 4 lines per load instead of 32).
+// The tap's weight vector is the same for all rows of the thread: loaded once per K block (3x3:
+// kept in registers). Two rows are in flight per iteration; rows >= M and channels >= C are
+// written as zeros.
+// 16-bit pair -> two fp32 (exact): bf16 is the high half of an fp32; fp16 via the converter
+__device__ __forceinline__ float2 up2(uint32_t u, __nv_bfloat16 *) {
+    return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
+}
+__device__ __forceinline__ float2 up2(uint32_t u, __half *) {
+    return __half22float2(*reinterpret_cast<const __half2 *>(&u));
+}
+// acc.{x,y} = fma(a.{x,y}, b.{x,y}, acc.{x,y}) in one FFMA2 (each lane rounds once, as fmaf)
+__device__ __forceinline__ void ffma2(float2 &acc, float2 a, float2 b) {
+    unsigned long long c = *reinterpret_cast<unsigned long long *>(&acc);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;"
+        : "+l"(c)
+        : "l"(*reinterpret_cast<unsigned long long *>(&a)), "l"(*reinterpret_cast<unsigned long long *>(&b)));
+    acc = *reinterpret_cast<float2 *>(&c);
+}
+// acc[0..3] += x[8 channels] * w[8 channels] (16-byte vectors of 16-bit values)
+template <typename T>
+__device__ __forceinline__ void mac8(float2 *acc, uint4 x, uint4 w) {
+    ffma2(acc[0], up2(x.x, (T *)nullptr), up2(w.x, (T *)nullptr));
+    ffma2(acc[1], up2(x.y, (T *)nullptr), up2(w.y, (T *)nullptr));
+    ffma2(acc[2], up2(x.z, (T *)nullptr), up2(w.z, (T *)nullptr));
+    ffma2(acc[3], up2(x.w, (T *)nullptr), up2(w.w, (T *)nullptr));
+}
+
+template <typename T, int R3>
+__device__ __forceinline__ void dw_rows(const UmmaArgs &a, uint32_t sbase, int mbase, int nrows, int t, int c0,
+                                       const uint4 *__restrict__ xv, const uint4 *__restrict__ wv,
+                                       const uint4 *__restrict__ bv) {
+    const int cv = a.C >> 3;
+    const int j = t & 7;
+    const int cvec = c0 + j;
+    const bool cok = cvec < cv;
+    const uint4 *wj = wv + cvec;   // tap i's weight vector: wj[i * cv] (an L1 hit shared by the row's threads)
+    const uint4 *xj = xv + cvec;
+    const int M = (int)a.M, PQ = (int)a.PQ;   // < 2^31 (plan validation)
+    uint32_t bb[4] = {0u, 0u, 0u, 0u};
+    if (bv && cok) {
+        const uint4 b4 = __ldg(bv + cvec);
+        bb[0] = b4.x; bb[1] = b4.y; bb[2] = b4.z; bb[3] = b4.w;
+    }
+#pragma unroll 1
+    for (int row0 = (t >> 3); row0 < nrows; row0 += 32) {
+        float2 acc[2][4];
+        bool ok[2];
+        uint4 xx[2][R3 ? 9 : 1];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int row = row0 + 16 * u;
+            const int m = mbase + row;
+            ok[u] = row < nrows && m < M && cok;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[u][e] = make_float2(0.f, 0.f);
+            const int mm = ok[u] ? m : 0;
+            const int n = mm / PQ;
+            const int rem = mm - n * PQ;
+            const int p = rem / a.Q, q = rem - p * a.Q;
+            const int h0 = p * a.stride_h - a.pad_h, w0 = q * a.stride_w - a.pad_w;
+            const int nh = n * a.H;
+            if constexpr (R3 != 0) {   // all 9 taps' loads issued before any math
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                    for (int s = 0; s < 3; ++s) {
+                        const int hi = h0 + r * a.dil_h, wi = w0 + s * a.dil_w;
+                        xx[u][r * 3 + s] = (ok[u] && hi >= 0 && hi < a.H && wi >= 0 && wi < a.W)
+                                               ? __ldg(xj + (size_t)((nh + hi) * a.W + wi) * cv)
+                                               : make_uint4(0u, 0u, 0u, 0u);
+                    }
+            } else if (ok[u]) {
+#pragma unroll 1
+                for (int r = 0; r < a.R; ++r) {
+                    const int hi = h0 + r * a.dil_h;
+                    if (hi < 0 || hi >= a.H) continue;
+#pragma unroll 1
+                    for (int s = 0; s < a.S; ++s) {
+                        const int wi = w0 + s * a.dil_w;
+                        if (wi < 0 || wi >= a.W) continue;
+                        mac8<T>(acc[u], __ldg(xj + (size_t)((nh + hi) * a.W + wi) * cv),
+                                __ldg(wj + (size_t)(r * a.S + s) * cv));
+                    }
+                }
+            }
+        }
+        if constexpr (R3 != 0) {
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+                const uint4 wq = cok ? __ldg(wj + (size_t)i * cv) : make_uint4(0u, 0u, 0u, 0u);
+                mac8<T>(acc[0], xx[0][i], wq);
+                mac8<T>(acc[1], xx[1][i], wq);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int row = row0 + 16 * u;
+            if (row >= nrows) break;
+            uint32_t o[4] = {0u, 0u, 0u, 0u};
+            if (ok[u]) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 bf = up2(bb[e], (T *)nullptr);
+                    float v0 = acc[u][e].x + bf.x, v1 = acc[u][e].y + bf.y;
+                    if (a.dw_relu) { v0 = fmaxf(v0, 0.f); v1 = fmaxf(v1, 0.f); }
+                    o[e] = pack2(v0, v1, (T *)nullptr);
+                }
+            }
+            const uint32_t rbase = sbase + (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u;
+            ptx::st_shared_v4(rbase + ((uint32_t)(j ^ (row & 7)) << 4), o[0], o[1], o[2], o[3]);
+        }
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void dw_producer(const UmmaArgs &a, uint8_t *smA, uint32_t a_bytes, uint64_t *full,
                                            uint64_t *empty, int nsub, long long wstart, long long wstep, int t,
@@ -805,82 +918,18 @@ __device__ __forceinline__ void dw_producer(const UmmaArgs &a, uint8_t *smA, uin
     const uint4 *xv = reinterpret_cast<const uint4 *>(a.x);
     const uint4 *wv = reinterpret_cast<const uint4 *>(a.dw_w);
     const uint4 *bv = reinterpret_cast<const uint4 *>(a.dw_b);
-    const int cv = a.C >> 3;                                    // 16-byte vectors per pixel
+    const bool r3 = a.R == 3 && a.S == 3;
     uint32_t stage = 0, phase = 0;
     for (long long w = wstart; w < a.work; w += wstep) {
         const WorkPos wp = decode_work(w, a);
         const int kb0 = wp.split * a.kb_per_split;
         const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
-        int rh0[2], rw0[2], rn[2];
-        bool rv[2];
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-            const long long m = (long long)wp.mt * a.bm + hh * 128 + t;
-            rv[hh] = hh < nsub && m < a.M;
-            const long long mm = rv[hh] ? m : 0;
-            const int n = (int)(mm / a.PQ);
-            const int rem = (int)(mm - (long long)n * a.PQ);
-            const int p = rem / a.Q, q = rem - (rem / a.Q) * a.Q;
-            rn[hh] = n;
-            rh0[hh] = p * a.stride_h - a.pad_h;
-            rw0[hh] = q * a.stride_w - a.pad_w;
-        }
+        const int mbase = wp.mt * a.bm;
         for (int kb = kb0; kb < kb1; ++kb) {
             ptx::mbar_wait(&empty[stage], phase ^ 1);
-            const int c0 = kb * 8;                              // first 16-byte channel vector of the block
-#pragma unroll 1
-            for (int hh = 0; hh < 2; ++hh) {
-                if (hh >= nsub) break;
-                const int row = hh * 128 + t;
-                const uint32_t rbase = ptx::smem_u32(smA + stage * a_bytes) + (uint32_t)(row >> 3) * 1024u +
-                                       (uint32_t)(row & 7) * 128u;
-                float acc[64];
-#pragma unroll
-                for (int i = 0; i < 64; ++i) acc[i] = 0.f;
-                if (rv[hh]) {
-#pragma unroll 1
-                    for (int r = 0; r < a.R; ++r) {
-                        const int hi = rh0[hh] + r * a.dil_h;
-                        if (hi < 0 || hi >= a.H) continue;
-#pragma unroll 1
-                        for (int s = 0; s < a.S; ++s) {
-                            const int wi = rw0[hh] + s * a.dil_w;
-                            if (wi < 0 || wi >= a.W) continue;
-                            const uint4 *xp = xv + ((long long)(rn[hh] * a.H + hi) * a.W + wi) * cv;
-                            const uint4 *wt = wv + (long long)(r * a.S + s) * cv;
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                if (c0 + j >= cv) break;
-                                const uint4 xx = __ldg(xp + c0 + j), ww = __ldg(wt + c0 + j);
-                                const uint32_t xs[4] = {xx.x, xx.y, xx.z, xx.w}, ws[4] = {ww.x, ww.y, ww.z, ww.w};
-#pragma unroll
-                                for (int e = 0; e < 8; ++e)
-                                    acc[j * 8 + e] = fmaf(to_f2(xs[e >> 1], e & 1, (T *)nullptr),
-                                                          to_f2(ws[e >> 1], e & 1, (T *)nullptr), acc[j * 8 + e]);
-                            }
-                        }
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    uint32_t o[4] = {0u, 0u, 0u, 0u};
-                    if (rv[hh] && c0 + j < cv) {
-                        uint32_t bb[4] = {0u, 0u, 0u, 0u};
-                        if (bv) {
-                            const uint4 b4 = __ldg(bv + c0 + j);
-                            bb[0] = b4.x; bb[1] = b4.y; bb[2] = b4.z; bb[3] = b4.w;
-                        }
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            float v0 = acc[j * 8 + 2 * e] + to_f2(bb[e], 0, (T *)nullptr);
-                            float v1 = acc[j * 8 + 2 * e + 1] + to_f2(bb[e], 1, (T *)nullptr);
-                            if (a.dw_relu) { v0 = fmaxf(v0, 0.f); v1 = fmaxf(v1, 0.f); }
-                            o[e] = pack2(v0, v1, (T *)nullptr);
-                        }
-                    }
-                    ptx::st_shared_v4(rbase + ((uint32_t)(j ^ (row & 7)) << 4), o[0], o[1], o[2], o[3]);
-                }
-            }
+            const uint32_t sbase = ptx::smem_u32(smA + stage * a_bytes);
+            if (r3) dw_rows<T, 3>(a, sbase, mbase, nsub * 128, t, kb * 8, xv, wv, bv);
+            else dw_rows<T, 0>(a, sbase, mbase, nsub * 128, t, kb * 8, xv, wv, bv);
             ptx::fence_proxy_async_smem();                 // generic-proxy writes -> async-proxy (MMA) reads
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&full[stage]);

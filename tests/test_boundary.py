@@ -205,3 +205,43 @@ def test_fp8_plans_host_validation():
                   dtype="fp8")
     assert st == L.ERR_UNSUPPORTED
     assert b"groups" in lib.wpk_last_error()
+
+
+def test_dwpw_plan_host_validation():
+    """wpk_dwpw_plan (fused depthwise + pointwise): shape / layout / dtype / channel checks, the
+    default config (tcgen05, A_MODE 0 = the depthwise producer, no pairs) and the run-entry guards
+    (host logic: no GPU needed)."""
+    lib = L.load()
+
+    def plan(c=144, k=24, groups=None, layout="nhwc", dtype="bf16", epi="bias_relu", pw=1):
+        shp = L.make_shape(n=1, c=c, h=14, w=14, k=c, r=3, s=3, stride=1, pad=1,
+                           groups=c if groups is None else groups, layout=layout, epilogue=epi)
+        h = ctypes.c_void_p()
+        return lib.wpk_dwpw_plan(ctypes.byref(shp), k, pw, L.DTYPES[dtype], 0, ctypes.byref(h)), h
+
+    st, h = plan()
+    assert st == 0, L.last_error()
+    fam, g = ctypes.c_int32(), (ctypes.c_int32 * L.NUM_GENES)()
+    assert lib.wpk_conv2d_get_config(h, ctypes.byref(fam), g) == 0
+    assert fam.value == 1 and g[4] == 0 and (g[3] >> 1) & 3 == 0
+    assert lib.wpk_conv2d_config_valid(h, 1, (ctypes.c_int32 * L.NUM_GENES)(64, 4, 2, 1, 0, 2, 256)) == 1
+    assert lib.wpk_conv2d_config_valid(h, 1, (ctypes.c_int32 * L.NUM_GENES)(64, 4, 1, 2, 0, 2, 256)) == 0   # pair
+    assert lib.wpk_conv2d_config_valid(h, 1, (ctypes.c_int32 * L.NUM_GENES)(64, 4, 1, 0, 4, 2, 128)) == 0   # A_MODE 4
+    assert lib.wpk_conv2d_config_valid(h, 0, (ctypes.c_int32 * L.NUM_GENES)(16, 4, 4, 1, 1, 1, 1)) == 0     # SIMT
+    # the plain run entry points refuse a fused plan (before touching any pointer)
+    assert lib.wpk_conv2d_run(h, 16, 16, 16, 16, None) == L.ERR_INVALID_ARGUMENT
+    assert b"wpk_dwpw_run" in lib.wpk_last_error()
+    lib.wpk_conv2d_destroy(h)
+    assert plan(groups=1)[0] == L.ERR_SHAPE                      # first conv not depthwise
+    assert plan(k=0)[0] == L.ERR_SHAPE
+    assert plan(c=12)[0] == L.ERR_UNSUPPORTED                    # C % 8
+    assert plan(layout="nchw")[0] == L.ERR_UNSUPPORTED
+    assert plan(dtype="f32")[0] == L.ERR_UNSUPPORTED
+    assert plan(dtype="fp8")[0] == L.ERR_UNSUPPORTED
+    assert plan(epi="bias_add_relu")[0] == L.ERR_UNSUPPORTED
+    assert plan(pw=3)[0] == L.ERR_INVALID_ARGUMENT               # residual pointwise epilogue
+    # a plain conv plan refuses the fused run entry point
+    st, h = _plan(L.make_shape(n=1, c=16, h=8, w=8, k=16, r=3, s=3, stride=1, pad=1, layout="nhwc"))
+    assert st == 0
+    assert lib.wpk_dwpw_run(h, 16, 16, 16, 16, 16, 16, None) == L.ERR_INVALID_ARGUMENT
+    lib.wpk_conv2d_destroy(h)

@@ -258,6 +258,48 @@ def test_depthwise(dtype, layout):
                 assert_bit_exact(from_layout(yy.cpu(), layout), oracle_full(L, x, w, b))
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+def test_depthwise_nhwc_sliding_window(dtype):
+    """The NHWC 3x3 sliding-window depthwise kernel (VEC_C 8, 16-bit, stride 1 / 2) against the oracle
+    (exact-integer: bit-exact; uniform: tolerance) and against the generic kernel on the same inputs
+    (NCHW plan): the same per-output order (taps in (r, s) order, fp32 FMA, bias after the sum), so the
+    outputs are bit-identical up to the sign of zero. Ragged Q (not a multiple of PIX), every epilogue."""
+    from paper_2008_04567_b200 import Conv2dPlan
+    from _util import canon_bits, from_layout, to_layout
+    for L in [ConvLayer("mb", 2, 144, 19, 17, 144, 3, 3, 1, 1, 1, 144), ConvLayer("mbs2", 3, 96, 21, 23, 96, 3, 3, 2, 1, 1, 96),
+              ConvLayer("c8", 1, 8, 9, 11, 8, 3, 3, 1, 1, 1, 8)]:
+        for epi in ("none", "bias", "bias_relu", "bias_add_relu"):
+            for mode in ("int", "uniform"):
+                x, w, b = workloads.generate(L, dtype, mode, seed=17)
+                p, q = (L.h + 2 - 2 - 1) // L.stride + 1, (L.w + 2 - 2 - 1) // L.stride + 1
+                z = torch.randint(-3, 4, (L.n, L.k, p, q), generator=torch.Generator().manual_seed(18)).to(x.dtype)
+                bb = b if epi != "none" else None
+                if epi == "bias_add_relu":
+                    ref = oracle.conv2d(x, w, b, stride=L.stride, pad=1, groups=L.groups, residual=z)
+                else:
+                    ref = oracle.conv2d(x, w, bb, stride=L.stride, pad=1, groups=L.groups, relu=(epi == "bias_relu"))
+                outs = {}
+                for layout in ("nhwc", "nchw"):
+                    plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, 3, 3, L.stride, 1, 1, L.groups, layout=layout,
+                                      epilogue=epi, dtype=dtype)
+                    xl, wl = to_layout(x, w, layout)
+                    zl = z.permute(0, 2, 3, 1).contiguous() if layout == "nhwc" else z
+                    for pix in (1, 2, 4):
+                        plan.set_config(2, [8, pix, 128, 1, 0, 0, 0])
+                        y = plan.run(xl.cuda(), wl.cuda(), bb.cuda() if bb is not None else None,
+                                     z=zl.cuda() if epi == "bias_add_relu" else None)
+                        torch.cuda.synchronize()
+                        y = from_layout(y.cpu(), layout)
+                        if mode == "int":
+                            assert_bit_exact(y, ref)
+                        else:
+                            assert rel_error(dtype, y, ref) <= TOL[dtype]
+                        outs[(layout, pix)] = y
+                base = canon_bits(outs[("nchw", 1)])
+                for key, y in outs.items():
+                    assert torch.equal(canon_bits(y), base), (L.name, epi, mode, key)
+
+
 def test_run_host_matches_device():
     L = SMALL[1]
     x, w, b = workloads.generate(L, "bf16", "int", seed=17)

@@ -1,0 +1,110 @@
+"""Fused depthwise + pointwise (wpk_dwpw_*) vs the unfused chain on MobileNet-V2's 17 (dw 3x3 -> 1x1
+projection) pairs (workloads.mobilenet_v2_dwpw), bf16 NHWC, selector timing protocol (a CUDA graph
+over cold input copies, interquartile mean per call):
+  fused      one tcgen05 kernel, the depthwise result made in shared memory (GA-tuned)
+  unfused    our depthwise kernel (DW family, GA-tuned) -> bf16 t in HBM -> our tcgen05 1x1 (GA-tuned)
+  cudnn      cuDNN depthwise conv + ReLU -> cuDNN 1x1 conv (+ bias), channels_last, cudnn.benchmark
+Writes OUT.json + OUT.md.      python tools/dwpw_suite.py OUT [--n 1,32] [--budget 64]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import torch.nn.functional as F
+
+import workloads
+from paper_2008_04567_b200 import Conv2dPlan, DwPwPlan, selector
+
+
+def run_block(bi, B, budget):
+    L = B.dw
+    n, c, h, w, k = L.n, L.c, L.h, L.w, B.k_out
+    x, w_dw, b_dw = workloads.generate(L, "bf16", "uniform", seed=workloads.config_seed(4, bi))
+    pw = workloads.ConvLayer(B.name + ".project", n, c, 1, 1, k, 1, 1)
+    _, w_pw, b_pw = workloads.generate(pw, "bf16", "uniform", seed=workloads.config_seed(4, 100 + bi))
+    xd = x.permute(0, 2, 3, 1).contiguous().cuda()
+    wdw, bdw, wpw, bpw = w_dw.contiguous().cuda(), b_dw.cuda(), w_pw.contiguous().cuda(), b_pw.cuda()
+    fused = DwPwPlan(n, c, h, w, k, 3, 3, L.stride, 1, 1, dw_epilogue="bias_relu", pw_epilogue="bias", dtype="bf16")
+    rf = fused.tune("ga", budget, seed=bi)
+    pdw = Conv2dPlan(n, c, h, w, c, 3, 3, L.stride, 1, 1, c, layout="nhwc", dtype="bf16")
+    pdw.tune("ga", budget, seed=bi)
+    ppw = Conv2dPlan(n, c, pdw.p, pdw.q, k, 1, 1, 1, 0, layout="nhwc", epilogue="bias", dtype="bf16")
+    ppw.tune("ga", budget, seed=bi)
+    ybytes = n * pdw.p * pdw.q * k * 2
+    xs = selector.rotating_copies(xd, ybytes + n * pdw.p * pdw.q * c * 2)
+    ys = [torch.empty(fused.y_shape(), dtype=torch.bfloat16, device="cuda") for _ in xs]
+    ts = [torch.empty((n, pdw.p, pdw.q, c), dtype=torch.bfloat16, device="cuda") for _ in xs]
+    wdw_nhwc = w_dw.permute(0, 2, 3, 1).contiguous().cuda()
+    wpw_nhwc = w_pw.permute(0, 2, 3, 1).contiguous().cuda()
+    t_fused = selector.time_rotating([lambda i=i: fused.run(xs[i], wdw, bdw, wpw, bpw, ys[i]) for i in range(len(xs))])
+
+    def unf(i):
+        pdw.run(xs[i], wdw_nhwc, bdw, ts[i])
+        ppw.run(ts[i], wpw_nhwc, bpw, ys[i])
+    t_unf = selector.time_rotating([lambda i=i: unf(i) for i in range(len(xs))])
+    torch.backends.cudnn.benchmark = True
+    wdw4, wpw4 = w_dw.cuda().to(memory_format=torch.channels_last), w_pw.cuda().to(memory_format=torch.channels_last)
+
+    def cud_fused(i):
+        xt = xs[i].permute(0, 3, 1, 2)
+        t = torch.cudnn_convolution_relu(xt, wdw4, bdw, (L.stride, L.stride), (1, 1), (1, 1), c)
+        return F.conv2d(t, wpw4, bpw)
+
+    def cud_plain(i):
+        xt = xs[i].permute(0, 3, 1, 2)
+        return F.conv2d(F.relu_(F.conv2d(xt, wdw4, bdw, L.stride, 1, 1, c)), wpw4, bpw)
+    try:
+        cud_fused(0)
+        cud = cud_fused
+    except (RuntimeError, TypeError):
+        cud = cud_plain
+        cud(0)
+    t_cud = selector.time_rotating([lambda i=i: cud(i) for i in range(len(xs))])
+    byt_f = 2 * (xd.numel() + wdw.numel() + bdw.numel() + wpw.numel() + bpw.numel() + ys[0].numel())
+    byt_u = byt_f + 2 * 2 * ts[0].numel()     # + the intermediate written and read back
+    fl = 2 * n * pdw.p * pdw.q * c * (9 + k)
+    return {"block": B.name, "count": B.count, "n": n, "c": c, "hw": h, "stride": L.stride, "k_out": k,
+            "fused_us": t_fused, "unfused_us": t_unf, "cudnn_us": t_cud,
+            "fused_vs_unfused": t_unf / t_fused, "fused_vs_cudnn": t_cud / t_fused,
+            "mbytes_fused": byt_f / 1e6, "mbytes_unfused": byt_u / 1e6, "gflop": fl / 1e9,
+            "fused_gbs": byt_f / (t_fused * 1e-6) / 1e9, "fused_config": rf.genes}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("out")
+    ap.add_argument("--n", default="1,32")
+    ap.add_argument("--budget", type=int, default=64)
+    a = ap.parse_args()
+    res = []
+    for n in [int(v) for v in a.n.split(",")]:
+        rows = []
+        for bi, B in enumerate(workloads.mobilenet_v2_dwpw(n)):
+            rows.append(run_block(bi, B, a.budget))
+            print(json.dumps(rows[-1]), flush=True)
+        res.append({"n": n, "budget": a.budget, "blocks": rows,
+                    "sum_fused_us": sum(r["fused_us"] * r["count"] for r in rows),
+                    "sum_unfused_us": sum(r["unfused_us"] * r["count"] for r in rows),
+                    "sum_cudnn_us": sum(r["cudnn_us"] * r["count"] for r in rows)})
+    json.dump(res, open(a.out + ".json", "w"), indent=1)
+    with open(a.out + ".md", "w") as f:
+        for r in res:
+            f.write(f"\n### MobileNet-V2 dw 3x3 -> 1x1 projection pairs, N={r['n']}, bf16 NHWC (GA budget "
+                    f"{r['budget']} per plan; selector protocol, us per call)\n\n")
+            f.write("| block | x | C | HxW | s | K | fused us | unfused (ours) us | cuDNN us | vs unfused | vs cuDNN | "
+                    "fused GB/s | config |\n|---|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+            for b in r["blocks"]:
+                f.write(f"| {b['block']} | {b['count']} | {b['c']} | {b['hw']} | {b['stride']} | {b['k_out']} | "
+                        f"{b['fused_us']:.1f} | {b['unfused_us']:.1f} | {b['cudnn_us']:.1f} | "
+                        f"{b['fused_vs_unfused']:.2f} | {b['fused_vs_cudnn']:.2f} | {b['fused_gbs']:.0f} | "
+                        f"{b['fused_config']} |\n")
+            f.write(f"\nsum (x count): fused {r['sum_fused_us']:.0f} us, unfused {r['sum_unfused_us']:.0f} us, "
+                    f"cuDNN {r['sum_cudnn_us']:.0f} us\n")
+    print("wrote", a.out + ".json", a.out + ".md")
+
+
+if __name__ == "__main__":
+    main()

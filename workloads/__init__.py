@@ -166,6 +166,40 @@ def mobilenet_v2(n: int = 1) -> list[ConvLayer]:
     return list(uniq.values())
 
 
+@dataclass(frozen=True)
+class DwPwBlock:
+    """A depthwise conv and the 1x1 projection that consumes it (the fused-operator unit of
+    wpk_dwpw_*): y = project(relu(dw(x) + b_dw)) + b_pw (MobileNet-V2's projection is linear)."""
+    name: str
+    dw: ConvLayer
+    k_out: int
+    count: int = 1
+
+
+def mobilenet_v2_dwpw(n: int = 1) -> list[DwPwBlock]:
+    """The 17 (depthwise 3x3 -> 1x1 projection) pairs of MobileNet-V2 (width 1.0, 224), merged by
+    shape: the fused-operator view of mobilenet_v2() (same dw / project shapes)."""
+    h, cin = 112, 32
+    blocks = [(1, 16, 1, 1), (6, 24, 2, 2), (6, 32, 3, 2), (6, 64, 4, 2),
+              (6, 96, 3, 1), (6, 160, 3, 2), (6, 320, 1, 1)]
+    out: dict[tuple, DwPwBlock] = {}
+    bi = 0
+    for t, cout, reps, s0 in blocks:
+        for i in range(reps):
+            s = s0 if i == 0 else 1
+            hid = cin * t
+            dw = ConvLayer(f"b{bi}.dw", n, hid, h, h, hid, 3, 3, s, 1, 1, hid)
+            key = (hid, h, s, cout)
+            if key in out:
+                out[key] = replace(out[key], count=out[key].count + 1)
+            else:
+                out[key] = DwPwBlock(f"b{bi}", dw, cout)
+            h = h // s
+            cin = cout
+            bi += 1
+    return list(out.values())
+
+
 def table1(n: int = 1) -> list[ConvLayer]:
     """PAPER.md:162-177 Table 1 ("Convolutions on which RL-search outperforms genetic search").
     Padding is VALID: the table's H/W chain is self-consistent only without padding."""
