@@ -166,8 +166,41 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     if (d.fused_dw) {
         // fused depthwise + pointwise: the A producer computes the depthwise conv (internal A_MODE 5);
         // the gene's other producers do not apply, K = the depthwise channels (C % 8 == 0)
-        if (cfg.genes[4] != 0) return no("fused depthwise+pointwise: A_MODE must be 0 (the depthwise producer)");
+        // A_MODE 0: the persistent tcgen05 kernel with a depthwise producer (internal A_MODE 5);
+        // A_MODE 1: the one-tile-per-CTA kernel of dwpw.cu (internal A_MODE 6), whose only free
+        // parameter is none: canonical genes {cover(K_out), 2, 1, 0, 1, 1, 128}
+        if (cfg.genes[4] != 0 && cfg.genes[4] != 1)
+            return no("fused depthwise+pointwise: A_MODE 0 (persistent, depthwise producer warps) or 1 (one tile per CTA)");
         if ((cfg.genes[3] >> 1) & 3) return no("fused depthwise+pointwise: no CTA pairs / dual accumulators");
+        // the depthwise result of an M tile is computed once per N tile: BLOCK_N must cover K_out
+        // (up to the widest tile) so that no tile recomputes it
+        int cover = 16;
+        for (int v : {16, 32, 64, 96, 128, 192, 256}) {
+            cover = v;
+            if (v >= std::min(round_up(d.k, 16), 256)) break;
+        }
+        if (g->bn < cover) return no("fused depthwise+pointwise: BLOCK_N must cover K_out (min(K_out, 256))");
+        if (cfg.genes[4] == 1) {
+            if (g->bn != cover || g->stages != 2 || g->splits != 1 || cfg.genes[3] != 0 || g->acc_stages != 1 || g->bm != 128)
+                return no("fused depthwise+pointwise A_MODE 1: genes must be {cover(K_out), 2, 1, 0, 1, 1, 128}");
+            if (d.k % 8) return no("fused depthwise+pointwise A_MODE 1: K_out % 8 == 0 (16-byte output rows)");
+            if (d.k > 512) return no("fused depthwise+pointwise A_MODE 1: K_out <= 512 (TMEM columns)");
+            if (d.M() >= 2147483647LL - 128) return no("fused depthwise+pointwise A_MODE 1: M < 2^31");
+            g->a_mode = 6;
+            g->cpad = d.c;
+            g->c_blocks = (d.c + 63) / 64;
+            g->num_kb = g->c_blocks;
+            g->kb_per_split = g->num_kb;
+            g->m_tiles = (int)((d.M() + 127) / 128);
+            g->n_tiles = 1;
+            g->work = g->m_tiles;
+            g->epi_tma = 0; g->csplit = 0; g->pair = 0; g->kdual = 0; g->prod_rr = 0; g->a_tiled = 0;
+            g->smem_bytes = 1024 + 2 * 16384 + 2 * (size_t)round_up(d.k, 16) * 128 + 64;
+            int cols = 32;
+            while (cols < round_up(d.k, 16)) cols <<= 1;
+            g->tmem_cols = cols;
+            return true;
+        }
         g->a_mode = 5;
         g->cpad = d.c;
         g->c_blocks = (d.c + g->bk - 1) / g->bk;
@@ -373,7 +406,15 @@ Config default_config(const ConvDesc &d, int family) {
     }
     const long long mt = (d.M() + 127) / 128;
     if (bn == 256 && mt * ((d.k + 255) / 256) < 120) bn = 128;
-    if (d.fused_dw) {   // fused depthwise + pointwise: 128-row 1-CTA tiles, the depthwise producer
+    if (d.fused_dw) {   // fused depthwise + pointwise: 128-row 1-CTA tiles, the depthwise producer,
+        // the narrowest BLOCK_N that covers K_out (the depthwise result is computed once per M tile)
+        for (int v : {16, 32, 64, 96, 128, 192, 256}) {
+            bn = v;
+            if (v >= std::min(round_up(d.k, 16), 256)) break;
+        }
+        int g1[7] = {bn, 2, 1, 0, 1, 1, 128};   // the one-tile-per-CTA kernel (dwpw.cu) when it applies
+        std::memcpy(c.genes, g1, sizeof g1);
+        if (config_valid(d, c, nullptr)) return c;
         int g[7] = {bn, 4, 1, 0, 0, 2, 128};
         std::memcpy(c.genes, g, sizeof g);
         for (int st = 8; st >= 2; --st) {

@@ -13,6 +13,7 @@
 #include <string>
 
 #include "dwconv.h"
+#include "dwpw.h"
 #include "gemm32.h"
 #include "simt_conv.cuh"
 #include "jit.h"
@@ -389,7 +390,7 @@ static WsLayout ws_layout(Plan &p, const Config &cfg, bool host_staging) {
     if (cfg.family == WPK_FAMILY_UMMA) {
         UmmaGeom g;
         if (!plan_geom(p, cfg, &g, nullptr)) return L;
-        if (g.a_mode == 5) {   // fused depthwise: its weights re-laid [R][S][C]
+        if (g.a_mode == 5 || g.a_mode == 6) {   // fused depthwise: its weights re-laid [R][S][C]
             L.w_off = off; L.w_bytes = al256((size_t)d.c * d.r * d.s * e); off += L.w_bytes;
         } else if (g.a_mode == 1) {
             L.x_off = off; L.x_bytes = al256((size_t)d.M() * g.cpad * e); off += L.x_bytes;
@@ -574,7 +575,7 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     const void *xk = x, *wk = w;
     const int pack_kind = WPK_FAMILY_UMMA * 10 + g.a_mode;
     const void *dwk = nullptr;
-    if (g.a_mode == 5) {
+    if (g.a_mode == 5 || g.a_mode == 6) {
         // fused depthwise + pointwise: x and the pointwise weights [K][C] are used as given; the
         // depthwise weights [C][R][S] are re-laid [R][S][C] once per weight pointer
         if (!w_dw) { set_error("fused depthwise+pointwise plan: depthwise weights missing"); return -1; }
@@ -585,6 +586,20 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
             p.packed_cfg_family = pack_kind;
         }
         dwk = ws + L.w_off;
+        if (g.a_mode == 6) {   // one-tile-per-CTA fused kernel (dwpw.cu)
+            cudaError_t pe = cudaGetLastError();
+            if (pe != cudaSuccess) { set_error(std::string("aux kernel launch: ") + cudaGetErrorString(pe)); return -1; }
+            DwpwArgs A{};
+            A.x = x; A.w_dw = dwk; A.b_dw = d.dw_epi != WPK_EPI_NONE ? b_dw : nullptr; A.w_pw = w;
+            A.b_pw = d.epilogue != WPK_EPI_NONE ? b : nullptr; A.y = y;
+            A.N = d.n; A.C = d.c; A.H = d.h; A.W = d.w; A.P = d.p; A.Q = d.q; A.R = d.r; A.S = d.s; A.K = d.k;
+            A.M = (int)d.M();
+            A.sh = d.sh; A.sw = d.sw; A.ph = d.ph; A.pw = d.pw; A.dh = d.dh; A.dw = d.dw;
+            A.dw_epi = d.dw_epi; A.pw_epi = d.epilogue;
+            int rc = dwpw_launch(A, d.dtype, stream, &err);
+            if (rc < 0) { set_error(err); return -1; }
+            return launches + rc;
+        }
     } else if (g.a_mode == 3) {
         // activations -> zero-padded NHWC image with 4 channels per pixel
         launch_aux(g.seg_two ? 8 : 7, x, ws + L.x_off, d, g.seg_hp, sm, st, g.seg_wp);

@@ -223,7 +223,9 @@ def test_dwpw_plan_host_validation():
     assert st == 0, L.last_error()
     fam, g = ctypes.c_int32(), (ctypes.c_int32 * L.NUM_GENES)()
     assert lib.wpk_conv2d_get_config(h, ctypes.byref(fam), g) == 0
-    assert fam.value == 1 and g[4] == 0 and (g[3] >> 1) & 3 == 0
+    assert fam.value == 1 and g[4] in (0, 1) and (g[3] >> 1) & 3 == 0   # 1: the one-tile-per-CTA kernel
+    assert lib.wpk_conv2d_config_valid(h, 1, (ctypes.c_int32 * L.NUM_GENES)(32, 2, 1, 0, 1, 1, 128)) == 1
+    assert lib.wpk_conv2d_config_valid(h, 1, (ctypes.c_int32 * L.NUM_GENES)(32, 4, 1, 0, 1, 1, 128)) == 0   # canonical only
     assert lib.wpk_conv2d_config_valid(h, 1, (ctypes.c_int32 * L.NUM_GENES)(64, 4, 2, 1, 0, 2, 256)) == 1
     assert lib.wpk_conv2d_config_valid(h, 1, (ctypes.c_int32 * L.NUM_GENES)(64, 4, 1, 2, 0, 2, 256)) == 0   # pair
     assert lib.wpk_conv2d_config_valid(h, 1, (ctypes.c_int32 * L.NUM_GENES)(64, 4, 1, 0, 4, 2, 128)) == 0   # A_MODE 4

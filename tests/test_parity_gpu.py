@@ -284,8 +284,9 @@ def test_depthwise_nhwc_sliding_window(dtype):
                                       epilogue=epi, dtype=dtype)
                     xl, wl = to_layout(x, w, layout)
                     zl = z.permute(0, 2, 3, 1).contiguous() if layout == "nhwc" else z
-                    for pix in (1, 2, 4):
-                        plan.set_config(2, [8, pix, 128, 1, 0, 0, 0])
+                    # NHWC VEC_C 8: the sliding-window kernel; NHWC VEC_C 4 and NCHW VEC_C 1: the generic one
+                    for vec, pix in ([(8, 1), (8, 2), (8, 4), (4, 2)] if layout == "nhwc" else [(1, 1), (1, 4)]):
+                        plan.set_config(2, [vec, pix, 128, 1, 0, 0, 0])
                         y = plan.run(xl.cuda(), wl.cuda(), bb.cuda() if bb is not None else None,
                                      z=zl.cuda() if epi == "bias_add_relu" else None)
                         torch.cuda.synchronize()
@@ -294,8 +295,8 @@ def test_depthwise_nhwc_sliding_window(dtype):
                             assert_bit_exact(y, ref)
                         else:
                             assert rel_error(dtype, y, ref) <= TOL[dtype]
-                        outs[(layout, pix)] = y
-                base = canon_bits(outs[("nchw", 1)])
+                        outs[(layout, vec, pix)] = y
+                base = canon_bits(outs[("nchw", 1, 1)])
                 for key, y in outs.items():
                     assert torch.equal(canon_bits(y), base), (L.name, epi, mode, key)
 

@@ -25,6 +25,7 @@ NETS = {
     "vgg16": (lambda: workloads.vgg16(64), "f16", "rl"),
     "mobilenet_v2": (lambda: workloads.mobilenet_v2(1), "bf16", "ga"),
     "mobilenet_v2_n32": (lambda: workloads.mobilenet_v2(32), "bf16", "ga"),
+    "mobilenet_v2_n128": (lambda: workloads.mobilenet_v2(128), "bf16", "ga"),
     "resnet50_n1": (lambda: workloads.resnet50(1), "bf16", "ga"),
     "resnet18_n1": (lambda: workloads.resnet18(1), "bf16", "ga"),
     "table1_n1": (lambda: workloads.table1(1), "bf16", "rl"),
