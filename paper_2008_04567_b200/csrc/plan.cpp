@@ -121,7 +121,16 @@ bool family_applicable(const ConvDesc &d, int family, std::string *why) {
     }
     if (family == WPK_FAMILY_UMMA) {
         if (d.dtype == WPK_F32) return no("UMMA family needs tf32/bf16/fp16 (F32 is the exact CUDA-core path)");
-        if (d.g != 1) return no("UMMA family needs groups == 1");
+        if (d.g != 1) {   // general groups on the tensor cores (gconv_tc.cu, A_MODE 1)
+            if (d.c == d.g && d.k == d.g) return no("UMMA family: depthwise convs run on the DW family");
+            if (d.dtype != WPK_BF16 && d.dtype != WPK_F16) return no("UMMA grouped conv needs bf16 / fp16");
+            if (d.layout != WPK_NHWC) return no("UMMA grouped conv needs NHWC");
+            if ((d.c / d.g) % 4) return no("UMMA grouped conv needs C/groups % 4 == 0");
+            if (d.k / d.g > 256) return no("UMMA grouped conv needs K/groups <= 256");
+            if ((double)d.n * d.h * d.w * d.c >= 2147483647.0 || (double)d.M() * d.k >= 2147483647.0)
+                return no("UMMA grouped conv needs < 2^31 elements per tensor");
+            return true;
+        }
         if (d.sh > 8 || d.sw > 8) return no("TMA im2col traversal stride must be <= 8");
         // TMA im2col 4-D bounding-box corners must lie in [-128, 127] (cuda.h cuTensorMapEncodeIm2col)
         int lo_h = -d.ph, lo_w = -d.pw, up_h = d.ph - (d.r - 1) * d.dh, up_w = d.pw - (d.s - 1) * d.dw;
@@ -163,6 +172,30 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     g->seg_sp = 0; g->seg_hp = 0; g->seg_wp = 0; g->seg_fast = 0; g->seg_two = 0;
     if (d.dtype == WPK_FP8E4M3 && g->a_mode != 0)
         return no("FP8 (e4m3) is instantiated for the TMA A producers only (A_MODE 0 / 4)");
+    if (d.g > 1) {
+        // grouped conv on the tensor cores (gconv_tc.cu, internal A_MODE 7): one tile = 128 pixels x
+        // BLOCK_N / Np groups; the only gene is BLOCK_N (a multiple of the per-group MMA width Np)
+        const int kpg = d.k / d.g;
+        const int np = std::max(16, round_up(kpg, 16));
+        if (cfg.genes[4] != 1 || g->stages != 2 || g->splits != 1 || cfg.genes[3] != 0 || g->acc_stages != 1 || g->bm != 128)
+            return no("UMMA grouped conv: genes must be {BLOCK_N, 2, 1, 0, 1, 1, 128}");
+        if (g->bn % np) return no("UMMA grouped conv: BLOCK_N must be a multiple of the per-group MMA width");
+        if (g->bn / np > d.g) return no("UMMA grouped conv: BLOCK_N covers more groups than the layer has");
+        g->a_mode = 7;
+        g->cpad = d.c;
+        g->c_blocks = (d.r * d.s * (d.c / d.g) + 63) / 64;
+        g->num_kb = g->c_blocks;
+        g->kb_per_split = g->num_kb;
+        g->m_tiles = (int)((d.M() + 127) / 128);
+        g->n_tiles = (d.g + g->bn / np - 1) / (g->bn / np);
+        g->work = (long long)g->m_tiles * g->n_tiles;
+        g->epi_tma = 0; g->csplit = 0; g->pair = 0; g->kdual = 0; g->prod_rr = 0; g->a_tiled = 0;
+        g->smem_bytes = 1024 + 2 * 16384 + 2 * (size_t)np * 128 + 64;
+        int cols = 32;
+        while (cols < g->bn) cols <<= 1;
+        g->tmem_cols = cols;
+        return true;
+    }
     if (d.fused_dw) {
         // fused depthwise + pointwise: the A producer computes the depthwise conv (internal A_MODE 5);
         // the gene's other producers do not apply, K = the depthwise channels (C % 8 == 0)

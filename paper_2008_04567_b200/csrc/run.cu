@@ -14,6 +14,7 @@
 
 #include "dwconv.h"
 #include "dwpw.h"
+#include "gconv_tc.h"
 #include "gemm32.h"
 #include "simt_conv.cuh"
 #include "jit.h"
@@ -390,7 +391,9 @@ static WsLayout ws_layout(Plan &p, const Config &cfg, bool host_staging) {
     if (cfg.family == WPK_FAMILY_UMMA) {
         UmmaGeom g;
         if (!plan_geom(p, cfg, &g, nullptr)) return L;
-        if (g.a_mode == 5 || g.a_mode == 6) {   // fused depthwise: its weights re-laid [R][S][C]
+        if (g.a_mode == 7) {
+            // tensor-core grouped conv: NHWC x and [K][R][S][C/g] weights used as given
+        } else if (g.a_mode == 5 || g.a_mode == 6) {   // fused depthwise: its weights re-laid [R][S][C]
             L.w_off = off; L.w_bytes = al256((size_t)d.c * d.r * d.s * e); off += L.w_bytes;
         } else if (g.a_mode == 1) {
             L.x_off = off; L.x_bytes = al256((size_t)d.M() * g.cpad * e); off += L.x_bytes;
@@ -575,7 +578,20 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
     const void *xk = x, *wk = w;
     const int pack_kind = WPK_FAMILY_UMMA * 10 + g.a_mode;
     const void *dwk = nullptr;
-    if (g.a_mode == 5 || g.a_mode == 6) {
+    if (g.a_mode == 7) {   // grouped conv on the tensor cores (gconv_tc.cu)
+        GconvArgs A{};
+        A.x = x; A.w = w; A.b = d.epilogue != WPK_EPI_NONE ? b : nullptr; A.z = z; A.y = y;
+        A.N = d.n; A.C = d.c; A.H = d.h; A.W = d.w; A.P = d.p; A.Q = d.q; A.R = d.r; A.S = d.s; A.K = d.k;
+        A.M = (int)d.M();
+        A.sh = d.sh; A.sw = d.sw; A.ph = d.ph; A.pw = d.pw; A.dh = d.dh; A.dw = d.dw;
+        A.groups = d.g; A.Cpg = d.c / d.g; A.Kpg = d.k / d.g;
+        A.np = std::max(16, (A.Kpg + 15) / 16 * 16);
+        A.gt = g.bn / A.np;
+        A.epilogue = d.epilogue;
+        int rc = gconv_tc_launch(A, d.dtype, stream, &err);
+        if (rc < 0) { set_error(err); return -1; }
+        return launches + rc;
+    } else if (g.a_mode == 5 || g.a_mode == 6) {
         // fused depthwise + pointwise: x and the pointwise weights [K][C] are used as given; the
         // depthwise weights [C][R][S] are re-laid [R][S][C] once per weight pointer
         if (!w_dw) { set_error("fused depthwise+pointwise plan: depthwise weights missing"); return -1; }
