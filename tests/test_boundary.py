@@ -247,3 +247,41 @@ def test_dwpw_plan_host_validation():
     assert st == 0
     assert lib.wpk_dwpw_run(h, 16, 16, 16, 16, 16, 16, None) == L.ERR_INVALID_ARGUMENT
     lib.wpk_conv2d_destroy(h)
+
+
+def test_grouped_tensor_core_configs_host_validation():
+    """1 < groups < C on the tcgen05 family (gconv_tc.cu): only {BLOCK_N, 2, 1, 0, 1, 1, 128} with
+    BLOCK_N a multiple of the per-group MMA width max(16, K/g rounded to 16) and at most `groups`
+    groups per tile; NHWC 16-bit only, C/g % 4 == 0; depthwise stays on the DW family."""
+    lib = L.load()
+
+    def plan(c, k, g, layout="nhwc", dtype="bf16"):
+        st, h = _plan(L.make_shape(n=2, c=c, h=14, w=14, k=k, r=3, s=3, stride=1, pad=1, groups=g, layout=layout),
+                      dtype=dtype)
+        assert st == 0, L.last_error()
+        return h
+
+    def ok(h, bn, rest=(2, 1, 0, 1, 1, 128)):
+        return lib.wpk_conv2d_config_valid(h, 1, (ctypes.c_int32 * L.NUM_GENES)(bn, *rest)) == 1
+
+    h = plan(128, 128, 32)                      # K/g = 4 -> Np 16: 1..16 groups per tile
+    assert [bn for bn in (16, 32, 64, 96, 128, 192, 256) if ok(h, bn)] == [16, 32, 64, 96, 128, 192, 256]
+    assert not ok(h, 64, (4, 1, 0, 1, 1, 128)) and not ok(h, 64, (2, 2, 0, 1, 1, 128))
+    assert not ok(h, 64, (2, 1, 0, 0, 2, 128))   # A_MODE 0 (TMA im2col) has no grouped variant
+    lib.wpk_conv2d_destroy(h)
+    h = plan(1024, 1024, 32)                    # K/g = 32 -> Np 32
+    assert not ok(h, 16) and ok(h, 32) and ok(h, 256) and not ok(h, 96 + 16)
+    lib.wpk_conv2d_destroy(h)
+    h = plan(32, 48, 4)                         # 4 groups: at most 4 x 16 columns
+    assert ok(h, 64) and not ok(h, 96)
+    lib.wpk_conv2d_destroy(h)
+    for kw in (dict(layout="nchw"), dict(dtype="f32"), dict(dtype="tf32")):
+        h = plan(128, 128, 32, **kw)
+        assert not ok(h, 64)
+        lib.wpk_conv2d_destroy(h)
+    h = plan(24, 24, 4)                          # C/g = 6
+    assert not ok(h, 16) and b"% 4" in lib.wpk_last_error()
+    lib.wpk_conv2d_destroy(h)
+    h = plan(32, 32, 32)                         # depthwise
+    assert not ok(h, 16) and b"depthwise" in lib.wpk_last_error()
+    lib.wpk_conv2d_destroy(h)

@@ -36,6 +36,8 @@ NETS = {
     # NEXT-4: e4m3 operands / bf16 output (tcgen05 kind::f8f6f4). cuDNN has no fp8 conv through torch:
     # the competitor columns are cuDNN bf16 and our own tuned bf16 kernel on the same (rounded) inputs
     "resnet50_fp8": (lambda: workloads.resnet50(32), "fp8", "ga"),
+    # NEXT-4 grouped convs on the tensor cores (gconv_tc.cu): every groups-per-tile choice measured
+    "resnext50_grouped_tc_bf16_n8": (lambda: workloads.resnext50_grouped(8), "bf16", "tc_sweep"),
 }
 
 
@@ -70,7 +72,20 @@ def run_net(name, budget):
         kw = dict(seed=i)
         if search == "rl":
             kw.update(rl_envs=4, rl_horizon=16)
-        res = plan.tune(search if fam != 2 else "ga", budget, **kw)
+        if search == "tc_sweep":   # the tcgen05 grouped kernel: its only gene is BLOCK_N
+            best = None
+            for bn in (16, 32, 64, 96, 128, 192, 256):
+                genes = [bn, 2, 1, 0, 1, 1, 128]
+                if plan.config_valid(1, genes):
+                    plan.set_config(1, genes)
+                    us = plan.measure()
+                    if best is None or us < best[0]:
+                        best = (us, genes)
+            plan.set_config(1, best[1])
+            from paper_2008_04567_b200.conv import TuneResult
+            res = TuneResult(1, best[1], best[0], 7, 1, 0.0)
+        else:
+            res = plan.tune(search if fam != 2 else "ga", budget, **kw)
         t_tune += time.perf_counter() - t0
         extra = {}
         if dtype == "fp8":
