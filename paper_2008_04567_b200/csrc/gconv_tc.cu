@@ -39,19 +39,24 @@ __device__ __forceinline__ uint32_t pk2(float a, float b, __half *) {
     return *reinterpret_cast<uint32_t *>(&h);
 }
 
-// im2col rows of one (group, K chunk): thread tid fills 16-byte pieces (row, j) = (tid >> 3) + 32 i, tid & 7
-template <typename T>
-__device__ __forceinline__ void gather_chunk(const GconvArgs &a, uint32_t sbase, int m0, int g, int k0, int tid) {
+// im2col rows of one (group, K chunk): thread tid owns the 16-byte pieces (row, j) =
+// ((tid >> 3) + 32 i, tid & 7), i < 4. Loaded into registers one step ahead of the smem store
+// (software pipeline: the loads of step s+1 are in flight while step s is stored and multiplied).
+struct Pieces {
+    uint32_t o[4][4];
+};
+__device__ __forceinline__ void gather_load(const GconvArgs &a, int m0, int g, int k0, int tid, Pieces &P) {
     const unsigned short *__restrict__ x = static_cast<const unsigned short *>(a.x);
     const int KG = a.R * a.S * a.Cpg;
     const int PQ = a.P * a.Q;
     const int j = tid & 7;
     const int kb = k0 + j * 8;                   // first K index of this 16-byte piece
-#pragma unroll 1
+#pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int row = (tid >> 3) + 32 * i;
         const int m = m0 + row;
-        uint32_t o[4] = {0u, 0u, 0u, 0u};
+        uint32_t *o = P.o[i];
+        o[0] = o[1] = o[2] = o[3] = 0u;
         if (m < a.M && kb < KG) {
             const int n = m / PQ;
             const int rem = m - n * PQ;
@@ -98,9 +103,16 @@ __device__ __forceinline__ void gather_chunk(const GconvArgs &a, uint32_t sbase,
                 for (int e = 0; e < 4; ++e) o[e] = (uint32_t)e16[2 * e] | ((uint32_t)e16[2 * e + 1] << 16);
             }
         }
+    }
+}
+__device__ __forceinline__ void gather_store(uint32_t sbase, int tid, const Pieces &P) {
+    const int j = tid & 7;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = (tid >> 3) + 32 * i;
         ptx::st_shared_v4(sbase + (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u +
                               ((uint32_t)(j ^ (row & 7)) << 4),
-                          o[0], o[1], o[2], o[3]);
+                          P.o[i][0], P.o[i][1], P.o[i][2], P.o[i][3]);
     }
 }
 
@@ -165,16 +177,26 @@ __global__ void __launch_bounds__(kThreads) gconv_tc_kernel(const GconvArgs a) {
     const int nkc = (KG + 63) / 64;
     uint32_t ph0 = 0, ph1 = 0;
     int step = 0;
+    Pieces cur;
+    gather_load(a, m0, g0, 0, tid, cur);
     for (int gl = 0; gl < ng; ++gl) {
         for (int kc = 0; kc < nkc; ++kc, ++step) {
             const int b = step & 1;
+            // next step's loads first: in flight while this step is stored and multiplied
+            Pieces nxt;
+            const bool more = kc + 1 < nkc || gl + 1 < ng;
+            if (more) {
+                const int ngl = (kc + 1 < nkc) ? gl : gl + 1, nkc1 = (kc + 1 < nkc) ? kc + 1 : 0;
+                gather_load(a, m0, g0 + ngl, nkc1 * 64, tid, nxt);
+            }
             if (step >= 2) {
                 if (b == 0) { ptx::mbar_wait(&bars[0], ph0); ph0 ^= 1; }
                 else { ptx::mbar_wait(&bars[1], ph1); ph1 ^= 1; }
             }
             const uint32_t aB = ptx::smem_u32(sA + b * 16384);
             const uint32_t bB = ptx::smem_u32(sB + (size_t)b * a.np * 128);
-            gather_chunk<T>(a, aB, m0, g0 + gl, kc * 64, tid);
+            gather_store(aB, tid, cur);
+            if (more) cur = nxt;
             weight_chunk(a, bB, g0 + gl, kc * 64, tid);
             ptx::fence_proxy_async_smem();
             __syncthreads();

@@ -9,9 +9,10 @@ from paper_2008_04567_b200 import Conv2dPlan
 name = sys.argv[1]
 reps = int(os.environ.get("REPS", "3"))
 net = os.environ.get("NET", "resnet50")
-batch = int(os.environ.get("BATCH", {"resnet50": "32", "vgg16": "64", "mobilenet_v2": "1"}[net]))
+batch = int(os.environ.get("BATCH", {"resnet50": "32", "vgg16": "64", "mobilenet_v2": "1"}.get(net, "8")))
 L = next(l for l in getattr(workloads, net)(batch) if l.name == name)
-plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype=os.environ.get("DT", "bf16"))
+plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, L.dil, L.groups, layout="nhwc",
+                  dtype=os.environ.get("DT", "bf16"))
 if len(sys.argv) > 2:
     plan.set_config(1, [int(v) for v in sys.argv[2:9]])
 elif os.environ.get("CFG_JSON"):   # the layer's config from a bench --configs-out file
