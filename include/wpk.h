@@ -29,7 +29,7 @@
  *      WPK_FP8E4M3 (NEXT-4): x and w are OCP float8 e4m3 ("e4m3fn": 1 sign, 4 exponent, 3 mantissa
  *               bits, bias 7, no infinities; torch.float8_e4m3fn), b, z and y are bfloat16;
  *               tcgen05.mma kind::f8f6f4 with fp32 accumulate. Tensor-core family only
- *               (WPK_FAMILY_UMMA, A_MODE 0 or 4, groups 1); other families return
+ *               (WPK_FAMILY_UMMA, A_MODE 0, 4, 5 or 6, groups 1); other families return
  *               WPK_ERR_UNSUPPORTED at plan time. x and w are taken as given (no scaling: a
  *               per-tensor scale folds into w and b outside the library).
  *    The accumulator is fp32; bias is up-converted to fp32 and added before ReLU; the output is
@@ -88,7 +88,12 @@ typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 
  *                     (plain TMA tiles for 1x1/s1/p0), 1 = explicit im2col matrix in the workspace,
  *                     2 = fused gather producer (im2col built in shared memory; small-C layers),
  *                     3 = pixel-segment gather (C <= 4), 4 = A_MODE 0 with the K blocks dealt round
- *                     robin over three TMA producer warps (A + B of a stage from one thread)
+ *                     robin over three TMA producer warps (A + B of a stage from one thread),
+ *                     5 / 6 = A_MODE 0 / 4 with K groups: two consecutive K blocks share one full /
+ *                     empty barrier pair (STAGES = K-block slots, even, >= 4). Grouped plans
+ *                     (1 < groups < C, NHWC 16-bit) accept only A_MODE 1 = the tensor-core grouped
+ *                     kernel, genes {BLOCK_N, 2, 1, 0, 1, 1, 128}; fused depthwise+pointwise plans
+ *                     accept A_MODE 0 (depthwise producer warps) and 1 (one tile per CTA)
  *   WPK_FAMILY_DW   : grouped conv on CUDA cores, groups > 1: depthwise (groups == C == K, vector
  *                     over channels) or general groups (vector over VEC_C outputs of one group,
  *                     VEC_C | K/groups), genes = (VEC_C, PIX_PER_THREAD, THREADS, -, -, -, -)

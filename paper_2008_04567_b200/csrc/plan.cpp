@@ -71,7 +71,7 @@ static Space make_space(int family) {
         sp.names = {"T_x", "T_y", "T_z", "Tile_x", "Tile_y", "Tile_z", "Tile_rz"};
     } else if (family == WPK_FAMILY_UMMA) {
         sp.dom = {{16, 32, 64, 96, 128, 192, 256}, {2, 3, 4, 5, 6, 7, 8}, {1, 2, 4, 8, 16},
-                  {0, 1, 2, 3, 4, 5, 6, 7}, {0, 1, 2, 3, 4}, {1, 2, 4}, {128, 256}};
+                  {0, 1, 2, 3, 4, 5, 6, 7}, {0, 1, 2, 3, 4, 5, 6}, {1, 2, 4}, {128, 256}};
         sp.names = {"BLOCK_N", "STAGES", "SPLIT_K", "MODE", "A_MODE", "ACC_STAGES", "BLOCK_M"};
     } else if (family == WPK_FAMILY_GEMM32) {
         sp.dom = {{64, 128}, {64, 128}, {8, 16}, {4, 8}, {1, 2, 4, 8}, {0}, {0}};
@@ -164,9 +164,19 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     // A_MODE 4: the TMA producer of A_MODE 0 with its K blocks dealt round robin over three
     // producer warps (A and B boxes of a stage from one thread) instead of an A / B warp split
     g->prod_rr = 0;
+    g->kgroup = 1;
     if (g->a_mode == 4) {
         g->a_mode = 0;
         g->prod_rr = 1;
+    }
+    // A_MODE 5 / 6: the TMA producers of A_MODE 0 / 4 with K groups -- two consecutive K blocks of a
+    // work item per full / empty barrier pair (one expect_tx, one wait and one MMA commit per two
+    // blocks); STAGES counts K-block slots, so it must be even and >= 4 (>= 2 groups in flight)
+    if (g->a_mode == 5 || g->a_mode == 6) {
+        if (g->stages % 2 || g->stages < 4) return no("A_MODE 5/6 (K groups of 2) need an even STAGES >= 4");
+        g->prod_rr = (g->a_mode == 6) ? 1 : 0;
+        g->a_mode = 0;
+        g->kgroup = 2;
     }
     g->acc_stages = cfg.genes[5];
     g->seg_sp = 0; g->seg_hp = 0; g->seg_wp = 0; g->seg_fast = 0; g->seg_two = 0;

@@ -195,6 +195,7 @@ launch:
     a.kpad_bias = (L.K + 255) / 256 * 256;
     a.kdual = g.kdual;
     a.prod_rr = (g.prod_rr && !a_split) ? 1 : 0;
+    a.kgroup = g.kgroup;
     {
         const long long stage_bytes = g.pair ? 128LL * 128 + (long long)(g.bn / 2) * 128 : (long long)g.bm * 128 + (long long)g.bn * 128;
         const long long slab = (long long)(g.splits - 1) * (g.pair ? 128 : g.bm) * g.bn * 4;

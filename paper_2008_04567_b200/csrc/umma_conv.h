@@ -42,6 +42,7 @@ struct UmmaArgs {
     int owner_bulk;                 // EK_SPLIT: the other splits' partial slab fits in the stage area
     int kdual;                      // two accumulators per 128-row tile (even / odd K steps)
     int prod_rr;                    // TMA producers: K blocks dealt round robin over warps 0, 2, 3
+    int kgroup;                     // K blocks per full / empty barrier group (1, or 2 for TMA producers)
     int recv_stride;                // EK_CSPLIT: bytes per received partial row
     int a_split;                    // A stage loaded by two threads (two half-height boxes)
     const void *z;                  // residual (epilogue 3), laid out as y

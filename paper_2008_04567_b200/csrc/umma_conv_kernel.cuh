@@ -1165,7 +1165,12 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
         // the stage's empty barrier for block g - STAGES, unambiguous only if block g - 2 STAGES has
         // been consumed: its own previous wait (block g - NPROD) saw g - NPROD - STAGES consumed, so
         // NPROD <= STAGES suffices.
-        const int NPROD = min(3, a.stages);
+        // K groups (a.kgroup = G in {1, 2}): G consecutive K blocks of a work item share one full /
+        // empty barrier pair (the first slot's), so one expect_tx / wait / commit serves G blocks;
+        // a producer loads whole groups: group gi (ring group gi % NG) belongs to producer gi % NPROD.
+        const int G = a.kgroup;
+        const int NG = a.stages / G;                   // barrier groups in the ring
+        const int NPROD = min(3, NG);
         const int pid = (warp == 0) ? 0 : warp - 1;
         if (lane == 0 && pid < NPROD) {
             const uint32_t a_rows = kPair ? 128u : (uint32_t)a.bm;
@@ -1174,14 +1179,14 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 int m0, nimg, wc, hc, n0;
             };
             auto walk = [&](auto &&fn) {
-                long long g = 0;
+                long long gi = 0;   // group index in this CTA's schedule
                 for (long long w = wstart; w < a.work; w += wstep) {
                     const WorkPos wp = decode_work(w, a);
                     const int kb0 = wp.split * a.kb_per_split;
                     const int kb1 = min(a.num_kb, kb0 + a.kb_per_split);
-                    int kb = kb0 + (int)((pid - g % NPROD + NPROD) % NPROD);
-                    g += kb - kb0;
-                    if (kb < kb1) {
+                    const int ngi = (kb1 - kb0 + G - 1) / G;
+                    int i = (int)((pid - gi % NPROD + NPROD) % NPROD);
+                    if (i < ngi) {
                         ItemPos ip;
                         ip.m0 = wp.mt * a.bm + (int)crank * 128;   // M < 2^31 (plan validation)
                         ip.nimg = ip.m0 / (int)a.PQ;
@@ -1190,51 +1195,59 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                         ip.wc = q * a.stride_w - a.pad_w;
                         ip.hc = p * a.stride_h - a.pad_h;
                         ip.n0 = wp.nt * a.bn + (int)crank * (a.bn / 2);
-                        for (; kb < kb1; kb += NPROD, g += NPROD)
-                            if (!fn(g, ip, kb)) return;
+                        for (; i < ngi; i += NPROD) {
+                            const int kb = kb0 + i * G;
+                            if (!fn(gi + i, ip, kb, min(G, kb1 - kb))) return;
+                        }
                     }
-                    g -= kb - kb1;   // back to the first K block of the next work item
+                    gi += ngi;
                 }
             };
-            auto load_b = [&](long long g, const ItemPos &ip, int kb) {
-                const uint32_t stage = (uint32_t)(g % a.stages);
-                const int rs = kb / a.c_blocks, cb = kb - rs * a.c_blocks;
-                if (leader) ptx::mbar_arrive_expect_tx(&full[stage], tx);
-                if constexpr (kPair) ptx::tma_load_3d_pair(smB + stage * b_bytes, &tmB, &full[stage], cb * a.bk, rs, ip.n0);
-                else ptx::tma_load_3d(smB + stage * b_bytes, &tmB, &full[stage], cb * a.bk, rs, ip.n0);
+            auto load_b = [&](long long gi, const ItemPos &ip, int kb, int nblk) {
+                const uint32_t grp = (uint32_t)(gi % NG);
+                if (leader) ptx::mbar_arrive_expect_tx(&full[grp * G], tx * (uint32_t)nblk);
+                for (int j = 0; j < nblk; ++j) {
+                    const uint32_t slot = grp * G + j;
+                    const int rs = (kb + j) / a.c_blocks, cb = (kb + j) - rs * a.c_blocks;
+                    if constexpr (kPair) ptx::tma_load_3d_pair(smB + slot * b_bytes, &tmB, &full[grp * G], cb * a.bk, rs, ip.n0);
+                    else ptx::tma_load_3d(smB + slot * b_bytes, &tmB, &full[grp * G], cb * a.bk, rs, ip.n0);
+                }
             };
-            auto load_a = [&](long long g, const ItemPos &ip, int kb) {
-                const uint32_t stage = (uint32_t)(g % a.stages);
-                uint8_t *dst = smA + stage * a_bytes;
-                const int rs = kb / a.c_blocks, cb = kb - rs * a.c_blocks;
-                if (a.a_tiled) {
-                    if constexpr (kPair) ptx::tma_load_2d_pair(dst, &tmA, &full[stage], cb * a.bk, ip.m0);
-                    else ptx::tma_load_2d(dst, &tmA, &full[stage], cb * a.bk, ip.m0);
-                } else {
-                    const int r = rs / a.S, s = rs - r * a.S;
-                    if constexpr (kPair)
-                        ptx::tma_load_im2col_4d_pair(dst, &tmA, &full[stage], cb * a.bk, ip.wc, ip.hc, ip.nimg,
-                                                     (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
-                    else
-                        ptx::tma_load_im2col_4d(dst, &tmA, &full[stage], cb * a.bk, ip.wc, ip.hc, ip.nimg,
-                                                (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+            auto load_a = [&](long long gi, const ItemPos &ip, int kb, int nblk) {
+                const uint32_t grp = (uint32_t)(gi % NG);
+                for (int j = 0; j < nblk; ++j) {
+                    const uint32_t slot = grp * G + j;
+                    uint8_t *dst = smA + slot * a_bytes;
+                    const int rs = (kb + j) / a.c_blocks, cb = (kb + j) - rs * a.c_blocks;
+                    if (a.a_tiled) {
+                        if constexpr (kPair) ptx::tma_load_2d_pair(dst, &tmA, &full[grp * G], cb * a.bk, ip.m0);
+                        else ptx::tma_load_2d(dst, &tmA, &full[grp * G], cb * a.bk, ip.m0);
+                    } else {
+                        const int r = rs / a.S, s = rs - r * a.S;
+                        if constexpr (kPair)
+                            ptx::tma_load_im2col_4d_pair(dst, &tmA, &full[grp * G], cb * a.bk, ip.wc, ip.hc, ip.nimg,
+                                                         (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                        else
+                            ptx::tma_load_im2col_4d(dst, &tmA, &full[grp * G], cb * a.bk, ip.wc, ip.hc, ip.nimg,
+                                                    (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                    }
                 }
             };
             // PDL: the ring starts empty, so this producer's first-pass weight boxes go out before
             // griddepcontrol.wait (the previous grid may still write this conv's input, never its weights)
-            walk([&](long long g, const ItemPos &ip, int kb) {
-                if (g >= a.stages) return false;
-                load_b(g, ip, kb);
+            walk([&](long long gi, const ItemPos &ip, int kb, int nblk) {
+                if (gi >= NG) return false;
+                load_b(gi, ip, kb, nblk);
                 return true;
             });
             asm volatile("griddepcontrol.wait;" ::: "memory");
             if (dbg && pid == 0) dbg[7] = ptx::globaltimer();
-            walk([&](long long g, const ItemPos &ip, int kb) {
-                if (g >= a.stages) {
-                    ptx::mbar_wait(&empty[(uint32_t)(g % a.stages)], (uint32_t)((g / a.stages) & 1) ^ 1u);
-                    load_b(g, ip, kb);
+            walk([&](long long gi, const ItemPos &ip, int kb, int nblk) {
+                if (gi >= NG) {
+                    ptx::mbar_wait(&empty[(uint32_t)(gi % NG) * G], (uint32_t)((gi / NG) & 1) ^ 1u);
+                    load_b(gi, ip, kb, nblk);
                 }
-                load_a(g, ip, kb);
+                load_a(gi, ip, kb, nblk);
                 return true;
             });
         }
@@ -1289,38 +1302,46 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 int cb = kb0 % a.c_blocks;
                 int rs = kb0 / a.c_blocks;
                 int r = rs / a.S, s = rs % a.S;
-                for (int kb = kb0; kb < kb1; ++kb) {
+                const int G = a.kgroup;   // K blocks per barrier group (slot stage .. stage + G - 1)
+                for (int kb = kb0; kb < kb1; kb += G) {
+                    const int nblk = min(G, kb1 - kb);
+                    uint64_t *fb = &full[stage];
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     // experiment (dbg_flags & 8): issue times of the first tile's A (B) loads
                     if (dbg && (WPK_DBG_FLAGS(a) & 8) && w == wstart && kb - kb0 < 16 && half == 0)
                         dbg[(isA ? 16 : 32) + (kb - kb0)] = ptx::globaltimer();
-                    uint8_t *dst = dst0 + stage * sstride;
-                    if constexpr (kPair) {
-                        // both CTAs' bytes land on the leader's barrier; only the leader arms it
-                        if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * tx);
-                        if (!isA)
-                            ptx::tma_load_3d_pair(dst, &tmB, &full[stage], cb * a.bk, rs, n0);
-                        else if (a.a_tiled)
-                            ptx::tma_load_2d_pair(dst, &tmA, &full[stage], cb * a.bk, (int)m0);
-                        else
-                            ptx::tma_load_im2col_4d_pair(dst, &tmA, &full[stage], cb * a.bk, wc, hc, nimg,
-                                                         (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                    if constexpr (kPair) {   // both CTAs' bytes land on the leader's barrier; only the leader arms it
+                        if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * tx * (uint32_t)nblk);
                     } else {
-                        ptx::mbar_arrive_expect_tx(&full[stage], tx);
-                        if (!isA)
-                            ptx::tma_load_3d(dst, &tmB, &full[stage], cb * a.bk, rs, n0);
-                        else if (a.a_tiled)
-                            ptx::tma_load_2d(dst, &tmA, &full[stage], cb * a.bk, (int)m0);
-                        else
-                            ptx::tma_load_im2col_4d(dst, &tmA, &full[stage], cb * a.bk, wc, hc, nimg,
-                                                    (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                        ptx::mbar_arrive_expect_tx(fb, tx * (uint32_t)nblk);
                     }
-                    if (++cb == a.c_blocks) {
-                        cb = 0;
-                        ++rs;
-                        if (++s == a.S) { s = 0; ++r; }
+                    for (int j = 0; j < nblk; ++j) {
+                        uint8_t *dst = dst0 + (stage + j) * sstride;
+                        if constexpr (kPair) {
+                            if (!isA)
+                                ptx::tma_load_3d_pair(dst, &tmB, fb, cb * a.bk, rs, n0);
+                            else if (a.a_tiled)
+                                ptx::tma_load_2d_pair(dst, &tmA, fb, cb * a.bk, (int)m0);
+                            else
+                                ptx::tma_load_im2col_4d_pair(dst, &tmA, fb, cb * a.bk, wc, hc, nimg,
+                                                             (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                        } else {
+                            if (!isA)
+                                ptx::tma_load_3d(dst, &tmB, fb, cb * a.bk, rs, n0);
+                            else if (a.a_tiled)
+                                ptx::tma_load_2d(dst, &tmA, fb, cb * a.bk, (int)m0);
+                            else
+                                ptx::tma_load_im2col_4d(dst, &tmA, fb, cb * a.bk, wc, hc, nimg,
+                                                        (uint16_t)(s * a.dil_w), (uint16_t)(r * a.dil_h));
+                        }
+                        if (++cb == a.c_blocks) {
+                            cb = 0;
+                            ++rs;
+                            if (++s == a.S) { s = 0; ++r; }
+                        }
                     }
-                    if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
+                    stage += G;
+                    if (stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
                 }
             }
         }
@@ -1372,7 +1393,9 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 const uint32_t d_tmem = tmem_base + acc * acc_cols;
                 const bool cyc = dbg && (WPK_DBG_FLAGS(a) & 128) && w == wstart;   // cycle accounting, first tile
                 long long c_wait = 0, c_issue = 0, c_t0 = cyc ? clock64() : 0, c1 = 0;
-                for (int kb = kb0; kb < kb1; ++kb) {
+                const int G = a.kgroup;   // K blocks per barrier group (slots stage .. stage + G - 1)
+                for (int kb = kb0; kb < kb1; kb += G) {
+                    const int nblk = min(G, kb1 - kb);
                     const long long c0 = cyc ? clock64() : 0;
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
@@ -1383,39 +1406,43 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                     if (dbg && w == wstart && kb == kb0) dbg[2] = ptx::globaltimer();
                     if (dbg && dit < 8 && kb == kb0 && !(WPK_DBG_FLAGS(a) & 8)) dbg[16 + dit * 6 + 1] = ptx::globaltimer();
                     if (dbg && (WPK_DBG_FLAGS(a) & 8) && w == wstart && kb - kb0 < 16) dbg[48 + (kb - kb0)] = ptx::globaltimer();
-                    const uint64_t ad = a_desc0 + (uint64_t)((stage * a_bytes) >> 4);
-                    const uint64_t bd = b_desc0 + (uint64_t)((stage * b_bytes) >> 4);
                     if (!kConv || ptx::elect_one()) {
+                    for (int j = 0; j < nblk; ++j) {
+                    const uint64_t ad = a_desc0 + (uint64_t)(((stage + j) * a_bytes) >> 4);
+                    const uint64_t bd = b_desc0 + (uint64_t)(((stage + j) * b_bytes) >> 4);
+                    const bool first = (kb == kb0 && j == 0);   // the work item's first K block
                     if constexpr (kPair) {
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             if constexpr (DUAL)   // even K steps -> accumulator 0, odd -> accumulator 1
                                 ptx::umma2<kKind>(d_tmem + (kk & 1) * a.bn, ad + 2 * kk, bd + 2 * kk, a.idesc,
-                                                  (kb > kb0 || kk > 1) ? 1u : 0u);
+                                                  (!first || kk > 1) ? 1u : 0u);
                             else
-                                ptx::umma2<kKind>(d_tmem, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                                ptx::umma2<kKind>(d_tmem, ad + 2 * kk, bd + 2 * kk, a.idesc, (!first || kk > 0) ? 1u : 0u);
                         }
-                        ptx::umma_commit2_multicast(&empty[stage]);   // frees the stage in both CTAs
                     } else {
                         if constexpr (DUAL) {   // even K steps -> accumulator 0, odd -> accumulator 1 (BN columns on)
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk)
                                 ptx::umma<kKind>(d_tmem + (kk & 1) * a.bn, ad + 2 * kk, bd + 2 * kk, a.idesc,
-                                                 (kb > kb0 || kk > 1) ? 1u : 0u);
+                                                 (!first || kk > 1) ? 1u : 0u);
                         } else {
                             for (int h = 0; h < nsub; ++h) {
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)   // 4 x 32 bytes of K per 128-byte stage (+2 desc units)
                                     ptx::umma<kKind>(d_tmem + h * a.bn, ad + h * (16384 >> 4) + 2 * kk, bd + 2 * kk, a.idesc,
-                                                     (kb > kb0 || kk > 0) ? 1u : 0u);
+                                                     (!first || kk > 0) ? 1u : 0u);
                             }
                         }
-                        ptx::umma_commit(&empty[stage]);   // frees this smem stage when the MMAs finish
                     }
+                    }
+                    if constexpr (kPair) ptx::umma_commit2_multicast(&empty[stage]);   // frees the group's slots in both CTAs
+                    else ptx::umma_commit(&empty[stage]);                               // frees the group's slots when the MMAs finish
                     }
                     if (kConv) __syncwarp();
                     if (cyc) c_issue += clock64() - c1;
-                    if (++stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
+                    stage += G;
+                    if (stage == (uint32_t)a.stages) { stage = 0; phase ^= 1; }
                 }
                 if (cyc && lane == 0) {
                     dbg[60] = (unsigned long long)c_wait;

@@ -78,7 +78,8 @@ struct UmmaGeom {
     int cpad;           // channel count as stored for the kernel (C rounded up to the alignment)
     int pair;           // 1: tcgen05 CTA pair (cta_group::2, cluster of 2), 256 x BLOCK_N tiles
     int kdual;          // 1: two accumulators per tile (even / odd 16-wide K steps), summed in the epilogue
-    int prod_rr;        // 1: TMA producers deal K blocks round robin over 3 warps (A_MODE 4)
+    int prod_rr;        // 1: TMA producers deal K blocks round robin over 3 warps (A_MODE 4 / 6)
+    int kgroup;         // K blocks per full / empty barrier group: 2 for A_MODE 5 / 6, else 1
     int a_mode;         // 0: TMA im2col (or tiled for 1x1), 1: explicit im2col matrix in the workspace,
                         // 2: element gather into smem, 3: pixel-segment gather (C <= 4)
     int seg_sp;         // A_MODE 3: filter columns per row padded to whole 16-byte chunks

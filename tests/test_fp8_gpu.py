@@ -74,7 +74,7 @@ def test_fp8_every_config_bit_exact():
     xl, wl = to_layout(x, w, "nhwc")
     xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
     n = 0
-    for genes in itertools.product([16, 32, 64, 128, 192, 256], [2, 4, 6], [1, 2, 4], range(8), [0, 4], [1, 2, 4],
+    for genes in itertools.product([16, 32, 64, 128, 192, 256], [2, 4, 6], [1, 2, 4], range(8), [0, 4, 5, 6], [1, 2, 4],
                                    [128, 256]):
         genes = list(genes)
         if not plan.config_valid(1, genes):

@@ -68,7 +68,7 @@ def test_epilogues(dtype, epilogue):
 def _umma_space():
     bns = [16, 32, 64, 96, 128, 192, 256]
     out = []
-    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1, 2, 3, 4, 5, 6, 7], [0, 1, 2, 4],
+    for bn, st, sp, ra, amode, acc, bm in itertools.product(bns, [2, 4, 6], [1, 2, 4], [0, 1, 2, 3, 4, 5, 6, 7], [0, 1, 2, 4, 5, 6],
                                                           [1, 2, 4], [128, 256]):
         out.append((bn, st, sp, ra, amode, acc, bm))
     return out
@@ -141,8 +141,9 @@ def test_cta_pair_configs(dtype):
         xl, wl = to_layout(x, w, "nhwc")
         xl, wl, bc = xl.cuda(), wl.cuda(), b.cuda()
         n = 0
-        for bn, st, mode, acc, sp in itertools.product([32, 64, 128, 256], [2, 4], [2, 3], [1, 2, 4], [1, 2, 4]):
-            genes = [bn, st, sp, mode, 0, acc, 256]
+        for bn, st, mode, acc, sp, am in itertools.product([32, 64, 128, 256], [2, 4], [2, 3], [1, 2, 4], [1, 2, 4],
+                                                           [0, 5]):
+            genes = [bn, st, sp, mode, am, acc, 256]
             if not plan.config_valid(1, genes):
                 continue
             plan.set_config(1, genes)
