@@ -173,6 +173,8 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
     // work item per full / empty barrier pair (one expect_tx, one wait and one MMA commit per two
     // blocks); STAGES counts K-block slots, so it must be even and >= 4 (>= 2 groups in flight)
     if (g->a_mode == 5 || g->a_mode == 6) {
+        static const int no_kgroup = env_knob("WPK_NO_KGROUP", 0);   // A/B experiments only
+        if (no_kgroup) return no("A_MODE 5/6 disabled (WPK_NO_KGROUP)");
         if (g->stages % 2 || g->stages < 4) return no("A_MODE 5/6 (K groups of 2) need an even STAGES >= 4");
         g->prod_rr = (g->a_mode == 6) ? 1 : 0;
         g->a_mode = 0;
