@@ -178,7 +178,8 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
         if (g->stages % 2 || g->stages < 4) return no("A_MODE 5/6 (K groups of 2) need an even STAGES >= 4");
         g->prod_rr = (g->a_mode == 6) ? 1 : 0;
         g->a_mode = 0;
-        g->kgroup = 2;
+        static const int kg_half = env_knob("WPK_KG_HALF", 0);   // experiment: two groups of STAGES/2 blocks
+        g->kgroup = kg_half ? g->stages / 2 : 2;
     }
     g->acc_stages = cfg.genes[5];
     g->seg_sp = 0; g->seg_hp = 0; g->seg_wp = 0; g->seg_fast = 0; g->seg_two = 0;

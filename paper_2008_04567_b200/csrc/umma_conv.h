@@ -13,7 +13,9 @@ namespace wpk {
 enum { DT_F16 = 0, DT_BF16 = 1, DT_TF32 = 2, DT_FP8 = 3 };   // DT_FP8: e4m3 x / w, bf16 b / z / y
 // A producer kinds: TMA (im2col / tiled), TMA for a CTA pair, element gather (A_MODE 2),
 // pixel-segment gather (A_MODE 3)
-enum { AK_TMA = 0, AK_PAIR = 1, AK_GATHER = 2, AK_SEG = 3, AK_DW = 4 };   // AK_DW: fused depthwise producer (wpk_dwpw_*)
+// AK_DW: fused depthwise producer (wpk_dwpw_*); AK_TMA_KG2 / AK_PAIR_KG2: the TMA producers with K groups
+// of two blocks per barrier pair (A_MODE 5 / 6; the group size is a template constant)
+enum { AK_TMA = 0, AK_PAIR = 1, AK_GATHER = 2, AK_SEG = 3, AK_DW = 4, AK_TMA_KG2 = 5, AK_PAIR_KG2 = 6 };
 // epilogue kinds: final output via TMA store, split-K partials via TMA store (+ in-kernel fixup),
 // direct global stores (NCHW output or K not a multiple of the 128-byte chunk; final or partial)
 enum { EK_TMA = 0, EK_SPLIT = 1, EK_DIRECT = 2, EK_CSPLIT = 3 };   // EK_CSPLIT: split-K over a cluster (DSMEM)

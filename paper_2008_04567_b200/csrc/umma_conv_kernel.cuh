@@ -1069,15 +1069,18 @@ __device__ __forceinline__ void prefetch_a_rows(const UmmaArgs &a, long long m0,
 // 2 = B producer, 3 = spare, 4..11 = epilogue (two groups of four; warp w reads TMEM lanes
 // [32*(w%4), +32)), 12..15 = gather producers.
 template <int DT, int AK, int EK, bool RES = false, bool DUAL = false>
-__global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
+__global__ void __launch_bounds__((AK >= AK_GATHER && AK <= AK_DW) ? 512 : 384, 1)
     umma_conv_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmP,
                      const __grid_constant__ UmmaArgs a) {
     using T = typename OutT<DT>::T;
     constexpr bool kTF32 = (DT == DT_TF32);
     constexpr int kKind = (DT == DT_TF32) ? 1 : (DT == DT_FP8) ? 2 : 0;   // tcgen05.mma kind
-    constexpr bool kPair = (AK == AK_PAIR);
-    constexpr bool kGather = (AK >= AK_GATHER);
+    constexpr bool kPair = (AK == AK_PAIR || AK == AK_PAIR_KG2);
+    constexpr bool kGather = (AK >= AK_GATHER && AK <= AK_DW);
+    // K blocks per full / empty barrier group: a compile-time constant, so the one-block variants
+    // keep the plain loops (a runtime group size cost ~5% of the step in instruction footprint)
+    constexpr int KG = (AK == AK_TMA_KG2 || AK == AK_PAIR_KG2) ? 2 : 1;
 
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = ptx::smem_u32(smem_raw);
@@ -1168,7 +1171,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
         // K groups (a.kgroup = G in {1, 2}): G consecutive K blocks of a work item share one full /
         // empty barrier pair (the first slot's), so one expect_tx / wait / commit serves G blocks;
         // a producer loads whole groups: group gi (ring group gi % NG) belongs to producer gi % NPROD.
-        const int G = a.kgroup;
+        constexpr int G = KG;
         const int NG = a.stages / G;                   // barrier groups in the ring
         const int NPROD = min(3, NG);
         const int pid = (warp == 0) ? 0 : warp - 1;
@@ -1206,6 +1209,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             auto load_b = [&](long long gi, const ItemPos &ip, int kb, int nblk) {
                 const uint32_t grp = (uint32_t)(gi % NG);
                 if (leader) ptx::mbar_arrive_expect_tx(&full[grp * G], tx * (uint32_t)nblk);
+#pragma unroll 1
                 for (int j = 0; j < nblk; ++j) {
                     const uint32_t slot = grp * G + j;
                     const int rs = (kb + j) / a.c_blocks, cb = (kb + j) - rs * a.c_blocks;
@@ -1215,6 +1219,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
             };
             auto load_a = [&](long long gi, const ItemPos &ip, int kb, int nblk) {
                 const uint32_t grp = (uint32_t)(gi % NG);
+#pragma unroll 1
                 for (int j = 0; j < nblk; ++j) {
                     const uint32_t slot = grp * G + j;
                     uint8_t *dst = smA + slot * a_bytes;
@@ -1302,7 +1307,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 int cb = kb0 % a.c_blocks;
                 int rs = kb0 / a.c_blocks;
                 int r = rs / a.S, s = rs % a.S;
-                const int G = a.kgroup;   // K blocks per barrier group (slot stage .. stage + G - 1)
+                constexpr int G = KG;   // K blocks per barrier group (slot stage .. stage + G - 1)
                 for (int kb = kb0; kb < kb1; kb += G) {
                     const int nblk = min(G, kb1 - kb);
                     uint64_t *fb = &full[stage];
@@ -1315,6 +1320,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                     } else {
                         ptx::mbar_arrive_expect_tx(fb, tx * (uint32_t)nblk);
                     }
+#pragma unroll 1
                     for (int j = 0; j < nblk; ++j) {
                         uint8_t *dst = dst0 + (stage + j) * sstride;
                         if constexpr (kPair) {
@@ -1393,7 +1399,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                 const uint32_t d_tmem = tmem_base + acc * acc_cols;
                 const bool cyc = dbg && (WPK_DBG_FLAGS(a) & 128) && w == wstart;   // cycle accounting, first tile
                 long long c_wait = 0, c_issue = 0, c_t0 = cyc ? clock64() : 0, c1 = 0;
-                const int G = a.kgroup;   // K blocks per barrier group (slots stage .. stage + G - 1)
+                constexpr int G = KG;   // K blocks per barrier group (slots stage .. stage + G - 1)
                 for (int kb = kb0; kb < kb1; kb += G) {
                     const int nblk = min(G, kb1 - kb);
                     const long long c0 = cyc ? clock64() : 0;
@@ -1407,6 +1413,7 @@ __global__ void __launch_bounds__(AK >= AK_GATHER ? 512 : 384, 1)
                     if (dbg && dit < 8 && kb == kb0 && !(WPK_DBG_FLAGS(a) & 8)) dbg[16 + dit * 6 + 1] = ptx::globaltimer();
                     if (dbg && (WPK_DBG_FLAGS(a) & 8) && w == wstart && kb - kb0 < 16) dbg[48 + (kb - kb0)] = ptx::globaltimer();
                     if (!kConv || ptx::elect_one()) {
+#pragma unroll 1
                     for (int j = 0; j < nblk; ++j) {
                     const uint64_t ad = a_desc0 + (uint64_t)(((stage + j) * a_bytes) >> 4);
                     const uint64_t bd = b_desc0 + (uint64_t)(((stage + j) * b_bytes) >> 4);
@@ -1661,7 +1668,7 @@ static cudaError_t launch_variant(cudaLaunchConfig_t &lc, const CUtensorMap &tmA
 template <int DT, int AK>
 static cudaError_t launch_ak(int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                              const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
-    if constexpr (AK == AK_TMA || AK == AK_PAIR) {   // dual accumulators (MODE bit 2): TMA A producers only (plan validation)
+    if constexpr (AK == AK_TMA || AK == AK_PAIR || AK == AK_TMA_KG2 || AK == AK_PAIR_KG2) {   // dual accumulators (MODE bit 2): TMA A producers only (plan validation)
         if (a.kdual) {
             if (ek == EK_TMA)
                 return a.epilogue == 3 ? launch_variant<DT, AK, EK_TMA, true, true>(lc, tmA, tmB, tmY, tmP, a)
@@ -1675,7 +1682,7 @@ static cudaError_t launch_ak(int ek, cudaLaunchConfig_t &lc, const CUtensorMap &
                                : launch_variant<DT, AK, EK_TMA, false>(lc, tmA, tmB, tmY, tmP, a);
     if (ek == EK_SPLIT) return launch_variant<DT, AK, EK_SPLIT>(lc, tmA, tmB, tmY, tmP, a);
     if (ek == EK_CSPLIT) {
-        if constexpr (AK == AK_TMA) return launch_variant<DT, AK, EK_CSPLIT>(lc, tmA, tmB, tmY, tmP, a);
+        if constexpr (AK == AK_TMA || AK == AK_TMA_KG2) return launch_variant<DT, AK, EK_CSPLIT>(lc, tmA, tmB, tmY, tmP, a);
         else return cudaErrorInvalidConfiguration;   // plan validation never pairs these
     }
     return launch_variant<DT, AK, EK_DIRECT>(lc, tmA, tmB, tmY, tmP, a);
@@ -1684,7 +1691,8 @@ static cudaError_t launch_ak(int ek, cudaLaunchConfig_t &lc, const CUtensorMap &
 template <int DT>
 cudaError_t umma_launch_dt(int ak, int ek, cudaLaunchConfig_t &lc, const CUtensorMap &tmA, const CUtensorMap &tmB,
                            const CUtensorMap &tmY, const CUtensorMap &tmP, const UmmaArgs &a) {
-    if (ak == AK_PAIR) return launch_ak<DT, AK_PAIR>(ek, lc, tmA, tmB, tmY, tmP, a);
+    if (ak == AK_PAIR) return a.kgroup == 2 ? launch_ak<DT, AK_PAIR_KG2>(ek, lc, tmA, tmB, tmY, tmP, a)
+                                            : launch_ak<DT, AK_PAIR>(ek, lc, tmA, tmB, tmY, tmP, a);
     if constexpr (DT == DT_FP8) {   // e4m3: TMA A producers only (plan validation)
         if (ak != AK_TMA) return cudaErrorInvalidConfiguration;
     } else {
@@ -1694,7 +1702,8 @@ cudaError_t umma_launch_dt(int ak, int ek, cudaLaunchConfig_t &lc, const CUtenso
             if (ak == AK_DW) return launch_ak<DT, AK_DW>(ek, lc, tmA, tmB, tmY, tmP, a);
         }
     }
-    return launch_ak<DT, AK_TMA>(ek, lc, tmA, tmB, tmY, tmP, a);
+    return a.kgroup == 2 ? launch_ak<DT, AK_TMA_KG2>(ek, lc, tmA, tmB, tmY, tmP, a)
+                         : launch_ak<DT, AK_TMA>(ek, lc, tmA, tmB, tmY, tmP, a);
 }
 
 }  // namespace wpk

@@ -1,6 +1,7 @@
 """Measure every valid tcgen05 config of a grid on given ResNet-50 N=32 bf16 layers with the tuner's
 protocol (wpk_conv2d_measure, rotating cold copies) -- how close the GA's pick is to the grid's best.
-usage: python tools/grid_measure.py CONFIGS_JSON LAYER [LAYER ...] > out.json"""
+usage: python tools/grid_measure.py CONFIGS_JSON LAYER [LAYER ...] > out.json
+(GRID_KG_ONLY=1: only the K-group producers A_MODE 5 / 6)"""
 import itertools
 import json
 import os
@@ -16,7 +17,8 @@ for name in sys.argv[2:]:
     L = next(l for l in workloads.resnet50(32) if l.name == name)
     plan = Conv2dPlan(L.n, L.c, L.h, L.w, L.k, L.r, L.s, L.stride, L.pad, layout="nhwc", dtype="bf16")
     res = []
-    for g in itertools.product([64, 128, 192, 256], [4, 6, 8], [1, 2], range(8), [0, 4, 5, 6], [1, 2], [128, 256]):
+    amodes = [5, 6] if os.environ.get("GRID_KG_ONLY") else [0, 4, 5, 6]
+    for g in itertools.product([64, 128, 192, 256], [4, 6, 8], [1, 2], range(8), amodes, [1, 2], [128, 256]):
         g = list(g)
         if not plan.config_valid(1, g):
             continue
