@@ -92,7 +92,9 @@ typedef enum { WPK_EVAL_MEASURED = 0, WPK_EVAL_REPLAY = 1, WPK_EVAL_SYNTHETIC = 
  *                     5 / 6 = A_MODE 0 / 4 with K groups: two consecutive K blocks share one full /
  *                     empty barrier pair (STAGES = K-block slots, even, >= 4). Grouped plans
  *                     (1 < groups < C, NHWC 16-bit) accept only A_MODE 1 = the tensor-core grouped
- *                     kernel, genes {BLOCK_N, 2, 1, 0, 1, 1, 128}; fused depthwise+pointwise plans
+ *                     kernel, genes {BLOCK_N, 2, 1, 0, 1, 1, 128} (a handful of valid points: set them
+ *                     with wpk_conv2d_set_config / measure, a sampled search rejects most draws);
+ *                     fused depthwise+pointwise plans
  *                     accept A_MODE 0 (depthwise producer warps) and 1 (one tile per CTA)
  *   WPK_FAMILY_DW   : grouped conv on CUDA cores, groups > 1: depthwise (groups == C == K, vector
  *                     over channels) or general groups (vector over VEC_C outputs of one group,

@@ -875,6 +875,8 @@ wpk_status wpk_conv2d_fold_batchnorm(wpk_plan plan, const void *w, const void *b
     const ConvDesc &d = p->d;
     if (d.dtype == WPK_FP8E4M3)
         return fail(WPK_ERR_UNSUPPORTED, "fold_batchnorm: FP8 plans take pre-folded (and pre-quantised) weights");
+    if (d.fused_dw)
+        return fail(WPK_ERR_UNSUPPORTED, "fold_batchnorm: fold each conv of a fused depthwise+pointwise plan with its own plain plan");
     const long long per_k = (long long)(d.c / d.g) * d.r * d.s;
     const long long total = (long long)d.k * per_k + d.k;
     const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 4096);

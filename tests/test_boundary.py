@@ -285,3 +285,14 @@ def test_grouped_tensor_core_configs_host_validation():
     h = plan(32, 32, 32)                         # depthwise
     assert not ok(h, 16) and b"depthwise" in lib.wpk_last_error()
     lib.wpk_conv2d_destroy(h)
+
+
+def test_dwpw_plan_refuses_batchnorm_fold():
+    lib = L.load()
+    shp = L.make_shape(n=1, c=144, h=14, w=14, k=144, r=3, s=3, stride=1, pad=1, groups=144, layout="nhwc")
+    h = ctypes.c_void_p()
+    assert lib.wpk_dwpw_plan(ctypes.byref(shp), 24, 1, L.DTYPES["bf16"], 0, ctypes.byref(h)) == 0
+    f = ctypes.c_void_p(16)
+    st = lib.wpk_conv2d_fold_batchnorm(h, f, None, f, f, f, f, ctypes.c_float(1e-5), f, f, None)
+    assert st == L.ERR_UNSUPPORTED and b"fused" in lib.wpk_last_error()
+    lib.wpk_conv2d_destroy(h)
