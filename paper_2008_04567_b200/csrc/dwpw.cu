@@ -180,14 +180,19 @@ __global__ void __launch_bounds__(kThreads) dwpw_kernel(const DwpwArgs a) {
     asm volatile("griddepcontrol.wait;" ::: "memory");   // x may still be written upstream, y read
 
     const int m0 = blockIdx.x * kRows;
-    const int nkc = (a.C + 63) / 64;
+    // split-K over the channel chunks (blockIdx.y = split s of a.splits): chunks [kc0, kc1)
+    const int nkc_all = (a.C + 63) / 64;
+    const int kc0 = blockIdx.y * a.kc_per_split;
+    const int kc1 = min(nkc_all, kc0 + a.kc_per_split);
+    const int nkc = kc1 - kc0;
     const int cv = a.C >> 3;
     const uint4 *__restrict__ wpw = static_cast<const uint4 *>(a.w_pw);
     const bool r3 = a.R == 3 && a.S == 3;
     uint32_t ph0 = 0, ph1 = 0;
-    for (int kc = 0; kc < nkc; ++kc) {
-        const int b = kc & 1;
-        if (kc >= 2) {   // the MMAs of chunk kc - 2 have finished reading buffer b
+    for (int kci = 0; kci < nkc; ++kci) {
+        const int kc = kc0 + kci;
+        const int b = kci & 1;
+        if (kci >= 2) {   // the MMAs of chunk kc - 2 have finished reading buffer b
             if (b == 0) { ptx::mbar_wait(&bars[0], ph0); ph0 ^= 1; }
             else { ptx::mbar_wait(&bars[1], ph1); ph1 ^= 1; }
         }
@@ -211,10 +216,10 @@ __global__ void __launch_bounds__(kThreads) dwpw_kernel(const DwpwArgs a) {
                 const uint64_t bd = ptx::sw128_kmajor_desc(bB);
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {   // 4 x 16 channels of the 64-channel chunk (+32 B each)
-                    ptx::umma<0>(tmem, ad + 2 * kk, bd + 2 * kk, a.idesc0, (kc > 0 || kk > 0) ? 1u : 0u);
+                    ptx::umma<0>(tmem, ad + 2 * kk, bd + 2 * kk, a.idesc0, (kci > 0 || kk > 0) ? 1u : 0u);
                     if (kp > 256)   // columns 256.. of a wide K_out: the next 256 rows of B
                         ptx::umma<0>(tmem + 256, ad + 2 * kk, bd + (uint64_t)((256 * 128) >> 4) + 2 * kk, a.idesc1,
-                                     (kc > 0 || kk > 0) ? 1u : 0u);
+                                     (kci > 0 || kk > 0) ? 1u : 0u);
                 }
                 ptx::umma_commit(&bars[b]);   // buffer b free (and, for the last chunk, the accumulator ready)
             }
@@ -238,7 +243,14 @@ __global__ void __launch_bounds__(kThreads) dwpw_kernel(const DwpwArgs a) {
         uint32_t r[16];
         ptx::tmem_ld16_nowait(tl + (uint32_t)c0, r);
         ptx::tmem_wait_ld();
-        if (m < a.M) {
+        if (m < a.M && a.splits > 1) {   // split-K: this split's fp32 partial, no bias / epilogue
+            float4 *dst = reinterpret_cast<float4 *>(a.partial + ((size_t)blockIdx.y * a.M + m) * a.K + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (c0 + 4 * q + 4 <= a.K)
+                    dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                         __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        } else if (m < a.M) {
             uint32_t o[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
@@ -259,6 +271,37 @@ __global__ void __launch_bounds__(kThreads) dwpw_kernel(const DwpwArgs a) {
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 0) ptx::tmem_dealloc(tmem, a.tmem_cols);
+}
+
+// split-K reduction: y = RN(pw_epi(sum_{s = 0..S-1} partial[s] + b_pw)), the partials summed in split
+// order (deterministic); one thread per 8 consecutive outputs (K_out % 8 == 0)
+template <typename T>
+__global__ void dwpw_reduce_kernel(const DwpwArgs a) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const long long n8 = (long long)a.M * a.K / 8;
+    const T *__restrict__ bpw = static_cast<const T *>(a.b_pw);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+        const long long e0 = i * 8;
+        const int k0 = (int)(e0 % a.K);
+        float v[8];
+        const float4 *p0 = reinterpret_cast<const float4 *>(a.partial + e0);
+        float4 u = p0[0], w = p0[1];
+        v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w; v[4] = w.x; v[5] = w.y; v[6] = w.z; v[7] = w.w;
+        for (int s = 1; s < a.splits; ++s) {
+            const float4 *ps = reinterpret_cast<const float4 *>(a.partial + (size_t)s * a.M * a.K + e0);
+            u = ps[0]; w = ps[1];
+            v[0] += u.x; v[1] += u.y; v[2] += u.z; v[3] += u.w; v[4] += w.x; v[5] += w.y; v[6] += w.z; v[7] += w.w;
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float v0 = v[2 * e], v1 = v[2 * e + 1];
+            if (a.pw_epi >= 1) { v0 += static_cast<float>(bpw[k0 + 2 * e]); v1 += static_cast<float>(bpw[k0 + 2 * e + 1]); }
+            if (a.pw_epi == 2) { v0 = fmaxf(v0, 0.f); v1 = fmaxf(v1, 0.f); }
+            o[e] = pack2(v0, v1, (T *)nullptr);
+        }
+        reinterpret_cast<uint4 *>(static_cast<T *>(a.y))[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
 }
 
 static uint32_t idesc_f16(bool bf16, int n) {   // kind::f16, fp32 accumulate, K-major A and B, M = 128
@@ -283,7 +326,10 @@ int dwpw_launch(DwpwArgs a, int dtype, void *stream, std::string *err) {
     a.idesc1 = idesc_f16(bf16, a.kp > 256 ? a.kp - 256 : 16);
     const size_t smem = dwpw_smem_bytes(a.kp);
     cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3((unsigned)((a.M + kRows - 1) / kRows));
+    const int nkc = (a.C + 63) / 64;
+    if (a.splits < 1) a.splits = 1;
+    a.kc_per_split = (nkc + a.splits - 1) / a.splits;
+    lc.gridDim = dim3((unsigned)((a.M + kRows - 1) / kRows), (unsigned)a.splits);
     lc.blockDim = dim3(kThreads);
     lc.dynamicSmemBytes = smem;
     lc.stream = (cudaStream_t)stream;
@@ -305,7 +351,21 @@ int dwpw_launch(DwpwArgs a, int dtype, void *stream, std::string *err) {
         *err = std::string("dwpw_kernel launch: ") + cudaGetErrorString(ce);
         return -1;
     }
-    return 1;
+    if (a.splits == 1) return 1;
+    cudaLaunchConfig_t rc{};
+    const long long n8 = (long long)a.M * a.K / 8;
+    rc.gridDim = dim3((unsigned)std::min<long long>((n8 + 255) / 256, 148 * 8));
+    rc.blockDim = dim3(256);
+    rc.stream = (cudaStream_t)stream;
+    rc.attrs = attr;
+    rc.numAttrs = 1;
+    ce = bf16 ? cudaLaunchKernelEx(&rc, dwpw_reduce_kernel<__nv_bfloat16>, a) : cudaLaunchKernelEx(&rc, dwpw_reduce_kernel<__half>, a);
+    if (ce == cudaSuccess) ce = cudaGetLastError();
+    if (ce != cudaSuccess) {
+        *err = std::string("dwpw_reduce_kernel launch: ") + cudaGetErrorString(ce);
+        return -1;
+    }
+    return 2;
 }
 
 }  // namespace wpk

@@ -18,6 +18,9 @@ struct DwpwArgs {
     int sh, sw, ph, pw, dh, dw;
     int dw_epi, pw_epi;     // 0 none, 1 bias, 2 bias + ReLU
     int kp;                 // K rounded up to 16 (set by dwpw_launch)
+    int splits;             // split-K over the 64-channel chunks (>= 1); > 1: fp32 partials + a reduction
+    int kc_per_split;       // chunks per split (set by dwpw_launch)
+    float *partial;         // [splits][M][K] fp32 (workspace) when splits > 1
     uint32_t tmem_cols, idesc0, idesc1;
 };
 

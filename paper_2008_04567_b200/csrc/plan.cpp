@@ -227,8 +227,14 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
         }
         if (g->bn < cover) return no("fused depthwise+pointwise: BLOCK_N must cover K_out (min(K_out, 256))");
         if (cfg.genes[4] == 1) {
-            if (g->bn != cover || g->stages != 2 || g->splits != 1 || cfg.genes[3] != 0 || g->acc_stages != 1 || g->bm != 128)
-                return no("fused depthwise+pointwise A_MODE 1: genes must be {cover(K_out), 2, 1, 0, 1, 1, 128}");
+            if (g->bn != cover || g->stages != 2 || cfg.genes[3] != 0 || g->acc_stages != 1 || g->bm != 128)
+                return no("fused depthwise+pointwise A_MODE 1: genes must be {cover(K_out), 2, SPLIT_K, 0, 1, 1, 128}");
+            // SPLIT_K: the 64-channel chunks split over SPLIT_K CTAs per tile (fp32 partials in the
+            // workspace, summed in split order by a second kernel)
+            const int nkc = (d.c + 63) / 64;
+            const int per = (nkc + g->splits - 1) / g->splits;
+            if (g->splits > nkc || (long long)(g->splits - 1) * per >= nkc)
+                return no("fused depthwise+pointwise A_MODE 1: SPLIT_K leaves an empty split");
             if (d.k % 8) return no("fused depthwise+pointwise A_MODE 1: K_out % 8 == 0 (16-byte output rows)");
             if (d.k > 512) return no("fused depthwise+pointwise A_MODE 1: K_out <= 512 (TMEM columns)");
             if (d.M() >= 2147483647LL - 128) return no("fused depthwise+pointwise A_MODE 1: M < 2^31");
@@ -236,10 +242,10 @@ bool umma_geometry(const ConvDesc &d, const Config &cfg, UmmaGeom *g, std::strin
             g->cpad = d.c;
             g->c_blocks = (d.c + 63) / 64;
             g->num_kb = g->c_blocks;
-            g->kb_per_split = g->num_kb;
+            g->kb_per_split = (g->num_kb + g->splits - 1) / g->splits;
             g->m_tiles = (int)((d.M() + 127) / 128);
             g->n_tiles = 1;
-            g->work = g->m_tiles;
+            g->work = (long long)g->m_tiles * g->splits;
             g->epi_tma = 0; g->csplit = 0; g->pair = 0; g->kdual = 0; g->prod_rr = 0; g->a_tiled = 0;
             g->smem_bytes = 1024 + 2 * 16384 + 2 * (size_t)round_up(d.k, 16) * 128 + 64;
             int cols = 32;

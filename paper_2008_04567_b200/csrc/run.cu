@@ -394,7 +394,7 @@ static WsLayout ws_layout(Plan &p, const Config &cfg, bool host_staging) {
         if (g.a_mode == 7) {
             // tensor-core grouped conv: NHWC x and [K][R][S][C/g] weights used as given
         } else if (g.a_mode == 5 || g.a_mode == 6) {   // fused depthwise: its weights re-laid [R][S][C]
-            L.w_off = off; L.w_bytes = al256((size_t)d.c * d.r * d.s * e); off += L.w_bytes;
+            L.w_off = off; L.w_bytes = al256((size_t)d.c * d.r * d.s * e); off += L.w_bytes;   // (+ split partials below)
         } else if (g.a_mode == 1) {
             L.x_off = off; L.x_bytes = al256((size_t)d.M() * g.cpad * e); off += L.x_bytes;
             L.w_off = off; L.w_bytes = al256((size_t)d.k * g.cpad * e); off += L.w_bytes;
@@ -612,6 +612,8 @@ int launch_conv(Plan &p, const Config &cfg, const void *x, const void *w, const 
             A.M = (int)d.M();
             A.sh = d.sh; A.sw = d.sw; A.ph = d.ph; A.pw = d.pw; A.dh = d.dh; A.dw = d.dw;
             A.dw_epi = d.dw_epi; A.pw_epi = d.epilogue;
+            A.splits = g.splits;
+            A.partial = g.splits > 1 ? reinterpret_cast<float *>(ws + L.p_off) : nullptr;
             int rc = dwpw_launch(A, d.dtype, stream, &err);
             if (rc < 0) { set_error(err); return -1; }
             return launches + rc;

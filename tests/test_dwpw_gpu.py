@@ -174,3 +174,23 @@ def test_dwpw_mobilenet_v2_n32_sampled():
     got = y[pts[:, 0], pts[:, 1], pts[:, 2], pts[:, 3]].double().numpy()
     err = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
     assert err <= TOL["bf16"], err
+
+
+@pytest.mark.parametrize("splits", [2, 4, 8])
+def test_dwpw_one_tile_kernel_split_k(splits):
+    """A_MODE 1 with SPLIT_K: the 64-channel chunks of a deep block (C = 960) split over CTAs, fp32
+    partials summed in split order by the reduction kernel (bias / epilogue there): bit-exact on
+    exact-integer inputs, within tolerance on uniform inputs."""
+    case = ("deep", 2, 960, 7, 9, 160, 1, 1, 1)
+    genes = [192, 2, splits, 0, 1, 1, 128]
+    for mode in ("int", "uniform"):
+        plan = _plan(case, "bf16")   # a fresh plan: the packed depthwise weights are cached per pointer
+        assert plan.config_valid(1, genes)
+        plan.set_config(1, genes)
+        x, w_dw, b_dw, w_pw, b_pw, conv = _inputs(case, "bf16", mode, seed=99)
+        ref = _oracle_chain(x, w_dw, b_dw, w_pw, b_pw, conv, torch.bfloat16)
+        y = _run(plan, x, w_dw, b_dw, w_pw, b_pw)
+        if mode == "int":
+            assert_bit_exact(y, ref)
+        else:
+            assert rel_error("bf16", y, ref) <= TOL["bf16"]

@@ -28,7 +28,30 @@ def run_block(bi, B, budget):
     xd = x.permute(0, 2, 3, 1).contiguous().cuda()
     wdw, bdw, wpw, bpw = w_dw.contiguous().cuda(), b_dw.cuda(), w_pw.contiguous().cuda(), b_pw.cuda()
     fused = DwPwPlan(n, c, h, w, k, 3, 3, L.stride, 1, 1, dw_epilogue="bias_relu", pw_epilogue="bias", dtype="bf16")
-    rf = fused.tune("ga", budget, seed=bi)
+    # GA over the fused plan's space, then every split of the one-tile-per-CTA kernel (A_MODE 1, a
+    # handful of configs) measured directly; keep the fastest. (For K_out = 320 the GA's rejection
+    # sampler -- 10^4 draws per individual, SPEC.md:190 -- finds no valid config: A_MODE 1 only.)
+    best = None
+    try:
+        rf = fused.tune("ga", budget, seed=bi)
+        best = (rf.best_us, rf.genes)
+    except Exception:
+        pass
+    bn0 = fused.config[1][0] if best is None else None
+    for sp in (1, 2, 4, 8, 16):
+        for bn in ([bn0] if bn0 else []) + [16, 32, 64, 96, 128, 192, 256]:
+            g = [bn, 2, sp, 0, 1, 1, 128]
+            if fused.config_valid(1, g):
+                fused.set_config(1, g)
+                us = fused.measure()
+                if best is None or us < best[0]:
+                    best = (us, g)
+                break
+    fused.set_config(1, best[1])
+
+    class _R:
+        genes = best[1]
+    rf = _R()
     pdw = Conv2dPlan(n, c, h, w, c, 3, 3, L.stride, 1, 1, c, layout="nhwc", dtype="bf16")
     pdw.tune("ga", budget, seed=bi)
     ppw = Conv2dPlan(n, c, pdw.p, pdw.q, k, 1, 1, 1, 0, layout="nhwc", epilogue="bias", dtype="bf16")
