@@ -62,33 +62,33 @@ __device__ __forceinline__ void mac8(float2 *acc, uint4 x, uint4 w) {
 constexpr int kThreads = 256;
 constexpr int kRows = 128;
 
-// depthwise result of (row, 8 channels) pairs: thread tid owns channel vector j = tid & 7 of rows
-// (tid >> 3) + 32 i, i < 4, two rows in flight per iteration (3x3: all 18 loads before the math)
+// depthwise result of the chunk's (row, 16-byte channel vector) pieces. Only the chunk's nvalid
+// real vectors are computed (C = 32, 96, 144 leave 4, 4, 2 of a chunk's 8): piece p = (row, j) =
+// (p / nvalid, p % nvalid), pieces tid and tid + 256 in flight per iteration (3x3: all 18 loads
+// before the math); the padded vectors j >= nvalid are written as zeros (the MMA reads them).
 template <typename T, bool R3>
 __device__ __forceinline__ void dw_chunk(const DwpwArgs &a, uint32_t sbase, int m0, int cvec0, int tid) {
     const int cv = a.C >> 3;
-    const int j = tid & 7;
-    const int cvec = cvec0 + j;
-    const bool cok = cvec < cv;
-    const uint4 *__restrict__ xj = static_cast<const uint4 *>(a.x) + cvec;
-    const uint4 *__restrict__ wj = static_cast<const uint4 *>(a.w_dw) + cvec;
-    float2 bf[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-    if (a.b_dw && cok) {
-        const uint4 b4 = __ldg(static_cast<const uint4 *>(a.b_dw) + cvec);
-        bf[0] = up2(b4.x, (T *)nullptr); bf[1] = up2(b4.y, (T *)nullptr);
-        bf[2] = up2(b4.z, (T *)nullptr); bf[3] = up2(b4.w, (T *)nullptr);
-    }
+    const int nvalid = min(8, cv - cvec0);
+    const int npieces = kRows * nvalid;
+    const uint4 *__restrict__ xv = static_cast<const uint4 *>(a.x);
+    const uint4 *__restrict__ wv = static_cast<const uint4 *>(a.w_dw);
+    const uint4 *__restrict__ bv = static_cast<const uint4 *>(a.b_dw);
     const int PQ = a.P * a.Q;
 #pragma unroll 1
-    for (int it = 0; it < 2; ++it) {
+    for (int p0 = tid; p0 < npieces; p0 += 2 * kThreads) {
         float2 acc[2][4];
         bool ok[2];
+        int row[2], jj[2];
         uint4 xx[2][R3 ? 9 : 1];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const int row = (tid >> 3) + 32 * (2 * it + u);
-            const int m = m0 + row;
-            ok[u] = m < a.M && cok;
+            const int pc = p0 + u * kThreads;
+            const bool inp = pc < npieces;
+            row[u] = inp ? pc / nvalid : 0;
+            jj[u] = inp ? pc - row[u] * nvalid : 0;
+            const int m = m0 + row[u];
+            ok[u] = inp && m < a.M;
 #pragma unroll
             for (int e = 0; e < 4; ++e) acc[u][e] = make_float2(0.f, 0.f);
             const int mm = ok[u] ? m : 0;
@@ -97,6 +97,7 @@ __device__ __forceinline__ void dw_chunk(const DwpwArgs &a, uint32_t sbase, int 
             const int p = rem / a.Q, q = rem - p * a.Q;
             const int h0 = p * a.sh - a.ph, w0 = q * a.sw - a.pw;
             const int nh = n * a.H;
+            const uint4 *xj = xv + cvec0 + jj[u];
             if constexpr (R3) {
 #pragma unroll
                 for (int r = 0; r < 3; ++r)
@@ -108,6 +109,7 @@ __device__ __forceinline__ void dw_chunk(const DwpwArgs &a, uint32_t sbase, int 
                                                : make_uint4(0u, 0u, 0u, 0u);
                     }
             } else if (ok[u]) {
+                const uint4 *wj = wv + cvec0 + jj[u];
 #pragma unroll 1
                 for (int r = 0; r < a.R; ++r) {
                     const int hi = h0 + r * a.dh;
@@ -125,16 +127,24 @@ __device__ __forceinline__ void dw_chunk(const DwpwArgs &a, uint32_t sbase, int 
         if constexpr (R3) {
 #pragma unroll
             for (int i = 0; i < 9; ++i) {
-                const uint4 wq = cok ? __ldg(wj + (size_t)i * cv) : make_uint4(0u, 0u, 0u, 0u);
-                mac8<T>(acc[0], xx[0][i], wq);
-                mac8<T>(acc[1], xx[1][i], wq);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint4 wq = __ldg(wv + (size_t)i * cv + cvec0 + jj[u]);
+                    mac8<T>(acc[u], xx[u][i], wq);
+                }
             }
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const int row = (tid >> 3) + 32 * (2 * it + u);
+            if (p0 + u * kThreads >= npieces) break;
             uint32_t o[4] = {0u, 0u, 0u, 0u};
             if (ok[u]) {
+                float2 bf[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                if (bv) {
+                    const uint4 b4 = __ldg(bv + cvec0 + jj[u]);
+                    bf[0] = up2(b4.x, (T *)nullptr); bf[1] = up2(b4.y, (T *)nullptr);
+                    bf[2] = up2(b4.z, (T *)nullptr); bf[3] = up2(b4.w, (T *)nullptr);
+                }
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     float v0 = acc[u][e].x, v1 = acc[u][e].y;
@@ -143,9 +153,17 @@ __device__ __forceinline__ void dw_chunk(const DwpwArgs &a, uint32_t sbase, int 
                     o[e] = pack2(v0, v1, (T *)nullptr);
                 }
             }
-            const uint32_t rb = sbase + (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u;
-            ptx::st_shared_v4(rb + ((uint32_t)(j ^ (row & 7)) << 4), o[0], o[1], o[2], o[3]);
+            const int rw = row[u];
+            const uint32_t rb = sbase + (uint32_t)(rw >> 3) * 1024u + (uint32_t)(rw & 7) * 128u;
+            ptx::st_shared_v4(rb + ((uint32_t)(jj[u] ^ (rw & 7)) << 4), o[0], o[1], o[2], o[3]);
         }
+    }
+    // the chunk's padded vectors (channels >= C): zeros
+    const int npad = 8 - nvalid;
+    for (int q = tid; q < kRows * npad; q += kThreads) {
+        const int rw = q / npad, jp = nvalid + (q - (q / npad) * npad);
+        const uint32_t rb = sbase + (uint32_t)(rw >> 3) * 1024u + (uint32_t)(rw & 7) * 128u;
+        ptx::st_shared_v4(rb + ((uint32_t)(jp ^ (rw & 7)) << 4), 0u, 0u, 0u, 0u);
     }
 }
 
