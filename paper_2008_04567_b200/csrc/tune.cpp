@@ -439,7 +439,13 @@ static wpk_status ga_search(TuneCtx &t) {
     Rng rng(o.seed, 0);
     for (int i = 0; i < popsize; ++i) {                      // Step1
         Config c;
-        if (!sample_valid(t, rng, &c)) return fail(WPK_ERR_EXHAUSTED, "GA Step1: no valid config sampled");
+        if (!sample_valid(t, rng, &c)) {
+            // a sparse space (e.g. a fused depthwise+pointwise plan with K_out = 320): the rejection
+            // sampler (10^4 draws) found nothing -- fall back to the expert template
+            // when there is one (reading "sparse spaces" in DESIGN.md)
+            if (!t.has_default) return fail(WPK_ERR_EXHAUSTED, "GA Step1: no valid config sampled");
+            c = t.default_cfg;
+        }
         pop.push_back(c);
     }
     // The expert template default replaces the first random individual, so a search
@@ -509,7 +515,10 @@ static wpk_status ga_search(TuneCtx &t) {
                     }
                 if (t.valid(c)) { child = c; got = true; }
             }
-            if (!got && !sample_valid(t, r, &child)) return fail(WPK_ERR_EXHAUSTED, "GA: no valid child");
+            if (!got && !sample_valid(t, r, &child)) {
+                if (!t.has_default) return fail(WPK_ERR_EXHAUSTED, "GA: no valid child");
+                child = t.default_cfg;   // sparse space: the expert template (memoised, costs no budget again)
+            }
             nxt.push_back(child);
         }
         pop.swap(nxt);

@@ -194,3 +194,16 @@ def test_dwpw_one_tile_kernel_split_k(splits):
             assert_bit_exact(y, ref)
         else:
             assert rel_error("bf16", y, ref) <= TOL["bf16"]
+
+
+def test_dwpw_tune_sparse_space_k320():
+    """K_out = 320 leaves only a handful of valid fused configs in the 7-gene space: the GA's rejection
+    sampler falls back to the expert-template default instead of failing (reading "sparse spaces"),
+    and the tuned plan is bit-exact."""
+    case = ("k320", 2, 960, 7, 7, 320, 1, 1, 1)
+    x, w_dw, b_dw, w_pw, b_pw, conv = _inputs(case, "bf16", "int", seed=111)
+    plan = _plan(case, "bf16")
+    res = plan.tune("ga", 16, seed=5)
+    assert res.measured >= 1 and res.best_us < float("inf")
+    assert_bit_exact(_run(plan, x, w_dw, b_dw, w_pw, b_pw),
+                     _oracle_chain(x, w_dw, b_dw, w_pw, b_pw, conv, torch.bfloat16))
